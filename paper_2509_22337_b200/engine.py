@@ -1,0 +1,408 @@
+"""Inference engine: the reference's ``hornbp.engine`` API on the B200 executor.
+
+``run(graph, schedule, options, workers)`` keeps the reference signature and
+result type (engine.py:531-594). Underneath, a graph is laid out on the device
+once (``hbp_graph_create``), a schedule becomes a device-resident level
+program once (``hbp_plan_create``), and every ``run`` is a single persistent
+kernel launch that iterates to convergence on the device
+(``csrc/engine.cu``). Both are cached per (graph, schedule) object, the
+reference's "compile once, run many" contract (storage.py:31-34).
+
+The single-pass functions (``update_vtof_batch``, ``update_ftov_batch``,
+``update_{and,or}_{body,head}``, ``compute_marginals``,
+``closed_form_message``) operate on a host ``MessageStore`` like the
+reference; each call ships the store to the device, runs one pass of the
+same message kernels, and scatters the results back.
+
+There is no CPU fallback: without the native library the package fails to
+import the engine, and without a GPU every device call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+import weakref
+from collections import OrderedDict
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from .graph import EdgeId, Factor, FactorGraph, FactorKind, KIND_OR
+from .schedule import Schedule
+from .storage import MessageStore, StorageError, initialize
+
+MIN_MESSAGE_SUM = 1e-300
+
+_native.lib()  # fail loudly at import if the engine library is missing
+
+
+class UnderflowError(RuntimeError):
+    """A message or marginal degenerated to total mass zero
+    (usually contradictory evidence on connected variables)."""
+
+
+class OpCounter:
+    """Counts elementwise multiplications executed by the message kernels."""
+
+    __slots__ = ("count",)
+
+    def __init__(self):
+        self.count = 0
+
+    def add(self, n: int) -> None:
+        self.count += int(n)
+
+
+@dataclass
+class EngineOptions:
+    max_iterations: int = 1000
+    tolerance: float = 1e-9
+    normalize_messages: bool = True
+    time_limit: Optional[float] = None
+    record_history: bool = False
+
+    def validate(self) -> None:
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be at least 1")
+        if self.tolerance < 0:
+            raise ValueError("tolerance must be nonnegative")
+        if self.time_limit is not None and self.time_limit <= 0:
+            raise ValueError("time_limit must be positive")
+
+
+@dataclass
+class InferenceResult:
+    marginals: np.ndarray  # (num_variables, 2): P(X=0), P(X=1)
+    converged: bool
+    iterations: int
+    last_delta: float
+    deltas: list[float] = field(default_factory=list)
+    history: Optional[list[np.ndarray]] = None
+    # additions (not in the reference): device time of the iteration loop and
+    # the bench numerator sum |s_i| + |t_i| (cli.py:337-339)
+    device_ms: Optional[float] = None
+    updates_per_iteration: Optional[int] = None
+
+
+# ---- device handles ----------------------------------------------------------------------
+
+_device_index = int(os.environ.get("HBP_DEVICE", "0"))
+_cache_lock = threading.Lock()
+_GRAPHS: "OrderedDict[int, tuple[weakref.ref, _DeviceGraph]]" = OrderedDict()
+_MAX_CACHED_GRAPHS = 6
+
+
+def set_device(index: int) -> None:
+    """CUDA device used for new device graphs (one process per GPU)."""
+    global _device_index
+    _device_index = int(index)
+
+
+def get_device() -> int:
+    return _device_index
+
+
+def _raise_status(status: int, what: str, result: Optional[_native.Result] = None,
+                  graph: Optional[FactorGraph] = None):
+    msg = _native.last_error()
+    if status == _native.HBP_EUNDERFLOW and result is not None:
+        kind = result.underflow_kind
+        idx = int(result.underflow_index)
+        if kind == 1:
+            raise UnderflowError(f"variable-to-factor message degenerated to zero mass at {idx} "
+                                 "(contradictory evidence?)")
+        if kind == 2:
+            pos = idx
+            if graph is not None:
+                rp, ved = graph._var_csr()
+                inv = np.empty(len(ved), dtype=np.int64)
+                inv[ved] = np.arange(len(ved))
+                pos = int(inv[idx])
+            raise UnderflowError(f"factor-to-variable message degenerated to zero mass at {pos} "
+                                 "(contradictory evidence?)")
+        raise UnderflowError(f"marginal of variable {idx} degenerated to zero mass "
+                             "(contradictory evidence?)")
+    if status in (_native.HBP_EINVAL, _native.HBP_ECYCLE):
+        raise ValueError(f"{what}: {msg}")
+    if status == _native.HBP_ENOMEM:
+        raise MemoryError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+class _Plan:
+    def __init__(self, dg: "_DeviceGraph", arrays):
+        s_off, s_e, t_off, t_e = arrays
+        self.dg = dg
+        self.updates = int(len(s_e) + len(t_e))
+        self.num_batches = len(s_off) - 1
+        h = C.c_void_p()
+        st = _native.lib().hbp_plan_create(
+            dg.handle, len(s_off) - 1, _native.ptr(np.ascontiguousarray(s_off), C.c_int64),
+            _native.ptr(np.ascontiguousarray(s_e, dtype=np.int32), C.c_int32),
+            _native.ptr(np.ascontiguousarray(t_off), C.c_int64),
+            _native.ptr(np.ascontiguousarray(t_e, dtype=np.int32), C.c_int32), C.byref(h))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_plan_create")
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _native.lib().hbp_plan_destroy(h)
+            self.handle = None
+
+    def options(self, options: EngineOptions) -> _native.Options:
+        return _native.Options(int(options.max_iterations), int(bool(options.normalize_messages)),
+                               int(bool(options.record_history)), 0, float(options.tolerance),
+                               float(options.time_limit) if options.time_limit else 0.0)
+
+    def run(self, options: EngineOptions, graph: FactorGraph) -> InferenceResult:
+        V = self.dg.num_variables
+        opt = self.options(options)
+        marg = np.empty((V, 2), dtype=np.float64)
+        deltas = np.empty(options.max_iterations, dtype=np.float64)
+        hist = (np.empty((options.max_iterations, V, 2), dtype=np.float64)
+                if options.record_history else None)
+        res = _native.Result()
+        st = _native.lib().hbp_run(self.handle, C.byref(opt), _native.ptr(marg, C.c_double),
+                                   _native.ptr(deltas, C.c_double),
+                                   None if hist is None else _native.ptr(hist, C.c_double),
+                                   C.byref(res))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_run", res, graph)
+        n = res.iterations
+        return InferenceResult(
+            marginals=marg, converged=bool(res.converged), iterations=n,
+            last_delta=float(res.last_delta), deltas=deltas[:n].tolist(),
+            history=None if hist is None else [hist[i].copy() for i in range(n)],
+            device_ms=float(res.device_ms), updates_per_iteration=self.updates)
+
+
+class _DeviceGraph:
+    """Device layout of one FactorGraph plus its compiled plans."""
+
+    def __init__(self, graph: FactorGraph, device: int):
+        self.arrays = _native.GraphArrays(graph)
+        self.num_variables = graph.num_variables
+        self.num_edges = graph.num_edges
+        self.device = device
+        h = C.c_void_p()
+        st = _native.lib().hbp_graph_create(C.byref(self.arrays.desc), device, C.byref(h))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_graph_create")
+        self.handle = h
+        self._plans: "OrderedDict[int, tuple[weakref.ref, _Plan]]" = OrderedDict()
+
+    def plan(self, schedule: Schedule, graph: FactorGraph) -> _Plan:
+        key = id(schedule)
+        hit = self._plans.get(key)
+        if hit is not None and hit[0]() is schedule:
+            self._plans.move_to_end(key)
+            return hit[1]
+        p = _Plan(self, schedule.arrays(graph))
+        self._plans[key] = (weakref.ref(schedule), p)
+        while len(self._plans) > 8:
+            self._plans.popitem(last=False)
+        return p
+
+    def __del__(self):
+        self._plans = OrderedDict()
+        h = getattr(self, "handle", None)
+        if h:
+            _native.lib().hbp_graph_destroy(h)
+            self.handle = None
+
+
+def device_graph(graph: FactorGraph) -> _DeviceGraph:
+    """Cached device layout for ``graph`` on the current device."""
+    key = id(graph)
+    with _cache_lock:
+        hit = _GRAPHS.get(key)
+        if hit is not None and hit[0]() is graph and hit[1].device == _device_index:
+            _GRAPHS.move_to_end(key)
+            return hit[1]
+    if graph.num_edges == 0:
+        raise StorageError("graph has no edges")
+    dg = _DeviceGraph(graph, _device_index)
+    with _cache_lock:
+        _GRAPHS[key] = (weakref.ref(graph, lambda _r, k=key: _GRAPHS.pop(k, None)), dg)
+        while len(_GRAPHS) > _MAX_CACHED_GRAPHS:
+            _GRAPHS.popitem(last=False)
+    return dg
+
+
+def clear_device_cache() -> None:
+    with _cache_lock:
+        _GRAPHS.clear()
+
+
+def _resolve_workers(workers: int) -> int:
+    """``workers`` is accepted for signature compatibility; results never
+    depend on it (engine.py:28) and the device ignores it."""
+    if workers < 0:
+        raise ValueError("workers must be nonnegative")
+    return workers or (os.cpu_count() or 1)
+
+
+# ---- run ----------------------------------------------------------------------------------
+
+def run(graph: FactorGraph, schedule: Schedule, options: Optional[EngineOptions] = None,
+        workers: int = 1) -> InferenceResult:
+    """Iterate the schedule until marginals stop moving or budgets run out
+    (engine.py:531-594): per iteration every batch refreshes its
+    variable-to-factor then its factor-to-variable messages; converged iff
+    max |dP1| < tolerance after an iteration."""
+    options = options or EngineOptions()
+    options.validate()
+    _resolve_workers(workers)
+    dg = device_graph(graph)
+    return dg.plan(schedule, graph).run(options, graph)
+
+
+# ---- single-pass API on a host store ------------------------------------------------------
+
+def _store_pass(store: MessageStore, direction: int, targets: np.ndarray, normalize: bool) -> None:
+    dg = device_graph(store.graph)
+    t = np.ascontiguousarray(targets, dtype=np.int32)
+    for name in ("vtof0", "vtof1", "ftov0", "ftov1"):
+        arr = getattr(store, name)
+        if not (arr.flags.c_contiguous and arr.dtype == np.float64):
+            setattr(store, name, np.ascontiguousarray(arr, dtype=np.float64))
+    where = C.c_int64(-1)
+    st = _native.lib().hbp_pass(dg.handle, direction, len(t), _native.ptr(t, C.c_int32),
+                                int(bool(normalize)), _native.ptr(store.vtof0, C.c_double),
+                                _native.ptr(store.vtof1, C.c_double),
+                                _native.ptr(store.ftov0, C.c_double),
+                                _native.ptr(store.ftov1, C.c_double), C.byref(where))
+    if st == _native.HBP_EUNDERFLOW:
+        if direction == 0:
+            raise UnderflowError(f"variable-to-factor message degenerated to zero mass at "
+                                 f"{int(where.value)} (contradictory evidence?)")
+        raise UnderflowError(f"factor-to-variable message degenerated to zero mass at "
+                             f"{int(store.vtof_to_ftov[where.value])} (contradictory evidence?)")
+    if st != _native.HBP_OK:
+        _raise_status(st, "hbp_pass")
+
+
+def _count_vtof(store: MessageStore, idx: np.ndarray, counter: Optional[OpCounter]) -> None:
+    if counter is not None:
+        d = store.av_end[idx] - store.av_start[idx]
+        counter.add(int((2 * np.maximum(d - 1, 0)).sum()))
+
+
+def _count_ftov(store: MessageStore, idx: np.ndarray, counter: Optional[OpCounter]) -> None:
+    """Multiplies the device kernel performs per target (ft_one in engine.cu):
+    head target 2(d-1) + 3, body target 2 (blend) + 2(d-2) + 1."""
+    if counter is not None:
+        f = idx  # canonical
+        ft = store.vtof_to_ftov[f]
+        d = store.af_end[ft] - store.af_start[ft]
+        head = store.af_head[ft]
+        n = np.where(head, 2 * (d - 1) + 3, 2 + 2 * (d - 2) + 1)
+        counter.add(int(n.sum()))
+
+
+def update_vtof_batch(store: MessageStore, edges: Sequence[EdgeId], normalize: bool = True,
+                      workers: int = 1, counter: Optional[OpCounter] = None) -> None:
+    """Recompute the named variable-to-factor messages (engine.py:413-428)."""
+    if not len(edges):
+        return
+    idx = store.vtof_indices(list(edges))
+    _count_vtof(store, idx, counter)
+    _store_pass(store, 0, idx, normalize)
+
+
+def update_ftov_batch(store: MessageStore, edges: Sequence[EdgeId], normalize: bool = True,
+                      workers: int = 1, counter: Optional[OpCounter] = None) -> None:
+    """Recompute the named factor-to-variable messages (engine.py:431-446);
+    the device groups them by (kind, head/body, degree) itself."""
+    if not len(edges):
+        return
+    idx = store.vtof_indices(list(edges))
+    _count_ftov(store, idx, counter)
+    _store_pass(store, 1, idx, normalize)
+
+
+def split_ftov_batch(graph: FactorGraph, batch: Sequence[EdgeId]):
+    """(AND body, AND head, OR body, OR head) routing of a batch (engine.py:357-377)."""
+    groups: tuple[list, list, list, list] = ([], [], [], [])
+    for edge in batch:
+        graph.check_edge(edge)
+        is_or = int(graph.kind[edge[0]]) == KIND_OR
+        groups[2 * is_or + (edge[1] == 0)].append(edge)
+    return groups
+
+
+def _routed_update(store, edges, kind: FactorKind, head: bool, normalize, counter) -> None:
+    if not len(edges):
+        return
+    graph = store.graph
+    want = 1 if kind is FactorKind.OR else 0
+    for edge in edges:
+        graph.check_edge(edge)
+        if int(graph.kind[edge[0]]) != want or (edge[1] == 0) != head:
+            where = "head" if head else "body"
+            raise ValueError(f"edge {EdgeId(*edge)} is not a {kind.value} {where} target")
+    update_ftov_batch(store, edges, normalize, counter=counter)
+
+
+def update_and_body(store, edges, normalize=True, workers=1, counter=None) -> None:
+    """Messages from AND factors toward body variables."""
+    _routed_update(store, edges, FactorKind.AND, False, normalize, counter)
+
+
+def update_and_head(store, edges, normalize=True, workers=1, counter=None) -> None:
+    """Messages from AND factors toward their head variable."""
+    _routed_update(store, edges, FactorKind.AND, True, normalize, counter)
+
+
+def update_or_body(store, edges, normalize=True, workers=1, counter=None) -> None:
+    """Messages from OR factors toward body variables."""
+    _routed_update(store, edges, FactorKind.OR, False, normalize, counter)
+
+
+def update_or_head(store, edges, normalize=True, workers=1, counter=None) -> None:
+    """Messages from OR factors toward their head variable."""
+    _routed_update(store, edges, FactorKind.OR, True, normalize, counter)
+
+
+def compute_marginals(store: MessageStore) -> np.ndarray:
+    """(P0, P1) per variable from the store's ftov buffers (engine.py:500-528)."""
+    dg = device_graph(store.graph)
+    out = np.empty((store.graph.num_variables, 2), dtype=np.float64)
+    f0 = np.ascontiguousarray(store.ftov0, dtype=np.float64)
+    f1 = np.ascontiguousarray(store.ftov1, dtype=np.float64)
+    bad = C.c_int64(-1)
+    st = _native.lib().hbp_marginals(dg.handle, _native.ptr(f0, C.c_double),
+                                     _native.ptr(f1, C.c_double), _native.ptr(out, C.c_double),
+                                     C.byref(bad))
+    if st == _native.HBP_EUNDERFLOW:
+        raise UnderflowError(f"marginal of variable {int(bad.value)} degenerated to zero mass "
+                             "(contradictory evidence?)")
+    if st != _native.HBP_OK:
+        _raise_status(st, "hbp_marginals")
+    return out
+
+
+def closed_form_message(kind: FactorKind, p1: float, p2: float,
+                        incoming: Sequence[Optional[tuple[float, float]]], target_slot: int,
+                        counter: Optional[OpCounter] = None) -> tuple[float, float]:
+    """One unnormalised factor-to-variable message through the device kernels
+    (engine.py:597-628); ``incoming`` is indexed by slot, head first."""
+    degree = len(incoming)
+    if not 0 <= target_slot < degree:
+        raise ValueError("target slot out of range")
+    factor = Factor(kind, 0, tuple(range(1, degree)), p1, p2)
+    store = initialize(FactorGraph(degree, [factor]))
+    for slot in range(degree):
+        if slot == target_slot:
+            continue
+        store.vtof0[slot], store.vtof1[slot] = incoming[slot]
+    edge = EdgeId(0, target_slot)
+    update_ftov_batch(store, [edge], normalize=False, counter=counter)
+    i = store.ftov_index(edge)
+    return float(store.ftov0[i]), float(store.ftov1[i])
