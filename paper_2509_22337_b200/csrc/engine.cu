@@ -12,19 +12,18 @@
 // time limit and underflow are decided on the device after phase 0; there
 // is no host round trip until the run ends.
 //
-// Work items: a "node" item computes every outgoing message of one
-// variable (or factor) from a single read of its row -- the O(d) form of the
-// reference's per-target O(d^2) gathers (_product_scan, engine.py:168-183;
-// _body_target_products :198-226) -- sharing prefix products across
-// targets, which is exact because a left-to-right product's prefixes are
-// the reference's own partial products. A "target" item is one edge
-// (partially covered rows in levelled schedules). Items are sorted by
-// (role, degree) on the host so warps are uniform in branch and trip count.
-#include <cooperative_groups.h>
+// Work decomposition: one thread per output message. Rows are laid out
+// degree-sorted (variables) and (kind, degree)-sorted (factors), so the 32
+// lanes of a warp read neighbouring rows of equal length: uniform trip count
+// and role, coalesced row loads shared through L1, and every lane multiplies
+// its row left to right in slot order (the reference's _product_scan order,
+// engine.py:168-183) -- bitwise-identical products. A 2-int slot word
+// {node, (degree << 16) | index-in-row} is the only per-message index.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -37,7 +36,8 @@ namespace hbp {
 
 using namespace dev;
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 1024;  // default block size (HBP_THREADS=512 selects the alternative)
+constexpr int kChunk = 8;       // row elements loaded per round trip
 
 struct Ctrl {
   unsigned int bar;  // grid barrier arrivals (monotonic)
@@ -49,28 +49,26 @@ struct Ctrl {
 
 struct KParams {
   // layout
-  const int *frow;
-  const double2 *fpar;
-  const int *vtof_twin;
-  const int *vrow;
-  const int *ftov_twin;
-  const int *vorig;
-  int V, F, f_or_begin;
-  int E;
+  const int2 *vslot;          // per ftov slot
+  const int2 *fslot;          // per vtof slot
+  const int *vtof_twin;       // vtof slot -> ftov slot
+  const unsigned *ftov_twin;  // ftov slot -> vtof slot | kUnaryBit
+  const double2 *fpar;        // per internal factor (p1, p2)
+  const int *vorig;           // internal variable -> original id
+  int V, F, E, f_or_begin;
   double2 *vtof, *ftov, *marg;
   double *prev;
   // plan
   const Phase *phases;
   int nphases;
-  const int *vnode, *fnode;
-  const int4 *vt, *ft;
+  const int *items;
   // control
   Ctrl *ctrl;
   unsigned long long *delta_bits;  // [max_it + 2]
   int *uf_msg;                     // [max_it + 2] bit0 vtof, bit1 ftov
   int *uf_marg;                    // [max_it + 2]
   int *uf_mwhere;                  // [max_it + 2] smallest underflowing variable
-  unsigned long long *uf_where;    // [max_it + 2] (phase<<33 | kind<<32 | pos) or var
+  unsigned long long *uf_where;    // [max_it + 2] (phase<<33 | kind<<32 | slot)
   int *tflag;                      // [max_it + 2]
   double2 *hist;                   // [max_it][V] or null
   int max_it;
@@ -109,13 +107,13 @@ __device__ __forceinline__ void bar_wait(Ctrl *c, unsigned target) {
 // message output with normalisation + underflow flag (engine.py:155-165)
 
 __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
-                                            int it, int phase, int kind, int pos) {
+                                            int it, int phase, int kind, int slot) {
   if (P.normalize) {
     double t = add(a0, a1);
     if (t < kMinMessageSum) {
       atomicOr(&P.uf_msg[it], 1 << kind);
       atomicMin(&P.uf_where[it], ((unsigned long long)phase << 33) |
-                                     ((unsigned long long)kind << 32) | (unsigned)pos);
+                                     ((unsigned long long)kind << 32) | (unsigned)slot);
     }
     a0 = dvd(a0, t);
     a1 = dvd(a1, t);
@@ -127,7 +125,7 @@ __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, doub
 __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
                                              unsigned long long &dmax) {
   double t = add(q0, q1);
-  int orig = P.vorig[v];
+  const int orig = P.vorig[v];
   if (t < kMinMessageSum) {
     atomicOr(&P.uf_marg[it - 1], 1);
     atomicMin(&P.uf_mwhere[it - 1], orig);
@@ -136,222 +134,179 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
   double p1 = sub(1.0, p0);
   double d = fabs(sub(p1, P.prev[v]));
   unsigned long long bits = (unsigned long long)__double_as_longlong(d);
-  dmax = bits > dmax ? bits : dmax;
+  dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
   P.prev[v] = p1;
   P.marg[orig] = make_double2(p0, p1);
   if (P.hist) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
 }
 
 // --------------------------------------------------------------------------------------
-// variable node: marginal and/or every non-unary outgoing vtof message
+// variable side, one ftov slot q: the vtof message of the same edge (product of
+// the row without q, engine.py:186-195) and, at a row start, the marginal
+// (full row product). write: 1 = yes, 0 = no, -1 = unless the edge's factor
+// is unary (PARALL range mode).
 
+// rows longer than kChunk (rare): same left-to-right products, chunked loads
+__device__ __noinline__ void v_row_long(const KParams &P, int r, int d, int j, bool marg,
+                                        double &a0, double &a1, double &q0, double &q1) {
+  for (int base = 0; base < d; base += 4) {
+    double2 m[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] = base + k < d ? P.ftov[r + base + k] : make_double2(1.0, 1.0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + k < d) {
+        if (base + k != j) {
+          a0 = mul(a0, m[k].x);
+          a1 = mul(a1, m[k].y);
+        }
+        if (marg) {
+          q0 = mul(q0, m[k].x);
+          q1 = mul(q1, m[k].y);
+        }
+      }
+    }
+  }
+}
+
+// fixed-length row: loads issued together, left-to-right products
 template <int D>
-__device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool do_marg,
-                                            bool do_vtof, int it, int phase,
-                                            unsigned long long &dmax) {
-  double x0[D], x1[D];
-  int tw[D];
+__device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg, double &a0,
+                                      double &a1, double &q0, double &q1) {
+  double2 m[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
-    double2 m = P.ftov[r + i];
-    x0[i] = m.x;
-    x1[i] = m.y;
-  }
-  if (do_vtof) {
+  for (int k = 0; k < D; ++k) m[k] = P.ftov[r + k];
 #pragma unroll
-    for (int i = 0; i < D; ++i) tw[i] = P.ftov_twin[r + i];
-  }
-  // a = left-to-right prefix product x[0] * ... * x[j-1] (reference acc)
-  double a0 = 1.0, a1 = 1.0;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    if (do_vtof && tw[j] >= 0) {
-      double b0 = a0, b1 = a1;
-#pragma unroll
-      for (int i = j + 1; i < D; ++i) {
-        b0 = mul(b0, x0[i]);
-        b1 = mul(b1, x1[i]);
-      }
-      put_message(P, P.vtof + tw[j], b0, b1, it, phase, 0, tw[j]);
+  for (int k = 0; k < D; ++k) {
+    if (k != j) {  // excluded slot: the reference multiplies by 1.0
+      a0 = mul(a0, m[k].x);
+      a1 = mul(a1, m[k].y);
     }
-    a0 = mul(a0, x0[j]);
-    a1 = mul(a1, x1[j]);
-  }
-  if (do_marg) put_marginal(P, v, a0, a1, it, dmax);
-}
-
-__device__ __noinline__ void vnode_generic(const KParams &P, int v, int r, int d, bool do_marg,
-                                           bool do_vtof, int it, int phase,
-                                           unsigned long long &dmax) {
-  if (do_vtof) {
-    for (int j = 0; j < d; ++j) {
-      int tw = P.ftov_twin[r + j];
-      if (tw < 0) continue;
-      double b0 = 1.0, b1 = 1.0;
-      for (int i = 0; i < d; ++i) {
-        if (i == j) continue;
-        double2 m = P.ftov[r + i];
-        b0 = mul(b0, m.x);
-        b1 = mul(b1, m.y);
-      }
-      put_message(P, P.vtof + tw, b0, b1, it, phase, 0, tw);
+    if (marg) {
+      q0 = mul(q0, m[k].x);
+      q1 = mul(q1, m[k].y);
     }
-  }
-  if (do_marg) {
-    double q0 = 1.0, q1 = 1.0;
-    for (int i = 0; i < d; ++i) {
-      double2 m = P.ftov[r + i];
-      q0 = mul(q0, m.x);
-      q1 = mul(q1, m.y);
-    }
-    put_marginal(P, v, q0, q1, it, dmax);
   }
 }
 
-__device__ __forceinline__ void vnode(const KParams &P, int v, bool do_marg, bool do_vtof, int it,
-                                      int phase, unsigned long long &dmax) {
-  const int r = P.vrow[v];
-  const int d = P.vrow[v + 1] - r;
+__device__ __forceinline__ void v_item(const KParams &P, int q, int write, bool want_marg, int it,
+                                       int phase, unsigned long long &dmax) {
+  const int2 w = P.vslot[q];
+  const unsigned tw = P.ftov_twin[q];
+  const int d = w.y >> 16, j = w.y & 0xffff;
+  const bool marg = want_marg && j == 0;
+  const bool wr = write > 0 || (write < 0 && !(tw & kUnaryBit));
+  if (!wr && !marg) return;
+  const int r = q - j;
+  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
   switch (d) {
-    case 1: vnode_fixed<1>(P, v, r, do_marg, do_vtof, it, phase, dmax); break;
-    case 2: vnode_fixed<2>(P, v, r, do_marg, do_vtof, it, phase, dmax); break;
-    case 3: vnode_fixed<3>(P, v, r, do_marg, do_vtof, it, phase, dmax); break;
-    case 4: vnode_fixed<4>(P, v, r, do_marg, do_vtof, it, phase, dmax); break;
-    default: vnode_generic(P, v, r, d, do_marg, do_vtof, it, phase, dmax); break;
+    case 1: v_row<1>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 2: v_row<2>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 3: v_row<3>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 4: v_row<4>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 5: v_row<5>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 6: v_row<6>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 7: v_row<7>(P, r, j, marg, a0, a1, q0, q1); break;
+    case 8: v_row<8>(P, r, j, marg, a0, a1, q0, q1); break;
+    default: v_row_long(P, r, d, j, marg, a0, a1, q0, q1); break;
   }
-}
-
-// single vtof target: row [r, r+d) minus slot x (engine.py:186-195)
-__device__ __forceinline__ void vt_target(const KParams &P, int4 t, int it, int phase) {
-  double b0 = 1.0, b1 = 1.0;
-  for (int i = 0; i < t.z; ++i) {
-    if (i == t.w) continue;
-    double2 m = P.ftov[t.y + i];
-    b0 = mul(b0, m.x);
-    b1 = mul(b1, m.y);
+  if (wr) {
+    const int out = (int)(tw & ~kUnaryBit);
+    put_message(P, P.vtof + out, a0, a1, it, phase, 0, out);
   }
-  put_message(P, P.vtof + t.x, b0, b1, it, phase, 0, t.x);
+  if (marg) put_marginal(P, w.x, q0, q1, it, dmax);
 }
 
 // --------------------------------------------------------------------------------------
-// factor node: every outgoing ftov message of one factor
+// factor side, one vtof slot p: the ftov message of the same edge.
+// Head target (index 0): products over body slots of (m0 + m1) and of
+// m1 (AND) / m0 (OR) -- engine.py:229-248. Body target: the head slot
+// contributes blend = (1-c) m0 + c m1 and (m0 - m1) -- engine.py:198-226.
+
+template <int KIND>
+__device__ __noinline__ void f_row_long(const KParams &P, int r, int d, int j, double2 pp,
+                                        double &b1, double &b2) {
+  for (int base = 0; base < d; base += 4) {
+    double2 m[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] = base + k < d ? P.vtof[r + base + k] : make_double2(1.0, 1.0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + k;
+      if (i < d && i != j) {
+        double f1, f2;
+        if (i == 0) {
+          head_slot_terms<KIND>(pp.x, pp.y, m[k].x, m[k].y, f1, f2);
+        } else {
+          f1 = add(m[k].x, m[k].y);
+          f2 = KIND == 0 ? m[k].y : m[k].x;
+        }
+        b1 = mul(b1, f1);
+        b2 = mul(b2, f2);
+      }
+    }
+  }
+}
 
 template <int D, int KIND>
-__device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int it, int phase) {
-  const double2 pp = P.fpar[f];
-  const double p1 = pp.x, p2 = pp.y;
-  double m0[D], m1[D];
-  int tw[D];
+__device__ __forceinline__ void f_row(const KParams &P, int r, int j, double2 pp, double &b1,
+                                      double &b2) {
+  double2 m[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
-    double2 m = P.vtof[r + i];
-    m0[i] = m.x;
-    m1[i] = m.y;
-    tw[i] = P.vtof_twin[r + i];
-  }
-  // s_i = m0 + m1 and tail_i = m1 (AND) / m0 (OR) for body slots
-  double s[D];
+  for (int k = 0; k < D; ++k) m[k] = P.vtof[r + k];
 #pragma unroll
-  for (int i = 1; i < D; ++i) s[i] = add(m0[i], m1[i]);
-  {  // head target: products over body slots 1..D-1
-    double h1 = 1.0, h2 = 1.0;
-#pragma unroll
-    for (int i = 1; i < D; ++i) {
-      h1 = mul(h1, s[i]);
-      h2 = mul(h2, KIND == 0 ? m1[i] : m0[i]);
-    }
-    double o0, o1;
-    head_message<KIND>(p1, p2, h1, h2, o0, o1);
-    put_message(P, P.ftov + tw[0], o0, o1, it, phase, 1, tw[0]);
-  }
-  if (D > 1) {
-    double blend, hd;
-    head_slot_terms<KIND>(p1, p2, m0[0], m1[0], blend, hd);
-    double a1 = blend, a2 = hd;  // prefix over slots 0..j-1 (1.0 * x == x)
-#pragma unroll
-    for (int j = 1; j < D; ++j) {
-      double b1 = a1, b2 = a2;
-#pragma unroll
-      for (int i = j + 1; i < D; ++i) {
-        b1 = mul(b1, s[i]);
-        b2 = mul(b2, KIND == 0 ? m1[i] : m0[i]);
+  for (int k = 0; k < D; ++k) {
+    if (k != j) {
+      double f1, f2;
+      if (k == 0) {
+        head_slot_terms<KIND>(pp.x, pp.y, m[k].x, m[k].y, f1, f2);
+      } else {
+        f1 = add(m[k].x, m[k].y);
+        f2 = KIND == 0 ? m[k].y : m[k].x;
       }
-      double o0, o1;
-      body_message<KIND>(p1, p2, b1, b2, o0, o1);
-      put_message(P, P.ftov + tw[j], o0, o1, it, phase, 1, tw[j]);
-      a1 = mul(a1, s[j]);
-      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
     }
   }
 }
 
-// one factor target with runtime degree; slot x excluded (head iff x == 0)
 template <int KIND>
-__device__ __forceinline__ void ft_one(const KParams &P, int r, int d, int x, double p1, double p2,
-                                       int out, int it, int phase) {
+__device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw, int it,
+                                         int phase) {
+  const int d = w.y >> 16, j = w.y & 0xffff;
+  const int r = p - j;
+  const double2 pp = P.fpar[w.x];
+  double b1 = 1.0, b2 = 1.0;
+  switch (d) {
+    case 1: break;  // prior / evidence: empty products
+    case 2: f_row<2, KIND>(P, r, j, pp, b1, b2); break;
+    case 3: f_row<3, KIND>(P, r, j, pp, b1, b2); break;
+    case 4: f_row<4, KIND>(P, r, j, pp, b1, b2); break;
+    case 5: f_row<5, KIND>(P, r, j, pp, b1, b2); break;
+    case 6: f_row<6, KIND>(P, r, j, pp, b1, b2); break;
+    case 7: f_row<7, KIND>(P, r, j, pp, b1, b2); break;
+    case 8: f_row<8, KIND>(P, r, j, pp, b1, b2); break;
+    default: f_row_long<KIND>(P, r, d, j, pp, b1, b2); break;
+  }
   double o0, o1;
-  if (x == 0) {
-    double h1 = 1.0, h2 = 1.0;
-    for (int i = 1; i < d; ++i) {
-      double2 m = P.vtof[r + i];
-      h1 = mul(h1, add(m.x, m.y));
-      h2 = mul(h2, KIND == 0 ? m.y : m.x);
-    }
-    head_message<KIND>(p1, p2, h1, h2, o0, o1);
-  } else {
-    double2 h = P.vtof[r];
-    double b1, b2;
-    head_slot_terms<KIND>(p1, p2, h.x, h.y, b1, b2);
-    for (int i = 1; i < d; ++i) {
-      if (i == x) continue;
-      double2 m = P.vtof[r + i];
-      b1 = mul(b1, add(m.x, m.y));
-      b2 = mul(b2, KIND == 0 ? m.y : m.x);
-    }
-    body_message<KIND>(p1, p2, b1, b2, o0, o1);
-  }
-  put_message(P, P.ftov + out, o0, o1, it, phase, 1, out);
-}
-
-template <int KIND>
-__device__ __noinline__ void fnode_generic(const KParams &P, int f, int r, int d, int it,
-                                           int phase) {
-  const double2 pp = P.fpar[f];
-  for (int x = 0; x < d; ++x) ft_one<KIND>(P, r, d, x, pp.x, pp.y, P.vtof_twin[r + x], it, phase);
-}
-
-__device__ __forceinline__ void fnode(const KParams &P, int f, int it, int phase) {
-  const int r = P.frow[f];
-  const int d = P.frow[f + 1] - r;
-  if (f < P.f_or_begin) {
-    switch (d) {
-      case 1: fnode_fixed<1, 0>(P, f, r, it, phase); break;
-      case 2: fnode_fixed<2, 0>(P, f, r, it, phase); break;
-      case 3: fnode_fixed<3, 0>(P, f, r, it, phase); break;
-      case 4: fnode_fixed<4, 0>(P, f, r, it, phase); break;
-      default: fnode_generic<0>(P, f, r, d, it, phase); break;
-    }
-  } else {
-    switch (d) {
-      case 2: fnode_fixed<2, 1>(P, f, r, it, phase); break;
-      case 3: fnode_fixed<3, 1>(P, f, r, it, phase); break;
-      case 4: fnode_fixed<4, 1>(P, f, r, it, phase); break;
-      default: fnode_generic<1>(P, f, r, d, it, phase); break;
-    }
-  }
-}
-
-__device__ __forceinline__ void ft_target(const KParams &P, int4 t, int it, int phase) {
-  const int d = t.z & 0xffff, x = (unsigned)t.z >> 16;
-  const double2 pp = P.fpar[t.w];
-  if (t.w < P.f_or_begin)
-    ft_one<0>(P, t.y, d, x, pp.x, pp.y, t.x, it, phase);
+  if (j == 0)
+    head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
   else
-    ft_one<1>(P, t.y, d, x, pp.x, pp.y, t.x, it, phase);
+    body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+  put_message(P, P.ftov + tw, o0, o1, it, phase, 1, tw);
+}
+
+__device__ __forceinline__ void f_item(const KParams &P, int p, int it, int phase) {
+  const int2 w = P.fslot[p];
+  const int tw = P.vtof_twin[p];
+  if (w.x < P.f_or_begin)
+    f_item_k<0>(P, p, w, tw, it, phase);
+  else
+    f_item_k<1>(P, p, w, tw, it, phase);
 }
 
 // --------------------------------------------------------------------------------------
-// one phase over [0, nodes + targets) with grid- or CTA-stride
+// one phase over its slots, grid- or CTA-strided
 
 __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, int pidx, int it,
                                            bool do_marg, bool do_vtof,
@@ -365,42 +320,32 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     start = threadIdx.x;
     stride = blockDim.x;
   }
-  const int nn = ph.node_end - ph.node_begin;
-  const int total = nn + (ph.tgt_end - ph.tgt_begin);
+  const int n = ph.end - ph.begin;
   if (ph.type == 0) {
-    const bool marg = do_marg && (ph.node_flags & 1);
-    for (int i = start; i < total; i += stride) {
-      if (i < nn) {
-        int v;
-        bool vt;
-        if (ph.node_list) {
-          int item = P.vnode[ph.node_begin + i];
-          v = item & (kVtofBit - 1);
-          vt = (item & kVtofBit) != 0;
-        } else {
-          v = ph.node_begin + i;
-          vt = (ph.node_flags & 2) != 0;
-        }
-        vt = vt && do_vtof;
-        if (marg || vt) vnode(P, v, marg, vt, it, pidx, dmax);
-      } else if (do_vtof) {
-        vt_target(P, P.vt[ph.tgt_begin + i - nn], it, pidx);
+    const bool marg = do_marg && ph.marg;
+    for (int i = start; i < n; i += stride) {
+      int q, write;
+      if (ph.list) {
+        const int item = P.items[ph.begin + i];
+        q = item & (kWriteBit - 1);
+        write = (item & kWriteBit) ? 1 : 0;
+      } else {
+        q = ph.begin + i;
+        write = -1;
       }
+      if (!do_vtof) write = 0;
+      v_item(P, q, write, marg, it, pidx, dmax);
     }
   } else {
-    for (int i = start; i < total; i += stride) {
-      if (i < nn) {
-        int f = ph.node_list ? P.fnode[ph.node_begin + i] : ph.node_begin + i;
-        fnode(P, f, it, pidx);
-      } else {
-        ft_target(P, P.ft[ph.tgt_begin + i - nn], it, pidx);
-      }
+    for (int i = start; i < n; i += stride) {
+      const int p = ph.list ? P.items[ph.begin + i] : ph.begin + i;
+      f_item(P, p, it, pidx);
     }
   }
 }
 
 __device__ __forceinline__ unsigned long long block_max(unsigned long long v) {
-  __shared__ unsigned long long red[kThreads / 32];
+  __shared__ unsigned long long red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
@@ -426,7 +371,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) lbp_persistent(const __grid_constant__ KParams P) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
   const bool multi = gridDim.x > 1;
   unsigned expected = 0;  // arrivals every CTA has seen so far (same on all CTAs)
@@ -488,20 +434,20 @@ __global__ void __launch_bounds__(kThreads, 1) lbp_persistent(const __grid_const
     }
     // remaining phases of this iteration
     for (int p = 1; p < P.nphases; ++p) {
-      const Phase &ph = P.phases[p];
-      const Phase &prv = P.phases[p - 1];
-      if (p > 1) {  // transition prv -> ph (phase 0 -> 1 was the full barrier above)
+      const Phase ph = P.phases[p];
+      if (p > 1) {  // transition p-1 -> p (phase 0 -> 1 was the full barrier above)
+        const int prev_grid = P.phases[p - 1].grid;
         if (!multi) {
           __syncthreads();
-        } else if (prv.grid && ph.grid) {
+        } else if (prev_grid && ph.grid) {
           bar_arrive(C);
           expected += gridDim.x;
           bar_wait(C, expected);
-        } else if (prv.grid && !ph.grid) {
+        } else if (prev_grid && !ph.grid) {
           bar_arrive(C);
           expected += gridDim.x;
           if (blockIdx.x == 0) bar_wait(C, expected);
-        } else if (!prv.grid && !ph.grid) {
+        } else if (!prev_grid && !ph.grid) {
           if (blockIdx.x == 0) __syncthreads();
         } else {  // CTA 0 -> grid
           if (blockIdx.x == 0) bar_arrive(C);
@@ -514,10 +460,10 @@ __global__ void __launch_bounds__(kThreads, 1) lbp_persistent(const __grid_const
     }
     // transition last phase -> phase 0 of the next iteration (a grid phase)
     if (P.nphases > 1) {
-      const Phase &last = P.phases[P.nphases - 1];
+      const int last_grid = P.phases[P.nphases - 1].grid;
       if (!multi) {
         __syncthreads();
-      } else if (last.grid) {
+      } else if (last_grid) {
         bar_arrive(C);
         expected += gridDim.x;
         bar_wait(C, expected);
@@ -537,20 +483,19 @@ __global__ void __launch_bounds__(kThreads, 1) lbp_persistent(const __grid_const
 
 namespace hbp {
 
-__global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KParams P, int type, const int4 *items, int n) {
+// items: list-mode slot words (type 0: ftov slot | kWriteBit, or a row start
+// for a marginal; type 1: vtof slot)
+__global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KParams P, int type,
+                                                   int marg, const int *items, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (type == 0)
-    vt_target(P, items[i], 1, 0);
-  else
-    ft_target(P, items[i], 1, 0);
-}
-
-__global__ void __launch_bounds__(256) marginal_kernel(const __grid_constant__ KParams P) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= P.V) return;
+  const int item = items[i];
   unsigned long long unused = 0;
-  vnode(P, v, true, false, 2, 0, unused);
+  if (type == 0)
+    v_item(P, item & (kWriteBit - 1), (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1, 0,
+           unused);
+  else
+    f_item(P, item, 1, 0);
 }
 
 }  // namespace hbp
@@ -585,9 +530,11 @@ struct hbp_graph {
   hbp::HostLayout L;
   int device = 0;
   cudaStream_t stream = nullptr;
-  int num_sms = 0, coop_blocks = 0;
-  int *d_frow = nullptr, *d_vtof_twin = nullptr, *d_vrow = nullptr, *d_ftov_twin = nullptr,
-      *d_vorig = nullptr;
+  int num_sms = 0, coop_blocks = 0, threads = 1024;
+  const void *kernel = nullptr;
+  int *d_vtof_twin = nullptr, *d_vorig = nullptr;
+  unsigned *d_ftov_twin = nullptr;
+  int2 *d_vslot = nullptr, *d_fslot = nullptr;
   double2 *d_fpar = nullptr, *d_vtof = nullptr, *d_ftov = nullptr, *d_marg = nullptr;
   double *d_prev = nullptr;
   // control block sized for max_iterations
@@ -599,7 +546,7 @@ struct hbp_graph {
 
   ~hbp_graph() {
     cudaSetDevice(device);
-    for (void *p : {(void *)d_frow, (void *)d_vtof_twin, (void *)d_vrow, (void *)d_ftov_twin,
+    for (void *p : {(void *)d_vslot, (void *)d_vtof_twin, (void *)d_fslot, (void *)d_ftov_twin,
                     (void *)d_vorig, (void *)d_fpar, (void *)d_vtof, (void *)d_ftov,
                     (void *)d_marg, (void *)d_prev, d_ctrl, (void *)d_hist})
       if (p) cudaFree(p);
@@ -613,12 +560,11 @@ struct hbp_plan {
   hbp_graph *g = nullptr;
   hbp::PlanHost host;
   hbp::Phase *d_phases = nullptr;
-  int *d_vnode = nullptr, *d_fnode = nullptr;
-  int4 *d_vt = nullptr, *d_ft = nullptr;
+  int *d_items = nullptr;
   int grid = 1;
   ~hbp_plan() {
     cudaSetDevice(g->device);
-    for (void *p : {(void *)d_phases, (void *)d_vnode, (void *)d_fnode, (void *)d_vt, (void *)d_ft})
+    for (void *p : {(void *)d_phases, (void *)d_items})
       if (p) cudaFree(p);
   }
 };
@@ -654,10 +600,10 @@ size_t ctrl_bytes(size_t n) { return 256 + n * (8 + 8 + 4 + 4 + 4 + 4); }
 
 hbp::KParams base_params(hbp_graph *g) {
   hbp::KParams P{};
-  P.frow = g->d_frow;
+  P.vslot = g->d_vslot;
+  P.fslot = g->d_fslot;
   P.fpar = g->d_fpar;
   P.vtof_twin = g->d_vtof_twin;
-  P.vrow = g->d_vrow;
   P.ftov_twin = g->d_ftov_twin;
   P.vorig = g->d_vorig;
   P.V = g->L.V;
@@ -716,15 +662,23 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   HBP_CUDA(cudaEventCreate(&g->ev1));
   HBP_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
   int per_sm = 0;
-  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hbp::lbp_persistent,
-                                                         hbp::kThreads, 0));
+  {
+    const char *env = getenv("HBP_THREADS");
+    g->threads = (env && atoi(env) == 512) ? 512 : hbp::kThreads;
+    g->kernel = g->threads == 512 ? (const void *)hbp::lbp_persistent<512>
+                                  : (const void *)hbp::lbp_persistent<hbp::kThreads>;
+  }
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
   const hbp::HostLayout &L = g->L;
   cudaStream_t s = g->stream;
   std::vector<double2> fpar((size_t)L.F);
   for (int32_t i = 0; i < L.F; ++i) fpar[i] = make_double2(L.p1[L.fperm[i]], L.p2[L.fperm[i]]);
-  if ((st = upload(&g->d_frow, L.frow, s)) || (st = upload(&g->d_vtof_twin, L.vtof_twin, s)) ||
-      (st = upload(&g->d_vrow, L.vrow, s)) || (st = upload(&g->d_ftov_twin, L.ftov_twin, s)) ||
+  std::vector<int2> vslot((size_t)L.E), fslot((size_t)L.E);
+  std::memcpy(vslot.data(), L.vslot.data(), (size_t)L.E * 8);
+  std::memcpy(fslot.data(), L.fslot.data(), (size_t)L.E * 8);
+  if ((st = upload(&g->d_vslot, vslot, s)) || (st = upload(&g->d_vtof_twin, L.vtof_twin, s)) ||
+      (st = upload(&g->d_fslot, fslot, s)) || (st = upload(&g->d_ftov_twin, L.ftov_twin, s)) ||
       (st = upload(&g->d_vorig, L.vperm, s)) || (st = upload(&g->d_fpar, fpar, s)))
     return st;
   HBP_CUDA(cudaMalloc(&g->d_vtof, (size_t)L.E * sizeof(double2)));
@@ -768,19 +722,14 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   if (st != HBP_OK) return st;
   HBP_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
-  std::vector<int4> vt(p->host.vt.size() / 4), ft(p->host.ft.size() / 4);
-  if (!vt.empty()) std::memcpy(vt.data(), p->host.vt.data(), vt.size() * 16);
-  if (!ft.empty()) std::memcpy(ft.data(), p->host.ft.data(), ft.size() * 16);
-  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_vnode, p->host.vnode, s)) ||
-      (st = upload(&p->d_fnode, p->host.fnode, s)) || (st = upload(&p->d_vt, vt, s)) ||
-      (st = upload(&p->d_ft, ft, s)))
+  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)))
     return st;
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
   for (const auto &ph : p->host.phases)
-    if (ph.grid) big = std::max<int64_t>(big, (ph.node_end - ph.node_begin) + (ph.tgt_end - ph.tgt_begin));
-  int64_t want = (big + hbp::kThreads - 1) / hbp::kThreads;
-  if (big < 2 * hbp::kThreads) want = 1;
+    if (ph.grid) big = std::max<int64_t>(big, ph.end - ph.begin);
+  int64_t want = (big + g->threads - 1) / g->threads;
+  if (big < 2 * g->threads) want = 1;
   p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();
@@ -828,10 +777,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   hbp::KParams P = base_params(g);
   P.phases = p->d_phases;
   P.nphases = (int)p->host.phases.size();
-  P.vnode = p->d_vnode;
-  P.fnode = p->d_fnode;
-  P.vt = p->d_vt;
-  P.ft = p->d_ft;
+  P.items = p->d_items;
   P.ctrl = c.ctrl;
   P.delta_bits = c.delta_bits;
   P.uf_msg = c.uf_msg;
@@ -847,8 +793,8 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   if (opt->time_limit > 0 && P.time_limit_ns == 0) P.time_limit_ns = 1;
   void *args[] = {&P};
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
-  HBP_CUDA(cudaLaunchCooperativeKernel((void *)hbp::lbp_persistent, dim3(p->grid),
-                                       dim3(hbp::kThreads), args, 0, g->stream));
+  HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
+                                       g->stream));
   HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
   g_last_launches = 1;
   hbp::Ctrl hc;
@@ -950,22 +896,18 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
     int32_t e = L.ref_ftov[q];
     hf[L.canon2f[e]] = make_double2(ftov0[q], ftov1[q]);
   }
-  std::vector<int4> items((size_t)n);
-  for (int64_t i = 0; i < n; ++i) {
-    if (direction == 0)
-      hbp::make_vt_item(L, targets[i], (int32_t *)&items[i]);
-    else
-      hbp::make_ft_item(L, targets[i], (int32_t *)&items[i]);
-  }
+  std::vector<int32_t> items((size_t)n);
+  for (int64_t i = 0; i < n; ++i)
+    items[i] = direction == 0 ? (L.canon2f[targets[i]] | hbp::kWriteBit) : L.canon2v[targets[i]];
   hbp_status st = ensure_ctrl(g, 4);
   if (st) return st;
   if ((st = reset_ctrl(g, 4))) return st;
-  int4 *d_items = nullptr;
-  HBP_CUDA(cudaMalloc(&d_items, items.size() * 16));
+  int *d_items = nullptr;
+  HBP_CUDA(cudaMalloc(&d_items, items.size() * 4));
   cudaStream_t s = g->stream;
   HBP_CUDA(cudaMemcpyAsync(g->d_vtof, hv.data(), hv.size() * 16, cudaMemcpyHostToDevice, s));
   HBP_CUDA(cudaMemcpyAsync(g->d_ftov, hf.data(), hf.size() * 16, cudaMemcpyHostToDevice, s));
-  HBP_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * 16, cudaMemcpyHostToDevice, s));
+  HBP_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * 4, cudaMemcpyHostToDevice, s));
   CtrlView c = ctrl_view(g->d_ctrl, g->ctrl_cap);
   hbp::KParams P = base_params(g);
   P.normalize = normalize ? 1 : 0;
@@ -973,7 +915,8 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
   P.uf_where = c.uf_where;
   P.uf_marg = c.uf_marg;
   P.uf_mwhere = c.uf_mwhere;
-  hbp::pass_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, direction ? 1 : 0, d_items, (int)n);
+  hbp::pass_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, direction ? 1 : 0, 0, d_items,
+                                                                (int)n);
   g_last_launches = 1;
   cudaError_t le = cudaGetLastError();
   int uf = 0;
@@ -1036,9 +979,17 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
   P.uf_where = c.uf_where;
   P.uf_marg = c.uf_marg;
   P.uf_mwhere = c.uf_mwhere;
-  hbp::marginal_kernel<<<(unsigned)((L.V + 255) / 256), 256, 0, s>>>(P);
+  std::vector<int32_t> rows((size_t)L.V);
+  for (int32_t vi = 0; vi < L.V; ++vi) rows[vi] = L.vrow[vi];
+  int *d_rows = nullptr;
+  HBP_CUDA(cudaMalloc(&d_rows, rows.size() * 4 + 4));
+  HBP_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, s));
+  hbp::pass_kernel<<<(unsigned)((L.V + 255) / 256), 256, 0, s>>>(P, 0, 1, d_rows, L.V);
   g_last_launches = 1;
-  HBP_CUDA(cudaGetLastError());
+  cudaError_t le = cudaGetLastError();
+  cudaStreamSynchronize(s);
+  cudaFree(d_rows);
+  HBP_CUDA(le);
   int uf = 0, mw = 0;
   HBP_CUDA(cudaMemcpyAsync(&uf, c.uf_marg + 1, 4, cudaMemcpyDeviceToHost, s));
   HBP_CUDA(cudaMemcpyAsync(&mw, c.uf_mwhere + 1, 4, cudaMemcpyDeviceToHost, s));

@@ -25,22 +25,28 @@ hbp_status compile(const hbp_graph_desc &g, int64_t m, const int32_t *before,
                    int64_t *cycle_edge);
 
 // ---- device-side plan records --------------------------------------------------------
-// A phase is one data-parallel sweep between two barriers. Type 0 reads
-// factor-to-variable messages (variable side: vtof updates, marginals);
-// type 1 reads variable-to-factor messages (factor side: ftov updates).
-// Work = node items (whole variable / whole factor, all outgoing messages
-// at once) followed by target items (single edges).
+// A phase is one data-parallel sweep between two barriers. Type 0 is the
+// variable side (reads factor-to-variable messages; writes variable-to-factor
+// messages and, in phase 0, the marginals); type 1 is the factor side.
+// Work items are message SLOTS, one thread each: an ftov slot for type 0
+// (the thread writes the vtof message of the same edge), a vtof slot for
+// type 1 (it writes the ftov message of the same edge). Range-mode phases
+// cover every slot [begin, end); list-mode phases read slot ids from the
+// item array (levelled schedules).
 struct Phase {
-  int32_t type;        // 0 variable side, 1 factor side
-  int32_t grid;        // 1: whole grid; 0: CTA 0 only (small level)
-  int32_t node_list;   // 1: node ids come from the item list; 0: contiguous id range
-  int32_t node_flags;  // bit0: marginal (phase 0 only), bit1: vtof for range-mode nodes
-  int32_t node_begin, node_end;  // item-list range, or id range if node_list == 0
-  int32_t tgt_begin, tgt_end;    // target-item range
+  int32_t type;   // 0 variable side, 1 factor side
+  int32_t grid;   // 1: whole grid; 0: CTA 0 only (small level)
+  int32_t list;   // 1: slot ids come from the item list; 0: slots [begin, end)
+  int32_t marg;   // 1: row-start slots also produce the marginal (phase 0)
+  int32_t begin, end;
 };
 
-// Node item (variable side, list mode): internal variable id | kVtofBit.
-constexpr int32_t kVtofBit = 1 << 30;
+// List items: slot id | kWriteBit (type 0 only: also write the vtof message;
+// items without it exist only to produce a marginal).
+constexpr int32_t kWriteBit = 1 << 30;
+// ftov_twin high bit: the edge belongs to a unary factor, whose vtof message
+// is never a PARALL target (schedule.py:303-312 skips it).
+constexpr uint32_t kUnaryBit = 1u << 31;
 
 // ---- graph layout ----------------------------------------------------------------------
 // Internal order: factors sorted by (kind, degree), variables by degree
@@ -66,26 +72,21 @@ struct HostLayout {
   std::vector<int32_t> vtof2canon;   // inverse of canon2v
   std::vector<int32_t> ftov2canon;   // inverse of canon2f
   std::vector<int32_t> vtof_twin;    // internal vtof pos -> internal ftov pos
-  std::vector<int32_t> ftov_twin;    // internal ftov pos -> internal vtof pos (~pos if unary factor)
+  std::vector<uint32_t> ftov_twin;   // internal ftov pos -> internal vtof pos | kUnaryBit
+  std::vector<int32_t> vslot;        // per internal ftov pos: {internal var, (deg << 16) | index}
+  std::vector<int32_t> fslot;        // per internal vtof pos: {internal factor, (deg << 16) | index}
   std::vector<int32_t> edge_factor;  // canonical edge -> original factor
   std::vector<int32_t> ref_ftov;     // reference ftov position -> canonical edge (storage.py:61)
   std::vector<int32_t> nonunary;     // per original variable: # slots in non-unary factors
-  int32_t f_or_begin = 0;            // internal factors >= this are OR
+  int32_t f_or_begin = 0;  // internal factors >= this are OR (order: kind, degree)
   int32_t max_fdeg = 0, max_vdeg = 0;
 };
 
 hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L);
 
-// Target-item encodings (4 x int32):
-//   vtof target: {out vtof pos, ftov row start, row length, excluded index in row}
-//   ftov target: {out ftov pos, vtof row start, (excluded slot << 16) | degree, internal factor}
-void make_vt_item(const HostLayout &L, int32_t e, int32_t *q);
-void make_ft_item(const HostLayout &L, int32_t e, int32_t *q);
-
 struct PlanHost {
   std::vector<Phase> phases;
-  std::vector<int32_t> vnode, fnode;   // node item lists
-  std::vector<int32_t> vt, ft;         // target items, 4 int32 each
+  std::vector<int32_t> items;          // list-mode slot items (both sides)
   int64_t updates_per_iter = 0;        // sum |s_i| + |t_i|
   int32_t max_items = 0;               // largest phase (work items)
 };

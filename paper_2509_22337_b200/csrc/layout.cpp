@@ -1,6 +1,6 @@
 // Host-side builders: the device message layout (MessageStore, storage.py:36-94)
 // and the per-schedule level program (the pass compilation of engine.py:128-152,
-// :357-410, :500-507, recast as node/target work items).
+// :357-410, :500-507, recast as slot work lists).
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -22,7 +22,7 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     set_error("graph has no edges");
     return HBP_EINVAL;
   }
-  if (g.num_edges >= (int64_t)1 << 31) {
+  if (g.num_edges >= ((int64_t)1 << 30)) {
     set_error("graph has too many edges for the int32 device layout");
     return HBP_EINVAL;
   }
@@ -60,7 +60,8 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     }
   L.max_fdeg = maxdeg;
 
-  // factors: stable counting sort by (kind, degree)
+  // factors: stable counting sort by (kind, degree) -> warp-uniform role and
+  // trip count across consecutive slots
   const int32_t nkeys = 2 * (maxdeg + 1);
   std::vector<int64_t> bucket((size_t)nkeys + 1, 0);
   auto fkey = [&](int32_t f) {
@@ -86,11 +87,18 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   }
   L.edge_factor.resize(E);
   L.canon2v.resize(E);
-  for (int32_t f = 0; f < F; ++f)
+  L.fslot.resize(2 * E);
+  for (int32_t f = 0; f < F; ++f) {
+    const int32_t d = (int32_t)(L.rowptr[f + 1] - L.rowptr[f]);
     for (int64_t e = L.rowptr[f]; e < L.rowptr[f + 1]; ++e) {
+      const int32_t j = (int32_t)(e - L.rowptr[f]);
+      const int32_t p = L.frow[L.finv[f]] + j;
       L.edge_factor[e] = f;
-      L.canon2v[e] = L.frow[L.finv[f]] + (int32_t)(e - L.rowptr[f]);
+      L.canon2v[e] = p;
+      L.fslot[2 * (size_t)p] = L.finv[f];
+      L.fslot[2 * (size_t)p + 1] = (d << 16) | j;
     }
+  }
 
   // variables: stable counting sort by degree
   std::vector<int32_t> vdeg((size_t)V, 0);
@@ -102,6 +110,10 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   }
   int32_t maxv = 0;
   for (int32_t v = 0; v < V; ++v) maxv = std::max(maxv, vdeg[v]);
+  if (maxv > 65535) {
+    set_error("variable degree above 65535");
+    return HBP_EINVAL;
+  }
   L.max_vdeg = maxv;
   std::vector<int64_t> vb((size_t)maxv + 2, 0);
   for (int32_t v = 0; v < V; ++v) vb[vdeg[v] + 1]++;
@@ -119,13 +131,20 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   L.vrow.assign((size_t)V + 1, 0);
   for (int32_t i = 0; i < V; ++i) L.vrow[i + 1] = L.vrow[i] + vdeg[L.vperm[i]];
 
-  // ftov rows: canonical order within each variable == (factor, slot) order
+  // ftov rows: canonical order within each variable == (factor, slot) order,
+  // which is the reference's product order (storage.py:59-61)
   L.canon2f.resize(E);
+  L.vslot.resize(2 * E);
   {
     std::vector<int32_t> fill((size_t)V, 0);
     for (int64_t e = 0; e < E; ++e) {
-      int32_t v = L.edge_var[e];
-      L.canon2f[e] = L.vrow[L.vinv[v]] + fill[v]++;
+      const int32_t v = L.edge_var[e];
+      const int32_t vi = L.vinv[v];
+      const int32_t j = fill[v]++;
+      const int32_t q = L.vrow[vi] + j;
+      L.canon2f[e] = q;
+      L.vslot[2 * (size_t)q] = vi;
+      L.vslot[2 * (size_t)q + 1] = (vdeg[v] << 16) | j;
     }
   }
   // the reference's own ftov order: variables by id, rows in canonical order
@@ -146,34 +165,15 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     L.vtof_twin[L.canon2v[e]] = L.canon2f[e];
     int32_t f = L.edge_factor[e];
     bool unary = L.rowptr[f + 1] - L.rowptr[f] == 1;
-    L.ftov_twin[L.canon2f[e]] = unary ? ~L.canon2v[e] : L.canon2v[e];
+    L.ftov_twin[L.canon2f[e]] = (uint32_t)L.canon2v[e] | (unary ? kUnaryBit : 0u);
   }
   return HBP_OK;
-}
-
-void make_vt_item(const HostLayout &L, int32_t e, int32_t *q) {
-  const int32_t vi = L.vinv[L.edge_var[e]];
-  const int32_t row = L.vrow[vi];
-  q[0] = L.canon2v[e];
-  q[1] = row;
-  q[2] = L.vrow[vi + 1] - row;
-  q[3] = L.canon2f[e] - row;
-}
-
-void make_ft_item(const HostLayout &L, int32_t e, int32_t *q) {
-  const int32_t f = L.edge_factor[e];
-  const int32_t fi = L.finv[f];
-  const int32_t slot = (int32_t)(e - L.rowptr[f]);
-  q[0] = L.canon2f[e];
-  q[1] = L.frow[fi];
-  q[2] = (slot << 16) | (L.frow[fi + 1] - L.frow[fi]);
-  q[3] = fi;
 }
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
                       PlanHost &P) {
-  const int32_t V = L.V, F = L.F;
+  const int32_t V = L.V;
   const int64_t E = L.E;
   if (k < 0 || (k > 0 && (s_off[0] != 0 || t_off[0] != 0))) {
     set_error("bad batch offsets");
@@ -198,167 +198,101 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
     }
   P.updates_per_iter = ns + nt;
   P.phases.clear();
-  P.vnode.clear();
-  P.fnode.clear();
-  P.vt.clear();
-  P.ft.clear();
+  P.items.clear();
   P.max_items = 0;
 
   std::vector<int64_t> stamp((size_t)E, -1);
-  std::vector<int32_t> vcount((size_t)V, 0), fcount((size_t)F, 0);
-  std::vector<int32_t> touched;
-  std::vector<int32_t> items;
+  std::vector<int32_t> slots;
 
-  auto add_vt = [&](int32_t e, std::vector<int32_t> &tg) {
-    int32_t q[4];
-    make_vt_item(L, e, q);
-    tg.insert(tg.end(), q, q + 4);
-  };
-  auto add_ft = [&](int32_t e, std::vector<int32_t> &tg) {
-    int32_t q[4];
-    make_ft_item(L, e, q);
-    tg.insert(tg.end(), q, q + 4);
-  };
-  // sort target quads by key
-  auto sort_quads = [](std::vector<int32_t> &q, auto key) {
-    size_t n = q.size() / 4;
-    std::vector<int32_t> idx(n);
-    std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
-      return key(&q[4 * (size_t)a]) < key(&q[4 * (size_t)b]);
-    });
-    std::vector<int32_t> out(q.size());
-    for (size_t i = 0; i < n; ++i) std::memcpy(&out[4 * i], &q[4 * (size_t)idx[i]], 16);
-    q.swap(out);
+  // the non-unary slot set: what a PARALL variable-side phase writes
+  int64_t nonunary_total = 0;
+  for (int32_t v = 0; v < V; ++v) nonunary_total += L.nonunary[v];
+
+  auto push_phase = [&](Phase ph, int32_t n) {
+    ph.grid = n >= kCta0Threshold;
+    P.max_items = std::max(P.max_items, n);
+    P.phases.push_back(ph);
   };
 
   const int64_t levels = std::max<int64_t>(k, 1);
   for (int64_t b = 0; b < levels; ++b) {
     // ---------------- variable side: vtof(t_b) (+ marginals in phase 0)
     {
-      std::vector<int32_t> tg;
-      touched.clear();
+      slots.clear();
+      int64_t n_nonunary = 0;
+      bool has_unary = false;
       if (b < k)
         for (int64_t i = t_off[b]; i < t_off[b + 1]; ++i) {
-          int32_t e = t_edges[i];
-          if (stamp[e] == (2 * b)) continue;  // duplicate target
-          stamp[e] = (2 * b);
-          int32_t v = L.edge_var[e];
-          int32_t f = L.edge_factor[e];
-          if (L.rowptr[f + 1] - L.rowptr[f] > 1) {
-            if (vcount[v]++ == 0) touched.push_back(v);
-          }
+          const int32_t e = t_edges[i];
+          if (stamp[e] == 2 * b) continue;  // duplicate target: computed once
+          stamp[e] = 2 * b;
+          slots.push_back(L.canon2f[e]);
+          const int32_t f = L.edge_factor[e];
+          if (L.rowptr[f + 1] - L.rowptr[f] > 1)
+            ++n_nonunary;
+          else
+            has_unary = true;
         }
-      // full variables: every non-unary slot targeted
-      std::vector<int32_t> full_ids;
-      for (int32_t v : touched)
-        if (vcount[v] == L.nonunary[v]) full_ids.push_back(L.vinv[v]);
-      std::sort(full_ids.begin(), full_ids.end());
-      // targets not covered by a full node
-      if (b < k)
-        for (int64_t i = t_off[b]; i < t_off[b + 1]; ++i) {
-          int32_t e = t_edges[i];
-          if (stamp[e] != (2 * b)) continue;
-          stamp[e] = (2 * b) + 1;  // emit once
-          int32_t v = L.edge_var[e];
-          int32_t f = L.edge_factor[e];
-          bool unary = L.rowptr[f + 1] - L.rowptr[f] == 1;
-          bool covered = !unary && vcount[v] == L.nonunary[v];
-          if (!covered) add_vt(e, tg);
-        }
-      for (int32_t v : touched) vcount[v] = 0;
-      sort_quads(tg, [](const int32_t *q) { return ((int64_t)q[2] << 32) | (uint32_t)q[0]; });
-
       Phase ph{};
       ph.type = 0;
-      ph.tgt_begin = (int32_t)(P.vt.size() / 4);
-      P.vt.insert(P.vt.end(), tg.begin(), tg.end());
-      ph.tgt_end = (int32_t)(P.vt.size() / 4);
-      if (b == 0) {
-        ph.node_flags = 1;  // marginal for every variable
-        // variables with no non-unary slot have no vtof target: trivially full
-        int64_t trivially = 0;
-        for (int32_t v = 0; v < V; ++v) trivially += L.nonunary[v] == 0;
-        if ((int64_t)full_ids.size() + trivially == V) {
-          ph.node_list = 0;
-          ph.node_begin = 0;
-          ph.node_end = V;
-          ph.node_flags |= 2;
-        } else {
-          // all variables, vtof bit on the full ones
-          ph.node_list = 1;
-          ph.node_begin = (int32_t)P.vnode.size();
-          size_t j = 0;
-          for (int32_t i = 0; i < V; ++i) {
-            bool isfull = j < full_ids.size() && full_ids[j] == i;
-            if (isfull) ++j;
-            P.vnode.push_back(isfull ? (i | kVtofBit) : i);
-          }
-          ph.node_end = (int32_t)P.vnode.size();
-        }
-        // variables with no non-unary slot are trivially full; nothing differs
+      ph.marg = b == 0;
+      if (b == 0 && n_nonunary == nonunary_total && !has_unary) {
+        // PARALL: every non-unary vtof slot + every marginal == all ftov slots
+        ph.list = 0;
+        ph.begin = 0;
+        ph.end = (int32_t)E;
+        push_phase(ph, (int32_t)E);
       } else {
-        ph.node_list = 1;
-        ph.node_flags = 0;
-        ph.node_begin = (int32_t)P.vnode.size();
-        for (int32_t i : full_ids) P.vnode.push_back(i | kVtofBit);
-        ph.node_end = (int32_t)P.vnode.size();
+        std::vector<int32_t> items;
+        items.reserve(slots.size() + (b == 0 ? V : 0));
+        for (int32_t q : slots) items.push_back(q | kWriteBit);
+        if (b == 0) {
+          // row-start slots that are not targets still owe their marginal
+          std::vector<char> tgt((size_t)V, 0);
+          for (int32_t q : slots)
+            if ((L.vslot[2 * (size_t)q + 1] & 0xffff) == 0) tgt[L.vslot[2 * (size_t)q]] = 1;
+          for (int32_t vi = 0; vi < V; ++vi)
+            if (!tgt[vi]) items.push_back(L.vrow[vi]);
+        }
+        // ascending slot order == (degree, variable) order: warp-uniform trip counts
+        std::sort(items.begin(), items.end(), [](int32_t a, int32_t c) {
+          return (a & (kWriteBit - 1)) < (c & (kWriteBit - 1));
+        });
+        ph.list = 1;
+        ph.begin = (int32_t)P.items.size();
+        P.items.insert(P.items.end(), items.begin(), items.end());
+        ph.end = (int32_t)P.items.size();
+        const int32_t n = ph.end - ph.begin;
+        if (b == 0 || n > 0) push_phase(ph, n);
       }
-      int32_t n = (ph.node_end - ph.node_begin) + (ph.tgt_end - ph.tgt_begin);
-      ph.grid = (b == 0) ? 1 : (n >= kCta0Threshold);
-      P.max_items = std::max(P.max_items, n);
-      if (b == 0 || n > 0) P.phases.push_back(ph);
+      if (b == 0) P.phases.back().grid = 1;  // phase 0 carries the convergence test
     }
     if (b >= k) break;
     // ---------------- factor side: ftov(s_b)
     {
-      std::vector<int32_t> tg;
-      touched.clear();
+      slots.clear();
       for (int64_t i = s_off[b]; i < s_off[b + 1]; ++i) {
-        int32_t e = s_edges[i];
-        if (stamp[e] == (2 * k + 2 * b)) continue;
-        stamp[e] = (2 * k + 2 * b);
-        int32_t f = L.edge_factor[e];
-        if (fcount[f]++ == 0) touched.push_back(f);
+        const int32_t e = s_edges[i];
+        if (stamp[e] == 2 * b + 1) continue;
+        stamp[e] = 2 * b + 1;
+        slots.push_back(L.canon2v[e]);
       }
-      std::vector<int32_t> full_ids;
-      for (int32_t f : touched)
-        if (fcount[f] == L.rowptr[f + 1] - L.rowptr[f]) full_ids.push_back(L.finv[f]);
-      std::sort(full_ids.begin(), full_ids.end());
-      for (int64_t i = s_off[b]; i < s_off[b + 1]; ++i) {
-        int32_t e = s_edges[i];
-        if (stamp[e] != (2 * k + 2 * b)) continue;
-        stamp[e] = (2 * k + 2 * b) + 1;
-        int32_t f = L.edge_factor[e];
-        if (fcount[f] != L.rowptr[f + 1] - L.rowptr[f]) add_ft(e, tg);
-      }
-      for (int32_t f : touched) fcount[f] = 0;
-      const int32_t orb = L.f_or_begin;
-      // group by (kind, head/body), then degree
-      sort_quads(tg, [orb](const int32_t *q) {
-        int64_t kind = q[3] >= orb;
-        int64_t head = (q[2] >> 16) == 0;
-        return (kind << 40) | (head << 39) | ((int64_t)(q[2] & 0xffff) << 20);
-      });
       Phase ph{};
       ph.type = 1;
-      ph.tgt_begin = (int32_t)(P.ft.size() / 4);
-      P.ft.insert(P.ft.end(), tg.begin(), tg.end());
-      ph.tgt_end = (int32_t)(P.ft.size() / 4);
-      if ((int64_t)full_ids.size() == F) {
-        ph.node_list = 0;
-        ph.node_begin = 0;
-        ph.node_end = F;
-      } else {
-        ph.node_list = 1;
-        ph.node_begin = (int32_t)P.fnode.size();
-        P.fnode.insert(P.fnode.end(), full_ids.begin(), full_ids.end());
-        ph.node_end = (int32_t)P.fnode.size();
+      if ((int64_t)slots.size() == E) {
+        ph.list = 0;
+        ph.begin = 0;
+        ph.end = (int32_t)E;
+        push_phase(ph, (int32_t)E);
+      } else if (!slots.empty()) {
+        // ascending vtof slot == (kind, degree, factor) order: warp-uniform role
+        std::sort(slots.begin(), slots.end());
+        ph.list = 1;
+        ph.begin = (int32_t)P.items.size();
+        P.items.insert(P.items.end(), slots.begin(), slots.end());
+        ph.end = (int32_t)P.items.size();
+        push_phase(ph, ph.end - ph.begin);
       }
-      int32_t n = (ph.node_end - ph.node_begin) + (ph.tgt_end - ph.tgt_begin);
-      ph.grid = n >= kCta0Threshold;
-      P.max_items = std::max(P.max_items, n);
-      if (n > 0) P.phases.push_back(ph);
     }
   }
   return HBP_OK;
