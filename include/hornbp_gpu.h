@@ -157,6 +157,11 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
  * reference order (rowptr_ftov [V+1], ftov_to_vtof [E]). */
 hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to_vtof);
 
+/* Self-test of the shared-reciprocal division against __ddiv_rn on the device:
+ * q_fast/q_ref [2n]: a[i]/b[i] and a[(i+1)%n]/b[i]. */
+hbp_status hbp_selftest_division(int64_t n, const double *a, const double *b, double *q_fast,
+                                 double *q_ref);
+
 /* Number of kernels the last hbp_run launched (bench gpu_launches). */
 int64_t hbp_last_launch_count(void);
 const char *hbp_last_error(void);

@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
                                      f64p, f64p, i64p]),
             "hbp_marginals": (C.c_int32, [vp, f64p, f64p, f64p, i64p]),
             "hbp_last_launch_count": (C.c_int64, []),
+            "hbp_selftest_division": (C.c_int32, [C.c_int64, f64p, f64p, f64p, f64p]),
             "hbp_last_error": (C.c_char_p, []),
             "hbp_version": (C.c_char_p, []),
         }
@@ -125,7 +126,8 @@ def lib() -> C.CDLL:
 EXPORTED = ("hbp_compile", "hbp_toposort", "hbp_schedule_sizes", "hbp_schedule_copy",
             "hbp_schedule_destroy", "hbp_graph_create", "hbp_graph_destroy", "hbp_graph_layout",
             "hbp_plan_create", "hbp_plan_destroy", "hbp_run", "hbp_run_device", "hbp_pass",
-            "hbp_marginals", "hbp_last_launch_count", "hbp_last_error", "hbp_version")
+            "hbp_marginals", "hbp_last_launch_count", "hbp_selftest_division", "hbp_last_error",
+            "hbp_version")
 
 
 def last_error() -> str:

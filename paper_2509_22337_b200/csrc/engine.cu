@@ -106,19 +106,29 @@ __device__ __forceinline__ void bar_wait(Ctrl *c, unsigned target) {
 // --------------------------------------------------------------------------------------
 // message output with normalisation + underflow flag (engine.py:155-165)
 
+// Underflow is recorded in a per-thread key (min over the phase) and
+// published once per phase by flush_underflow, so the common path issues no
+// atomics. key = phase << 33 | kind << 32 | slot.
 __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
-                                            int it, int phase, int kind, int slot) {
+                                            int phase, int kind, int slot,
+                                            unsigned long long &ufkey) {
   if (P.normalize) {
-    double t = add(a0, a1);
+    const double t = add(a0, a1);
     if (t < kMinMessageSum) {
-      atomicOr(&P.uf_msg[it], 1 << kind);
-      atomicMin(&P.uf_where[it], ((unsigned long long)phase << 33) |
-                                     ((unsigned long long)kind << 32) | (unsigned)slot);
+      const unsigned long long key = ((unsigned long long)phase << 33) |
+                                     ((unsigned long long)kind << 32) | (unsigned)slot;
+      ufkey = key < ufkey ? key : ufkey;
     }
-    a0 = dvd(a0, t);
-    a1 = dvd(a1, t);
+    div2_rn(a0, a1, t, a0, a1);
   }
   *dst = make_double2(a0, a1);
+}
+
+__device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsigned long long ufkey) {
+  if (ufkey != ~0ull) {
+    atomicOr(&P.uf_msg[it], 1 << (int)((ufkey >> 32) & 1));
+    atomicMin(&P.uf_where[it], ufkey);
+  }
 }
 
 // marginal of iteration it-1 + its |dP1| (engine.py:510-523, :572)
@@ -130,10 +140,14 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
     atomicOr(&P.uf_marg[it - 1], 1);
     atomicMin(&P.uf_mwhere[it - 1], orig);
   }
-  double p0 = dvd(q0, t);
-  double p1 = sub(1.0, p0);
-  double d = fabs(sub(p1, P.prev[v]));
-  unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+  const double p0 = quot_rn(q0, t, rcp_refined(t));
+  const double p1 = sub(1.0, p0);
+  // |P1 - prev| as np.abs does it: clear the sign bit, keep any NaN payload
+  // (integer AND in PTX: the compiler would otherwise turn it into an FP abs,
+  // which canonicalises NaN payloads differently from numpy)
+  const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, P.prev[v]));
+  unsigned long long bits;
+  asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
   dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
   P.prev[v] = p1;
   P.marg[orig] = make_double2(p0, p1);
@@ -190,7 +204,8 @@ __device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg,
 }
 
 __device__ __forceinline__ void v_item(const KParams &P, int q, int write, bool want_marg, int it,
-                                       int phase, unsigned long long &dmax) {
+                                       int phase, unsigned long long &dmax,
+                                       unsigned long long &ufkey) {
   const int2 w = P.vslot[q];
   const unsigned tw = P.ftov_twin[q];
   const int d = w.y >> 16, j = w.y & 0xffff;
@@ -212,7 +227,7 @@ __device__ __forceinline__ void v_item(const KParams &P, int q, int write, bool 
   }
   if (wr) {
     const int out = (int)(tw & ~kUnaryBit);
-    put_message(P, P.vtof + out, a0, a1, it, phase, 0, out);
+    put_message(P, P.vtof + out, a0, a1, phase, 0, out, ufkey);
   }
   if (marg) put_marginal(P, w.x, q0, q1, it, dmax);
 }
@@ -271,8 +286,8 @@ __device__ __forceinline__ void f_row(const KParams &P, int r, int j, double2 pp
 }
 
 template <int KIND>
-__device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw, int it,
-                                         int phase) {
+__device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw, int phase,
+                                         unsigned long long &ufkey) {
   const int d = w.y >> 16, j = w.y & 0xffff;
   const int r = p - j;
   const double2 pp = P.fpar[w.x];
@@ -293,16 +308,17 @@ __device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw
     head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
   else
     body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-  put_message(P, P.ftov + tw, o0, o1, it, phase, 1, tw);
+  put_message(P, P.ftov + tw, o0, o1, phase, 1, tw, ufkey);
 }
 
-__device__ __forceinline__ void f_item(const KParams &P, int p, int it, int phase) {
+__device__ __forceinline__ void f_item(const KParams &P, int p, int phase,
+                                       unsigned long long &ufkey) {
   const int2 w = P.fslot[p];
   const int tw = P.vtof_twin[p];
   if (w.x < P.f_or_begin)
-    f_item_k<0>(P, p, w, tw, it, phase);
+    f_item_k<0>(P, p, w, tw, phase, ufkey);
   else
-    f_item_k<1>(P, p, w, tw, it, phase);
+    f_item_k<1>(P, p, w, tw, phase, ufkey);
 }
 
 // --------------------------------------------------------------------------------------
@@ -321,6 +337,7 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     stride = blockDim.x;
   }
   const int n = ph.end - ph.begin;
+  unsigned long long ufkey = ~0ull;
   if (ph.type == 0) {
     const bool marg = do_marg && ph.marg;
     for (int i = start; i < n; i += stride) {
@@ -334,14 +351,15 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
         write = -1;
       }
       if (!do_vtof) write = 0;
-      v_item(P, q, write, marg, it, pidx, dmax);
+      v_item(P, q, write, marg, it, pidx, dmax, ufkey);
     }
   } else {
     for (int i = start; i < n; i += stride) {
       const int p = ph.list ? P.items[ph.begin + i] : ph.begin + i;
-      f_item(P, p, it, pidx);
+      f_item(P, p, pidx, ufkey);
     }
   }
+  flush_underflow(P, it, ufkey);
 }
 
 __device__ __forceinline__ unsigned long long block_max(unsigned long long v) {
@@ -490,12 +508,25 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int item = items[i];
-  unsigned long long unused = 0;
+  unsigned long long unused = 0, ufkey = ~0ull;
   if (type == 0)
     v_item(P, item & (kWriteBit - 1), (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1, 0,
-           unused);
+           unused, ufkey);
   else
-    f_item(P, item, 1, 0);
+    f_item(P, item, 0, ufkey);
+  flush_underflow(P, 1, ufkey);
+}
+
+__global__ void division_selftest_kernel(const double *a, const double *b, double *qf, double *qr,
+                                         long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x, y;
+  div2_rn(a[i], a[(i + 1) % n], b[i], x, y);
+  qf[2 * i] = x;
+  qf[2 * i + 1] = y;
+  qr[2 * i] = __ddiv_rn(a[i], b[i]);
+  qr[2 * i + 1] = __ddiv_rn(a[(i + 1) % n], b[i]);
 }
 
 }  // namespace hbp
@@ -1004,5 +1035,25 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
 }
 
 int64_t hbp_last_launch_count(void) { return g_last_launches; }
+
+hbp_status hbp_selftest_division(int64_t n, const double *a, const double *b, double *q_fast,
+                                 double *q_ref) {
+  if (n <= 0 || !a || !b || !q_fast || !q_ref) {
+    hbp::set_error("bad selftest arguments");
+    return HBP_EINVAL;
+  }
+  double *d = nullptr;
+  HBP_CUDA(cudaMalloc(&d, (size_t)n * 48));
+  HBP_CUDA(cudaMemcpy(d, a, (size_t)n * 8, cudaMemcpyHostToDevice));
+  HBP_CUDA(cudaMemcpy(d + n, b, (size_t)n * 8, cudaMemcpyHostToDevice));
+  hbp::division_selftest_kernel<<<(unsigned)((n + 255) / 256), 256>>>(d, d + n, d + 2 * n,
+                                                                      d + 4 * n, n);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(q_fast, d + 2 * n, (size_t)n * 16, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(q_ref, d + 4 * n, (size_t)n * 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  HBP_CUDA(e);
+  return HBP_OK;
+}
 
 }  // extern "C"
