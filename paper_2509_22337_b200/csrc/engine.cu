@@ -38,6 +38,7 @@ using namespace dev;
 
 constexpr int kThreads = 1024;  // default block size (HBP_THREADS=512 selects the alternative)
 constexpr int kChunk = 8;       // row elements loaded per round trip
+constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 
 struct Ctrl {
   unsigned int bar;  // grid barrier arrivals (monotonic)
@@ -49,13 +50,15 @@ struct Ctrl {
 
 struct KParams {
   // layout
+  const int *vrow;            // [V+1] internal variable rows in the ftov buffer
+  const int *frow;            // [F+1] internal factor rows in the vtof buffer
   const int2 *vslot;          // per ftov slot
   const int2 *fslot;          // per vtof slot
   const int *vtof_twin;       // vtof slot -> ftov slot
   const unsigned *ftov_twin;  // ftov slot -> vtof slot | kUnaryBit
   const double2 *fpar;        // per internal factor (p1, p2)
   const int *vorig;           // internal variable -> original id
-  int V, F, E, f_or_begin;
+  int V, F, E, f_or_light, f_heavy, f_or_heavy;
   double2 *vtof, *ftov, *marg;
   double *prev;
   // plan
@@ -71,6 +74,7 @@ struct KParams {
   unsigned long long *uf_where;    // [max_it + 2] (phase<<33 | kind<<32 | slot)
   int *tflag;                      // [max_it + 2]
   double2 *hist;                   // [max_it][V] or null
+  unsigned long long *trace;       // debug: [kTraceIters][nphases][grid][2] or null
   int max_it;
   int normalize;
   double tol;
@@ -88,17 +92,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 
 __device__ __forceinline__ void bar_arrive(Ctrl *c) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&c->bar, 1u);
-  }
+  if (threadIdx.x == 0)  // release: the CTA's writes (ordered by bar.sync) before the arrival
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&c->bar) : "memory");
 }
 
 __device__ __forceinline__ void bar_wait(Ctrl *c, unsigned target) {
   if (threadIdx.x == 0) {
     while (ld_acquire(&c->bar) < target) {
     }
-    __threadfence();  // gpu-scope fence: also invalidates this SM's L1
   }
   __syncthreads();
 }
@@ -140,7 +141,7 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
     atomicOr(&P.uf_marg[it - 1], 1);
     atomicMin(&P.uf_mwhere[it - 1], orig);
   }
-  const double p0 = quot_rn(q0, t, rcp_refined(t));
+  const double p0 = div_rn(q0, t);
   const double p1 = sub(1.0, p0);
   // |P1 - prev| as np.abs does it: clear the sign bit, keep any NaN payload
   // (integer AND in PTX: the compiler would otherwise turn it into an FP abs,
@@ -203,11 +204,9 @@ __device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg,
   }
 }
 
-__device__ __forceinline__ void v_item(const KParams &P, int q, int write, bool want_marg, int it,
-                                       int phase, unsigned long long &dmax,
+__device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned tw, int write,
+                                       bool want_marg, int it, int phase, unsigned long long &dmax,
                                        unsigned long long &ufkey) {
-  const int2 w = P.vslot[q];
-  const unsigned tw = P.ftov_twin[q];
   const int d = w.y >> 16, j = w.y & 0xffff;
   const bool marg = want_marg && j == 0;
   const bool wr = write > 0 || (write < 0 && !(tw & kUnaryBit));
@@ -237,6 +236,10 @@ __device__ __forceinline__ void v_item(const KParams &P, int q, int write, bool 
 // Head target (index 0): products over body slots of (m0 + m1) and of
 // m1 (AND) / m0 (OR) -- engine.py:229-248. Body target: the head slot
 // contributes blend = (1-c) m0 + c m1 and (m0 - m1) -- engine.py:198-226.
+
+__device__ __forceinline__ bool factor_is_or(const KParams &P, int f) {
+  return (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
+}
 
 template <int KIND>
 __device__ __noinline__ void f_row_long(const KParams &P, int r, int d, int j, double2 pp,
@@ -311,14 +314,139 @@ __device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw
   put_message(P, P.ftov + tw, o0, o1, phase, 1, tw, ufkey);
 }
 
-__device__ __forceinline__ void f_item(const KParams &P, int p, int phase,
+__device__ __forceinline__ void f_item(const KParams &P, int p, int2 w, int tw, int phase,
                                        unsigned long long &ufkey) {
-  const int2 w = P.fslot[p];
-  const int tw = P.vtof_twin[p];
-  if (w.x < P.f_or_begin)
+  if (!factor_is_or(P, w.x))
     f_item_k<0>(P, p, w, tw, phase, ufkey);
   else
     f_item_k<1>(P, p, w, tw, phase, ufkey);
+}
+
+
+// --------------------------------------------------------------------------------------
+// node-centric items (PARALL range phases): one thread owns a whole variable or
+// factor, reads its row once into registers and emits every outgoing message.
+// The exclusion index is a compile-time constant of the unrolled loops, and
+// the left-to-right prefix products are shared across targets -- exact,
+// because they ARE the reference's partial products (engine.py:173-180).
+
+template <int D>
+__device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool marg, bool vt,
+                                            int it, int phase, unsigned long long &dmax,
+                                            unsigned long long &ufkey) {
+  double x0[D], x1[D];
+  unsigned tw[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double2 m = P.ftov[r + k];
+    x0[k] = m.x;
+    x1[k] = m.y;
+  }
+  if (vt) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) tw[k] = __ldg(P.ftov_twin + r + k);
+  }
+  double a0 = 1.0, a1 = 1.0;  // prefix x[0] * ... * x[j-1]
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (vt && !(tw[j] & kUnaryBit)) {
+      double b0 = a0, b1 = a1;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b0 = mul(b0, x0[k]);
+        b1 = mul(b1, x1[k]);
+      }
+      put_message(P, P.vtof + tw[j], b0, b1, phase, 0, (int)tw[j], ufkey);
+    }
+    a0 = mul(a0, x0[j]);
+    a1 = mul(a1, x1[j]);
+  }
+  if (marg) put_marginal(P, v, a0, a1, it, dmax);
+}
+
+
+
+__device__ __forceinline__ void vnode(const KParams &P, int v, bool marg, bool vt, int it,
+                                      int phase, unsigned long long &dmax,
+                                      unsigned long long &ufkey) {
+  const int r = __ldg(P.vrow + v);
+  const int d = __ldg(P.vrow + v + 1) - r;
+  switch (d) {
+    case 1: vnode_fixed<1>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
+    case 2: vnode_fixed<2>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
+    case 3: vnode_fixed<3>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
+    default: vnode_fixed<4>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
+  }
+}
+
+template <int D, int KIND>
+__device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int phase,
+                                            unsigned long long &ufkey) {
+  const double2 pp = __ldg(P.fpar + f);
+  double m0[D], m1[D];
+  int tw[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double2 m = P.vtof[r + k];
+    m0[k] = m.x;
+    m1[k] = m.y;
+    tw[k] = __ldg(P.vtof_twin + r + k);
+  }
+  double s[D];
+#pragma unroll
+  for (int k = 1; k < D; ++k) s[k] = add(m0[k], m1[k]);
+  {  // head target: products over the body slots
+    double h1 = 1.0, h2 = 1.0;
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+      h1 = mul(h1, s[k]);
+      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
+    }
+    double o0, o1;
+    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
+    put_message(P, P.ftov + tw[0], o0, o1, phase, 1, tw[0], ufkey);
+  }
+  if (D > 1) {  // body targets: the head slot contributes blend / (m0 - m1)
+    double a1, a2;
+    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+      double b1 = a1, b2 = a2;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b1 = mul(b1, s[k]);
+        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
+      }
+      double o0, o1;
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+      put_message(P, P.ftov + tw[j], o0, o1, phase, 1, tw[j], ufkey);
+      a1 = mul(a1, s[j]);
+      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
+    }
+  }
+}
+
+
+
+template <int KIND>
+__device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, int phase,
+                                        unsigned long long &ufkey) {
+  switch (d) {
+    case 1: fnode_fixed<1, KIND>(P, f, r, phase, ufkey); break;
+    case 2: fnode_fixed<2, KIND>(P, f, r, phase, ufkey); break;
+    case 3: fnode_fixed<3, KIND>(P, f, r, phase, ufkey); break;
+    default: fnode_fixed<4, KIND>(P, f, r, phase, ufkey); break;
+  }
+}
+
+__device__ __forceinline__ void fnode(const KParams &P, int f, int phase,
+                                      unsigned long long &ufkey) {
+  const int r = __ldg(P.frow + f);
+  const int d = __ldg(P.frow + f + 1) - r;
+  if (f < P.f_or_light)
+    fnode_k<0>(P, f, r, d, phase, ufkey);
+  else
+    fnode_k<1>(P, f, r, d, phase, ufkey);
 }
 
 // --------------------------------------------------------------------------------------
@@ -338,25 +466,102 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
   }
   const int n = ph.end - ph.begin;
   unsigned long long ufkey = ~0ull;
+  if (ph.list == 2) {
+    // whole light nodes [begin, end), then the slots of the heavy nodes
+    // [sbegin, send); grid-strided so a warp's 32 items are neighbouring rows
+    // (coalesced row loads, uniform degree).
+    const int nn = ph.end - ph.begin;
+    const int total = nn + (ph.send - ph.sbegin);
+    // warp chunks of 32 consecutive items (coalesced rows, uniform degree)
+    // dealt round-robin over CTAs, so every SM gets the same degree mix
+    // (heavy rows sit at the end of the degree-sorted order)
+    const int lane = threadIdx.x & 31;
+    int c0, cstride;
+    if (ph.grid) {
+      c0 = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+      cstride = gridDim.x * (blockDim.x >> 5);
+    } else {
+      c0 = threadIdx.x >> 5;
+      cstride = blockDim.x >> 5;
+    }
+    if (ph.type == 0) {
+      const bool marg = do_marg && ph.marg;
+      if (marg || do_vtof)
+        for (int c = c0; c * 32 < total; c += cstride) {
+          const int i = c * 32 + lane;
+          if (i >= total) break;
+          if (i < nn) {
+            vnode(P, ph.begin + i, marg, do_vtof, it, pidx, dmax, ufkey);
+          } else {
+            const int q = ph.sbegin + (i - nn);
+            v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
+                   pidx, dmax, ufkey);
+          }
+        }
+    } else {
+      for (int c = c0; c * 32 < total; c += cstride) {
+        const int i = c * 32 + lane;
+        if (i >= total) break;
+        if (i < nn) {
+          fnode(P, ph.begin + i, pidx, ufkey);
+        } else {
+          const int p = ph.sbegin + (i - nn);
+          f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
+        }
+      }
+    }
+    flush_underflow(P, it, ufkey);
+    return;
+  }
+  // Slot words, twins and item lists are read-only for the whole launch
+  // (ld.global.nc); the next item's are fetched before the current item is
+  // computed, so the per-item dependent chain is one memory round trip.
   if (ph.type == 0) {
     const bool marg = do_marg && ph.marg;
-    for (int i = start; i < n; i += stride) {
-      int q, write;
+    int q = 0, write = 0;
+    int2 w = make_int2(0, 0);
+    unsigned tw = 0;
+    auto fetch = [&](int i, int &q_, int &write_, int2 &w_, unsigned &tw_) {
       if (ph.list) {
-        const int item = P.items[ph.begin + i];
-        q = item & (kWriteBit - 1);
-        write = (item & kWriteBit) ? 1 : 0;
+        const int item = __ldg(P.items + ph.begin + i);
+        q_ = item & (kWriteBit - 1);
+        write_ = (item & kWriteBit) ? 1 : 0;
       } else {
-        q = ph.begin + i;
-        write = -1;
+        q_ = ph.begin + i;
+        write_ = -1;
       }
-      if (!do_vtof) write = 0;
-      v_item(P, q, write, marg, it, pidx, dmax, ufkey);
+      w_ = __ldg(P.vslot + q_);
+      tw_ = __ldg(P.ftov_twin + q_);
+    };
+    if (start < n) fetch(start, q, write, w, tw);
+    for (int i = start; i < n; i += stride) {
+      int qn = 0, writen = 0;
+      int2 wn = make_int2(0, 0);
+      unsigned twn = 0;
+      if (i + stride < n) fetch(i + stride, qn, writen, wn, twn);
+      v_item(P, q, w, tw, do_vtof ? write : 0, marg, it, pidx, dmax, ufkey);
+      q = qn;
+      write = writen;
+      w = wn;
+      tw = twn;
     }
   } else {
+    int p = 0, tw = 0;
+    int2 w = make_int2(0, 0);
+    auto fetch = [&](int i, int &p_, int2 &w_, int &tw_) {
+      p_ = ph.list ? __ldg(P.items + ph.begin + i) : ph.begin + i;
+      w_ = __ldg(P.fslot + p_);
+      tw_ = __ldg(P.vtof_twin + p_);
+    };
+    if (start < n) fetch(start, p, w, tw);
     for (int i = start; i < n; i += stride) {
-      const int p = ph.list ? P.items[ph.begin + i] : ph.begin + i;
-      f_item(P, p, pidx, ufkey);
+      int pn = 0, twn = 0;
+      int2 wn = make_int2(0, 0);
+      if (i + stride < n) fetch(i + stride, pn, wn, twn);
+      f_item(P, p, w, tw, pidx, ufkey);
+      p = pn;
+      w = wn;
+      tw = twn;
     }
   }
   flush_underflow(P, it, ufkey);
@@ -389,6 +594,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// debug timeline (HBP_TRACE=1): per CTA, phase start / end after a CTA sync
+__device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int which) {
+  if (P.trace == nullptr || it < 2 || it >= 2 + kTraceIters) return;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    P.trace[(((size_t)(it - 2) * P.nphases + p) * gridDim.x + blockIdx.x) * 2 + which] = globaltimer();
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
@@ -416,7 +629,9 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
   for (int it = 1;; ++it) {
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
+    trace_mark(P, it, 0, 0);
     exec_phase(P, P.phases[0], 0, it, it > 1, !final_pass, dmax);
+    trace_mark(P, it, 0, 1);
     if (it > 1) {
       unsigned long long m = block_max(dmax);
       if (threadIdx.x == 0) {
@@ -432,20 +647,33 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
     } else {
       __syncthreads();
     }
-    if (it > 1) {
-      const int done = it - 1;
-      const volatile int *ufm = P.uf_msg, *ufg = P.uf_marg, *tf = P.tflag;
-      const volatile unsigned long long *db = P.delta_bits;
-      int stop = 0;
-      if (ufm[done] || ufg[done]) stop = 4;
-      else if (__longlong_as_double((long long)db[done]) < P.tol) stop = 1;
+    // Stop decision for iteration it-1 (all CTAs passed the barrier, so the
+    // flags and delta are final). With two phases per iteration (PARALL)
+    // the decision is applied at the end of this iteration instead, so its
+    // loads overlap phase 1; a stop then only wastes a factor-side phase
+    // whose output (ftov) is never observed.
+    __shared__ int s_stop;
+    int stop = 0;  // thread 0
+    const int done = it - 1;
+    if (it > 1 && threadIdx.x == 0) {
+      const int ufm = ((const volatile int *)P.uf_msg)[done];
+      const int ufg = ((const volatile int *)P.uf_marg)[done];
+      const int tf = ((const volatile int *)P.tflag)[done];
+      const unsigned long long db = ((const volatile unsigned long long *)P.delta_bits)[done];
+      if (ufm || ufg) stop = 4;
+      else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
       else if (done == P.max_it) stop = 2;
-      else if (tf[done]) stop = 3;
-      if (stop) {
+      else if (tf) stop = 3;
+    }
+    const bool defer = P.nphases == 2 && !final_pass;
+    if (it > 1 && !defer) {
+      if (threadIdx.x == 0) s_stop = stop;
+      __syncthreads();
+      if (s_stop) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
           C->iterations = done;
-          C->converged = stop == 1;
-          C->stop = stop;
+          C->converged = s_stop == 1;
+          C->stop = s_stop;
         }
         return;
       }
@@ -474,7 +702,9 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         }
       }
       unsigned long long unused = 0;
+      trace_mark(P, it, p, 0);
       exec_phase(P, ph, p, it, false, true, unused);
+      trace_mark(P, it, p, 1);
     }
     // transition last phase -> phase 0 of the next iteration (a grid phase)
     if (P.nphases > 1) {
@@ -489,6 +719,18 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         if (blockIdx.x == 0) bar_arrive(C);
         expected += 1;
         bar_wait(C, expected);
+      }
+    }
+    if (it > 1 && defer) {
+      if (threadIdx.x == 0) s_stop = stop;
+      __syncthreads();
+      if (s_stop) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          C->iterations = done;
+          C->converged = s_stop == 1;
+          C->stop = s_stop;
+        }
+        return;
       }
     }
   }
@@ -509,11 +751,13 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   if (i >= n) return;
   const int item = items[i];
   unsigned long long unused = 0, ufkey = ~0ull;
-  if (type == 0)
-    v_item(P, item & (kWriteBit - 1), (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1, 0,
-           unused, ufkey);
-  else
-    f_item(P, item, 0, ufkey);
+  if (type == 0) {
+    const int q = item & (kWriteBit - 1);
+    v_item(P, q, P.vslot[q], P.ftov_twin[q], (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1,
+           0, unused, ufkey);
+  } else {
+    f_item(P, item, P.fslot[item], P.vtof_twin[item], 0, ufkey);
+  }
   flush_underflow(P, 1, ufkey);
 }
 
@@ -563,7 +807,7 @@ struct hbp_graph {
   cudaStream_t stream = nullptr;
   int num_sms = 0, coop_blocks = 0, threads = 1024;
   const void *kernel = nullptr;
-  int *d_vtof_twin = nullptr, *d_vorig = nullptr;
+  int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
   int2 *d_vslot = nullptr, *d_fslot = nullptr;
   double2 *d_fpar = nullptr, *d_vtof = nullptr, *d_ftov = nullptr, *d_marg = nullptr;
@@ -573,13 +817,16 @@ struct hbp_graph {
   size_t ctrl_cap = 0;  // entries per array
   double2 *d_hist = nullptr;
   size_t hist_cap = 0;  // double2 entries
+  unsigned long long *d_trace = nullptr;
+  size_t trace_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   ~hbp_graph() {
     cudaSetDevice(device);
     for (void *p : {(void *)d_vslot, (void *)d_vtof_twin, (void *)d_fslot, (void *)d_ftov_twin,
                     (void *)d_vorig, (void *)d_fpar, (void *)d_vtof, (void *)d_ftov,
-                    (void *)d_marg, (void *)d_prev, d_ctrl, (void *)d_hist})
+                    (void *)d_marg, (void *)d_prev, d_ctrl, (void *)d_hist, (void *)d_trace,
+                    (void *)d_vrow, (void *)d_frow})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -631,6 +878,8 @@ size_t ctrl_bytes(size_t n) { return 256 + n * (8 + 8 + 4 + 4 + 4 + 4); }
 
 hbp::KParams base_params(hbp_graph *g) {
   hbp::KParams P{};
+  P.vrow = g->d_vrow;
+  P.frow = g->d_frow;
   P.vslot = g->d_vslot;
   P.fslot = g->d_fslot;
   P.fpar = g->d_fpar;
@@ -640,7 +889,9 @@ hbp::KParams base_params(hbp_graph *g) {
   P.V = g->L.V;
   P.F = g->L.F;
   P.E = (int)g->L.E;
-  P.f_or_begin = g->L.f_or_begin;
+  P.f_or_light = g->L.f_or_light;
+  P.f_heavy = g->L.f_heavy;
+  P.f_or_heavy = g->L.f_or_heavy;
   P.vtof = g->d_vtof;
   P.ftov = g->d_ftov;
   P.marg = g->d_marg;
@@ -708,7 +959,8 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   std::vector<int2> vslot((size_t)L.E), fslot((size_t)L.E);
   std::memcpy(vslot.data(), L.vslot.data(), (size_t)L.E * 8);
   std::memcpy(fslot.data(), L.fslot.data(), (size_t)L.E * 8);
-  if ((st = upload(&g->d_vslot, vslot, s)) || (st = upload(&g->d_vtof_twin, L.vtof_twin, s)) ||
+  if ((st = upload(&g->d_vrow, L.vrow, s)) || (st = upload(&g->d_frow, L.frow, s)) ||
+      (st = upload(&g->d_vslot, vslot, s)) || (st = upload(&g->d_vtof_twin, L.vtof_twin, s)) ||
       (st = upload(&g->d_fslot, fslot, s)) || (st = upload(&g->d_ftov_twin, L.ftov_twin, s)) ||
       (st = upload(&g->d_vorig, L.vperm, s)) || (st = upload(&g->d_fpar, fpar, s)))
     return st;
@@ -758,7 +1010,8 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
   for (const auto &ph : p->host.phases)
-    if (ph.grid) big = std::max<int64_t>(big, ph.end - ph.begin);
+    if (ph.grid)
+      big = std::max<int64_t>(big, (ph.end - ph.begin) + (ph.list == 2 ? ph.send - ph.sbegin : 0));
   int64_t want = (big + g->threads - 1) / g->threads;
   if (big < 2 * g->threads) want = 1;
   p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
@@ -817,6 +1070,17 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.uf_where = c.uf_where;
   P.tflag = c.tflag;
   P.hist = hist;
+  P.trace = nullptr;
+  if (getenv("HBP_TRACE")) {
+    const size_t n_tr = (size_t)hbp::kTraceIters * P.nphases * p->grid * 2;
+    if (g->trace_cap < n_tr) {
+      if (g->d_trace) cudaFree(g->d_trace);
+      HBP_CUDA(cudaMalloc(&g->d_trace, n_tr * 8));
+      g->trace_cap = n_tr;
+    }
+    HBP_CUDA(cudaMemsetAsync(g->d_trace, 0, n_tr * 8, g->stream));
+    P.trace = g->d_trace;
+  }
   P.max_it = opt->max_iterations;
   P.normalize = opt->normalize_messages ? 1 : 0;
   P.tol = opt->tolerance;
@@ -1035,6 +1299,22 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
 }
 
 int64_t hbp_last_launch_count(void) { return g_last_launches; }
+
+// Debug: phase count and grid size of a plan (not part of the public header).
+void hbp_debug_plan_info(hbp_plan *p, int32_t *nphases, int32_t *grid, int32_t *threads) {
+  *nphases = (int32_t)p->host.phases.size();
+  *grid = p->grid;
+  *threads = p->g->threads;
+}
+
+// Debug timeline of the last run with HBP_TRACE=1 (not part of the public header).
+int64_t hbp_debug_trace(hbp_plan *p, unsigned long long *out, int64_t cap) {
+  hbp_graph *g = p->g;
+  const int64_t n = (int64_t)hbp::kTraceIters * (int64_t)p->host.phases.size() * p->grid * 2;
+  if (!g->d_trace || cap < n) return -n;
+  cudaMemcpy(out, g->d_trace, (size_t)n * 8, cudaMemcpyDeviceToHost);
+  return n;
+}
 
 hbp_status hbp_selftest_division(int64_t n, const double *a, const double *b, double *q_fast,
                                  double *q_ref) {

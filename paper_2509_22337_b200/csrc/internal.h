@@ -36,10 +36,17 @@ hbp_status compile(const hbp_graph_desc &g, int64_t m, const int32_t *before,
 struct Phase {
   int32_t type;   // 0 variable side, 1 factor side
   int32_t grid;   // 1: whole grid; 0: CTA 0 only (small level)
-  int32_t list;   // 1: slot ids come from the item list; 0: slots [begin, end)
+  int32_t list;   // 0: slots [begin, end); 1: slot ids from the item list;
+                  // 2: whole nodes [begin, end) (variables for type 0, factors for
+                  //    type 1), every outgoing message of a node from one row read
   int32_t marg;   // 1: row-start slots also produce the marginal (phase 0)
-  int32_t begin, end;
+  int32_t begin, end;     // nodes (list == 2) or slots / items
+  int32_t sbegin, send;   // list == 2: slots of the heavy nodes, one thread per slot
 };
+
+// Nodes up to this degree are processed whole by one thread (row in
+// registers); the rows of larger nodes are processed one slot per thread.
+constexpr int32_t kNodeMax = 4;
 
 // List items: slot id | kWriteBit (type 0 only: also write the vtof message;
 // items without it exist only to produce a marginal).
@@ -78,7 +85,13 @@ struct HostLayout {
   std::vector<int32_t> edge_factor;  // canonical edge -> original factor
   std::vector<int32_t> ref_ftov;     // reference ftov position -> canonical edge (storage.py:61)
   std::vector<int32_t> nonunary;     // per original variable: # slots in non-unary factors
-  int32_t f_or_begin = 0;  // internal factors >= this are OR (order: kind, degree)
+  // internal factor order: (heavy, kind, degree) with heavy = degree > kNodeMax:
+  // [light AND | light OR | heavy AND | heavy OR]
+  int32_t f_or_light = 0, f_heavy = 0, f_or_heavy = 0;
+  int32_t v_heavy = 0;  // internal variables >= this have degree > kNodeMax
+  bool factor_is_or(int32_t fi) const {
+    return (fi >= f_or_light && fi < f_heavy) || fi >= f_or_heavy;
+  }
   int32_t max_fdeg = 0, max_vdeg = 0;
 };
 

@@ -60,16 +60,19 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     }
   L.max_fdeg = maxdeg;
 
-  // factors: stable counting sort by (kind, degree) -> warp-uniform role and
-  // trip count across consecutive slots
-  const int32_t nkeys = 2 * (maxdeg + 1);
+  // factors: stable counting sort by (heavy, kind, degree) -> warp-uniform role
+  // and trip count across consecutive ids; heavy rows form the slot tail
+  const int32_t nkeys = 4 * (maxdeg + 1);
   std::vector<int64_t> bucket((size_t)nkeys + 1, 0);
   auto fkey = [&](int32_t f) {
-    return (int32_t)L.kind[f] * (maxdeg + 1) + (int32_t)(L.rowptr[f + 1] - L.rowptr[f]);
+    const int32_t d = (int32_t)(L.rowptr[f + 1] - L.rowptr[f]);
+    return ((d > kNodeMax) * 2 + (int32_t)L.kind[f]) * (maxdeg + 1) + d;
   };
   for (int32_t f = 0; f < F; ++f) bucket[fkey(f) + 1]++;
   for (int32_t k = 0; k < nkeys; ++k) bucket[k + 1] += bucket[k];
-  L.f_or_begin = (int32_t)bucket[maxdeg + 1];
+  L.f_or_light = (int32_t)bucket[1 * (maxdeg + 1)];
+  L.f_heavy = (int32_t)bucket[2 * (maxdeg + 1)];
+  L.f_or_heavy = (int32_t)bucket[3 * (maxdeg + 1)];
   L.fperm.resize(F);
   L.finv.resize(F);
   {
@@ -130,6 +133,12 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   }
   L.vrow.assign((size_t)V + 1, 0);
   for (int32_t i = 0; i < V; ++i) L.vrow[i + 1] = L.vrow[i] + vdeg[L.vperm[i]];
+  L.v_heavy = V;
+  for (int32_t i = 0; i < V; ++i)
+    if (L.vrow[i + 1] - L.vrow[i] > kNodeMax) {
+      L.v_heavy = i;
+      break;
+    }
 
   // ftov rows: canonical order within each variable == (factor, slot) order,
   // which is the reference's product order (storage.py:59-61)
@@ -237,11 +246,14 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       ph.type = 0;
       ph.marg = b == 0;
       if (b == 0 && n_nonunary == nonunary_total && !has_unary) {
-        // PARALL: every non-unary vtof slot + every marginal == all ftov slots
-        ph.list = 0;
+        // PARALL: every non-unary vtof slot + every marginal == every variable
+        // node in full
+        ph.list = 2;
         ph.begin = 0;
-        ph.end = (int32_t)E;
-        push_phase(ph, (int32_t)E);
+        ph.end = L.v_heavy;
+        ph.sbegin = L.vrow[L.v_heavy];
+        ph.send = (int32_t)E;
+        push_phase(ph, L.v_heavy + (ph.send - ph.sbegin));
       } else {
         std::vector<int32_t> items;
         items.reserve(slots.size() + (b == 0 ? V : 0));
@@ -280,10 +292,12 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       Phase ph{};
       ph.type = 1;
       if ((int64_t)slots.size() == E) {
-        ph.list = 0;
+        ph.list = 2;  // every factor node in full
         ph.begin = 0;
-        ph.end = (int32_t)E;
-        push_phase(ph, (int32_t)E);
+        ph.end = L.f_heavy;
+        ph.sbegin = L.frow[L.f_heavy];
+        ph.send = (int32_t)E;
+        push_phase(ph, L.f_heavy + (ph.send - ph.sbegin));
       } else if (!slots.empty()) {
         // ascending vtof slot == (kind, degree, factor) order: warp-uniform role
         std::sort(slots.begin(), slots.end());
