@@ -162,6 +162,60 @@ hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to
 hbp_status hbp_selftest_division(int64_t n, const double *a, const double *b, double *q_fast,
                                  double *q_ref);
 
+/* ---- multi-evidence sweep (new API; ranking.py:94-135 made embarrassingly parallel) ----
+ *
+ * Runs many independent evidence sets over one graph under the PARALL schedule.
+ * Set j is bitwise identical to engine.run(G_j, Strategy.parall().compile(G_j))
+ * where G_j = clamp_evidence applied to the base graph for each (var, value) of
+ * set j in order (graph.py:189-200). Sets stop at their own convergence
+ * iteration. Sets are processed in passes of hbp_sweep_capacity() sets. */
+
+typedef struct hbp_sweep hbp_sweep;
+
+typedef struct {
+  int32_t num_sets;
+  const int64_t *offsets;  /* [num_sets + 1] into var / value                  */
+  const int32_t *var;      /* observed variable (original id)                   */
+  const int8_t *value;     /* 0 = observed false, 1 = observed true             */
+} hbp_evidence;
+
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double last_delta;
+  int32_t underflow_kind;  /* 0 none, 1 vtof, 2 ftov (index = canonical edge), 3 marginal (variable) */
+  int32_t underflow_iteration;
+  int64_t underflow_index;
+} hbp_set_result;
+
+typedef struct {
+  hbp_set_result *sets;          /* host [num_sets], required                           */
+  double *deltas;                /* host [num_sets][max_iterations] or NULL             */
+  double *marginals;             /* [num_sets][V][2] (P0, P1) or NULL                   */
+  int32_t marginals_on_device;   /* 1: marginals is a device pointer on the graph's GPU */
+  int32_t num_select;            /* selected variables (ascending original ids)         */
+  const int32_t *select;         /* host [num_select]                                   */
+  double *p1_select;             /* [num_sets][num_select] P1 of the selection, or NULL */
+  int32_t p1_on_device;
+  int32_t topk;                  /* ranking of the selection (rank_alarms order)        */
+  int32_t *ranked;               /* [num_sets][topk] variable ids, -1 padded, or NULL   */
+  int32_t ranked_on_device;
+  /* filled in by hbp_sweep_run */
+  double device_ms;              /* stream time of all passes (evidence, sweep, outputs) */
+  double kernel_ms;              /* the persistent sweep kernel(s) alone                 */
+  double wall_ms;
+  int32_t launches;
+  int32_t passes;
+} hbp_sweep_outputs;
+
+/* max_sets_per_pass: 0 = as many as fit in half of the free device memory. */
+hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep **out);
+int32_t hbp_sweep_capacity(const hbp_sweep *sw);
+/* Per-set underflow is reported in sets[j] (HBP_OK overall). */
+hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_evidence *ev,
+                         hbp_sweep_outputs *out);
+void hbp_sweep_destroy(hbp_sweep *sw);
+
 /* Number of kernels the last hbp_run launched (bench gpu_launches). */
 int64_t hbp_last_launch_count(void);
 const char *hbp_last_error(void);

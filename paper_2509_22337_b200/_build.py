@@ -17,8 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhbp.so")
 
-SOURCES = ["engine.cu", "layout.cpp", "compiler.cpp", "capi.cpp"]
-HEADERS = ["internal.h", "lbp_kernels.cuh", os.path.join("..", "..", "include", "hornbp_gpu.h")]
+SOURCES = ["engine.cu", "sweep.cu", "layout.cpp", "compiler.cpp", "capi.cpp"]
+HEADERS = ["internal.h", "device.h", "lbp_kernels.cuh", os.path.join("..", "..", "include", "hornbp_gpu.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -68,6 +68,47 @@ class Result(C.Structure):
     ]
 
 
+class Evidence(C.Structure):
+    _fields_ = [
+        ("num_sets", C.c_int32),
+        ("offsets", i64p),
+        ("var", i32p),
+        ("value", i8p),
+    ]
+
+
+class SetResult(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32),
+        ("converged", C.c_int32),
+        ("last_delta", C.c_double),
+        ("underflow_kind", C.c_int32),
+        ("underflow_iteration", C.c_int32),
+        ("underflow_index", C.c_int64),
+    ]
+
+
+class SweepOutputs(C.Structure):
+    _fields_ = [
+        ("sets", C.POINTER(SetResult)),
+        ("deltas", f64p),
+        ("marginals", f64p),
+        ("marginals_on_device", C.c_int32),
+        ("num_select", C.c_int32),
+        ("select", i32p),
+        ("p1_select", f64p),
+        ("p1_on_device", C.c_int32),
+        ("topk", C.c_int32),
+        ("ranked", i32p),
+        ("ranked_on_device", C.c_int32),
+        ("device_ms", C.c_double),
+        ("kernel_ms", C.c_double),
+        ("wall_ms", C.c_double),
+        ("launches", C.c_int32),
+        ("passes", C.c_int32),
+    ]
+
+
 class NativeError(RuntimeError):
     def __init__(self, status: int, message: str):
         super().__init__(message)
@@ -110,6 +151,11 @@ def lib() -> C.CDLL:
             "hbp_pass": (C.c_int32, [vp, C.c_int32, C.c_int64, i32p, C.c_int32, f64p, f64p,
                                      f64p, f64p, i64p]),
             "hbp_marginals": (C.c_int32, [vp, f64p, f64p, f64p, i64p]),
+            "hbp_sweep_create": (C.c_int32, [vp, C.c_int32, C.POINTER(vp)]),
+            "hbp_sweep_capacity": (C.c_int32, [vp]),
+            "hbp_sweep_run": (C.c_int32, [vp, C.POINTER(Options), C.POINTER(Evidence),
+                                          C.POINTER(SweepOutputs)]),
+            "hbp_sweep_destroy": (None, [vp]),
             "hbp_last_launch_count": (C.c_int64, []),
             "hbp_selftest_division": (C.c_int32, [C.c_int64, f64p, f64p, f64p, f64p]),
             "hbp_last_error": (C.c_char_p, []),
@@ -126,7 +172,8 @@ def lib() -> C.CDLL:
 EXPORTED = ("hbp_compile", "hbp_toposort", "hbp_schedule_sizes", "hbp_schedule_copy",
             "hbp_schedule_destroy", "hbp_graph_create", "hbp_graph_destroy", "hbp_graph_layout",
             "hbp_plan_create", "hbp_plan_destroy", "hbp_run", "hbp_run_device", "hbp_pass",
-            "hbp_marginals", "hbp_last_launch_count", "hbp_selftest_division", "hbp_last_error",
+            "hbp_marginals", "hbp_sweep_create", "hbp_sweep_capacity", "hbp_sweep_run",
+            "hbp_sweep_destroy", "hbp_last_launch_count", "hbp_selftest_division", "hbp_last_error",
             "hbp_version")
 
 

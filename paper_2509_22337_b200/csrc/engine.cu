@@ -29,6 +29,7 @@
 #include <string>
 #include <vector>
 
+#include "device.h"
 #include "internal.h"
 #include "lbp_kernels.cuh"
 
@@ -779,73 +780,13 @@ __global__ void division_selftest_kernel(const double *a, const double *b, doubl
 // host side: handles + C ABI
 
 namespace {
-
 thread_local int64_t g_last_launches = 0;
-
-#define HBP_CUDA(call)                                                          \
-  do {                                                                          \
-    cudaError_t _e = (call);                                                    \
-    if (_e != cudaSuccess) {                                                    \
-      hbp::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));       \
-      return HBP_ECUDA;                                                         \
-    }                                                                           \
-  } while (0)
-
-template <typename T>
-hbp_status upload(T **dst, const std::vector<T> &src, cudaStream_t s) {
-  HBP_CUDA(cudaMalloc((void **)dst, std::max<size_t>(1, src.size()) * sizeof(T)));
-  if (!src.empty())
-    HBP_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s));
-  return HBP_OK;
-}
-
 }  // namespace
 
-struct hbp_graph {
-  hbp::HostLayout L;
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int num_sms = 0, coop_blocks = 0, threads = 1024;
-  const void *kernel = nullptr;
-  int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
-  unsigned *d_ftov_twin = nullptr;
-  int2 *d_vslot = nullptr, *d_fslot = nullptr;
-  double2 *d_fpar = nullptr, *d_vtof = nullptr, *d_ftov = nullptr, *d_marg = nullptr;
-  double *d_prev = nullptr;
-  // control block sized for max_iterations
-  void *d_ctrl = nullptr;
-  size_t ctrl_cap = 0;  // entries per array
-  double2 *d_hist = nullptr;
-  size_t hist_cap = 0;  // double2 entries
-  unsigned long long *d_trace = nullptr;
-  size_t trace_cap = 0;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-
-  ~hbp_graph() {
-    cudaSetDevice(device);
-    for (void *p : {(void *)d_vslot, (void *)d_vtof_twin, (void *)d_fslot, (void *)d_ftov_twin,
-                    (void *)d_vorig, (void *)d_fpar, (void *)d_vtof, (void *)d_ftov,
-                    (void *)d_marg, (void *)d_prev, d_ctrl, (void *)d_hist, (void *)d_trace,
-                    (void *)d_vrow, (void *)d_frow})
-      if (p) cudaFree(p);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
-  }
-};
-
-struct hbp_plan {
-  hbp_graph *g = nullptr;
-  hbp::PlanHost host;
-  hbp::Phase *d_phases = nullptr;
-  int *d_items = nullptr;
-  int grid = 1;
-  ~hbp_plan() {
-    cudaSetDevice(g->device);
-    for (void *p : {(void *)d_phases, (void *)d_items})
-      if (p) cudaFree(p);
-  }
-};
+namespace hbp {
+void set_last_launches(int64_t n) { g_last_launches = n; }
+void add_last_launches(int64_t n) { g_last_launches += n; }
+}  // namespace hbp
 
 namespace {
 

@@ -1,0 +1,879 @@
+// Multi-evidence sweep: many independent evidence / feedback sets over ONE
+// graph under the PARALL schedule -- the embarrassingly parallel form of the
+// interactive ranking loop (ranking.py:94-135: clamp_evidence + compile + run
+// from uniform, once per set), executed as one cooperative launch per pass.
+//
+// Semantics. Clamping variable v (graph.py:189-200)
+// appends a body-empty AND factor whose factor-to-variable message is exactly
+// (1, 0) (observed false) or (0, 1) (observed true) from iteration 1 on, and
+// (1, 1) before its first update. Its slot is the LAST one of v's ftov row
+// (highest factor id, rows in (factor, slot) order, storage.py:59-61), so the
+// clamped graph's products are the base graph's row products with one more
+// multiplication by 0.0 / 1.0 at the end: exact, no rounding change. Under
+// PARALL the clamped graph's schedule is the base schedule plus the clamp
+// edges in s_0 (they are unary, so t_0 is unchanged). Therefore set j of the
+// sweep reproduces hornbp.run(clamped graph j, PARALL) bit for bit by sharing
+// the base graph's CSR and applying a per-(variable, set) evidence code:
+//   - vtof of iteration 1 reads only initial (1,1) messages -> (0.5, 0.5)
+//     everywhere (or (1,1) unnormalised), so iteration 1 loads no messages;
+//   - vtof of iterations >= 2 and every marginal multiply the clamp in last.
+//
+// Layout: set-minor. Every message / marginal array is [row][S] with S = the
+// sets of this pass rounded up to 32, so a warp owns ONE graph node for 32
+// consecutive sets: the node's row indices, twins and factor parameters are
+// warp-uniform broadcast loads, each message load is a fully coalesced 512-byte
+// row segment, and control flow (role, degree) is identical across the warp --
+// the grouping the paper's per-group kernels aim for, with zero divergence.
+// Each lane multiplies its set's row left to right in slot order, the
+// reference's own order (engine.py:168-183), so results are bitwise.
+//
+// Per-set convergence: each set stops at its own iteration (delta < tol,
+// max_iterations, time limit, underflow); stopped sets are masked out and a
+// CTA whose 32 sets have all stopped skips the phase. No host round trip until
+// every set of the pass has stopped.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "device.h"
+#include "lbp_kernels.cuh"
+
+namespace hbp {
+
+using namespace dev;
+
+constexpr int kSwWarps = 8;  // warps per CTA (blockDim = 256); lanes = 32 sets
+constexpr int kSwThreads = 32 * kSwWarps;
+constexpr int kNoVar = 0x7f7f7f7f;  // ufmarg reset value (memset 0x7F)
+
+struct SweepParams {
+  const int *vrow, *frow;     // internal rows
+  const int *vtof_twin;       // vtof slot -> ftov slot
+  const unsigned *ftov_twin;  // ftov slot -> vtof slot | kUnaryBit
+  const double2 *fpar;        // per internal factor (p1, p2)
+  const int *vorig;           // internal variable -> original id
+  int V, F, f_or_light, f_heavy, f_or_heavy;
+  int S;                      // row stride (sets in this pass, multiple of 32)
+  int nsets;                  // real sets in this pass
+  double2 *vtof, *ftov;       // [E][S]
+  double *p0;                 // [V][S] P(X=0) of the last marginal pass
+  const unsigned char *ev;    // [V][S] evidence code: bit0 observed false, bit1 observed true
+  // per-set control, [iteration][S]
+  unsigned long long *dbits;  // |dP1| max, as ordered bits
+  unsigned long long *ufkey;  // first underflowing message: kind << 32 | slot
+  int *ufmarg;                // smallest underflowing variable (original id)
+  int *tflag;                 // [iteration] time limit exceeded
+  int *res_it, *res_stop;     // [S] stopping iteration, reason
+  unsigned *nstop;            // sets stopped so far (padding counts as stopped)
+  unsigned *bar;              // grid barrier arrivals
+  unsigned long long *t0;
+  int max_it, normalize;
+  double tol;
+  long long time_limit_ns;
+};
+
+// ---- grid barrier (same protocol as the single-graph executor) ---------------------------
+
+__device__ __forceinline__ unsigned sw_ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sw_grid_sync(unsigned *bar, unsigned &expected, unsigned nblocks) {
+  __syncthreads();
+  expected += nblocks;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    while (sw_ld_acquire(bar) < expected) {
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long sw_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---- message output: normalise, record underflow (engine.py:155-165) ------------------------
+
+__device__ __forceinline__ void sw_put(const SweepParams &P, double2 *dst, double a0, double a1,
+                                      unsigned kind, unsigned slot, unsigned long long &uf) {
+  if (P.normalize) {
+    const double t = add(a0, a1);
+    if (t < kMinMessageSum) {
+      const unsigned long long key = ((unsigned long long)kind << 32) | slot;
+      uf = key < uf ? key : uf;
+    }
+    div2_rn(a0, a1, t, a0, a1);
+  }
+  *dst = make_double2(a0, a1);
+}
+
+// the clamp factor's message, multiplied in after the row (it is the row's last slot)
+__device__ __forceinline__ void sw_clamp(unsigned code, double &a0, double &a1) {
+  if (code & 1u) {  // observed false: (1, 0)
+    a0 = mul(a0, 1.0);
+    a1 = mul(a1, 0.0);
+  }
+  if (code & 2u) {  // observed true: (0, 1)
+    a0 = mul(a0, 0.0);
+    a1 = mul(a1, 1.0);
+  }
+}
+
+// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572)
+__device__ __forceinline__ void sw_marginal(const SweepParams &P, int v, int s, int it, double q0,
+                                           double q1, unsigned long long &dmax) {
+  const double t = add(q0, q1);
+  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + s], P.vorig[v]);
+  const double p0 = div_rn(q0, t);
+  const double p1 = sub(1.0, p0);
+  double *slot = P.p0 + (size_t)v * P.S + s;
+  const double prev = it == 2 ? 0.5 : sub(1.0, *slot);  // prev P1 starts at 0.5
+  const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, prev));
+  unsigned long long bits;
+  asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
+  dmax = bits > dmax ? bits : dmax;
+  *slot = p0;
+}
+
+// ---- variable side: every outgoing vtof message of node v + its marginal ------------------
+
+template <int D>
+__device__ __forceinline__ void sw_var_fixed(const SweepParams &P, int v, int r, int s, int it,
+                                            bool write_vtof, unsigned long long &dmax,
+                                            unsigned long long &uf) {
+  const size_t S = (size_t)P.S;
+  double x0[D], x1[D];
+  unsigned tw[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double2 m = P.ftov[(size_t)(r + k) * S + s];
+    x0[k] = m.x;
+    x1[k] = m.y;
+    tw[k] = __ldg(P.ftov_twin + r + k);
+  }
+  const unsigned code = P.ev[(size_t)v * S + s];
+  double a0 = 1.0, a1 = 1.0;  // prefix x[0] * ... * x[j-1]: the reference's partial products
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (write_vtof && !(tw[j] & kUnaryBit)) {
+      double b0 = a0, b1 = a1;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b0 = mul(b0, x0[k]);
+        b1 = mul(b1, x1[k]);
+      }
+      if (code) sw_clamp(code, b0, b1);
+      sw_put(P, P.vtof + (size_t)tw[j] * S + s, b0, b1, 0u, tw[j], uf);
+    }
+    a0 = mul(a0, x0[j]);
+    a1 = mul(a1, x1[j]);
+  }
+  if (code) sw_clamp(code, a0, a1);
+  sw_marginal(P, v, s, it, a0, a1, dmax);
+}
+
+// rows longer than 8: per target, re-read the row (L1 hits), same left-to-right order
+__device__ __noinline__ void sw_var_long(const SweepParams &P, int v, int r, int d, int s, int it,
+                                         bool write_vtof, unsigned long long &dmax,
+                                         unsigned long long &uf) {
+  const size_t S = (size_t)P.S;
+  const unsigned code = P.ev[(size_t)v * S + s];
+  if (write_vtof) {
+    for (int j = 0; j < d; ++j) {
+      const unsigned tw = __ldg(P.ftov_twin + r + j);
+      if (tw & kUnaryBit) continue;
+      double b0 = 1.0, b1 = 1.0;
+      for (int k = 0; k < d; ++k) {
+        if (k == j) continue;
+        const double2 m = P.ftov[(size_t)(r + k) * S + s];
+        b0 = mul(b0, m.x);
+        b1 = mul(b1, m.y);
+      }
+      if (code) sw_clamp(code, b0, b1);
+      sw_put(P, P.vtof + (size_t)tw * S + s, b0, b1, 0u, tw, uf);
+    }
+  }
+  double q0 = 1.0, q1 = 1.0;
+  for (int k = 0; k < d; ++k) {
+    const double2 m = P.ftov[(size_t)(r + k) * S + s];
+    q0 = mul(q0, m.x);
+    q1 = mul(q1, m.y);
+  }
+  if (code) sw_clamp(code, q0, q1);
+  sw_marginal(P, v, s, it, q0, q1, dmax);
+}
+
+__device__ __forceinline__ void sw_var(const SweepParams &P, int v, int s, int it, bool write_vtof,
+                                      unsigned long long &dmax, unsigned long long &uf) {
+  const int r = __ldg(P.vrow + v);
+  const int d = __ldg(P.vrow + v + 1) - r;
+  switch (d) {
+    case 1: sw_var_fixed<1>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    case 2: sw_var_fixed<2>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    case 3: sw_var_fixed<3>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    case 4: sw_var_fixed<4>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    case 5: sw_var_fixed<5>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    case 6: sw_var_fixed<6>(P, v, r, s, it, write_vtof, dmax, uf); break;
+    default: sw_var_long(P, v, r, d, s, it, write_vtof, dmax, uf); break;
+  }
+}
+
+// ---- factor side: every outgoing ftov message of factor f ---------------------------------
+// Head target: products over body slots of (m0 + m1) and m1 (AND) / m0 (OR),
+// engine.py:229-248; body targets: the head slot contributes the blend and
+// (m0 - m1), engine.py:198-226. Iteration 1 reads no messages: every vtof
+// message is still the normalised uniform one.
+
+template <int D, int KIND>
+__device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r, int s, int it,
+                                            unsigned long long &uf) {
+  const size_t S = (size_t)P.S;
+  const double2 pp = __ldg(P.fpar + f);
+  double m0[D], m1[D];
+  int tw[D];
+  const double c = P.normalize ? 0.5 : 1.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    tw[k] = __ldg(P.vtof_twin + r + k);
+    if (it == 1) {
+      m0[k] = c;
+      m1[k] = c;
+    } else {
+      const double2 m = P.vtof[(size_t)(r + k) * S + s];
+      m0[k] = m.x;
+      m1[k] = m.y;
+    }
+  }
+  double sm[D];
+#pragma unroll
+  for (int k = 1; k < D; ++k) sm[k] = add(m0[k], m1[k]);
+  {
+    double h1 = 1.0, h2 = 1.0;
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+      h1 = mul(h1, sm[k]);
+      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
+    }
+    double o0, o1;
+    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
+    sw_put(P, P.ftov + (size_t)tw[0] * S + s, o0, o1, 1u, (unsigned)tw[0], uf);
+  }
+  if (D > 1) {
+    double a1, a2;
+    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+      double b1 = a1, b2 = a2;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b1 = mul(b1, sm[k]);
+        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
+      }
+      double o0, o1;
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+      sw_put(P, P.ftov + (size_t)tw[j] * S + s, o0, o1, 1u, (unsigned)tw[j], uf);
+      a1 = mul(a1, sm[j]);
+      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
+    }
+  }
+}
+
+template <int KIND>
+__device__ __noinline__ void sw_fac_long(const SweepParams &P, int f, int r, int d, int s, int it,
+                                         unsigned long long &uf) {
+  const size_t S = (size_t)P.S;
+  const double2 pp = __ldg(P.fpar + f);
+  const double c = P.normalize ? 0.5 : 1.0;
+  for (int j = 0; j < d; ++j) {
+    double b1 = 1.0, b2 = 1.0;
+    for (int k = 0; k < d; ++k) {
+      if (k == j) continue;
+      double2 m = it == 1 ? make_double2(c, c) : P.vtof[(size_t)(r + k) * S + s];
+      double f1, f2;
+      if (k == 0) {
+        head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
+      } else {
+        f1 = add(m.x, m.y);
+        f2 = KIND == 0 ? m.y : m.x;
+      }
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
+    }
+    double o0, o1;
+    if (j == 0)
+      head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+    else
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+    const int tw = __ldg(P.vtof_twin + r + j);
+    sw_put(P, P.ftov + (size_t)tw * S + s, o0, o1, 1u, (unsigned)tw, uf);
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void sw_fac_k(const SweepParams &P, int f, int r, int d, int s, int it,
+                                        unsigned long long &uf) {
+  switch (d) {
+    case 1:  // prior / unary: a constant message, written once
+      if (it == 1) sw_fac_fixed<1, KIND>(P, f, r, s, it, uf);
+      break;
+    case 2: sw_fac_fixed<2, KIND>(P, f, r, s, it, uf); break;
+    case 3: sw_fac_fixed<3, KIND>(P, f, r, s, it, uf); break;
+    case 4: sw_fac_fixed<4, KIND>(P, f, r, s, it, uf); break;
+    case 5: sw_fac_fixed<5, KIND>(P, f, r, s, it, uf); break;
+    default: sw_fac_long<KIND>(P, f, r, d, s, it, uf); break;
+  }
+}
+
+__device__ __forceinline__ void sw_fac(const SweepParams &P, int f, int s, int it,
+                                      unsigned long long &uf) {
+  const int r = __ldg(P.frow + f);
+  const int d = __ldg(P.frow + f + 1) - r;
+  const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
+  if (!is_or)
+    sw_fac_k<0>(P, f, r, d, s, it, uf);
+  else
+    sw_fac_k<1>(P, f, r, d, s, it, uf);
+}
+
+// ---- the persistent sweep kernel -----------------------------------------------------------
+// grid (NX, S/32), block 256 = 8 warps; lane = set blockIdx.y*32 + lane, warps
+// stride over nodes. Per iteration: [variable side: marginal(it-1) + delta +
+// vtof(it)] -> grid sync -> per-set stop decision -> [factor side: ftov(it)]
+// -> grid sync -> exit when every set has stopped.
+
+__global__ void __launch_bounds__(kSwThreads, 4) sweep_persistent(const __grid_constant__ SweepParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = blockIdx.y * 32 + lane;
+  const unsigned nblocks = gridDim.x * gridDim.y;
+  const int wstride = gridDim.x * kSwWarps;
+  const int w0 = blockIdx.x * kSwWarps + warp;
+  bool alive = s < P.nsets;
+  unsigned expected = 0;
+  __shared__ unsigned long long red[kSwWarps][32];
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
+
+  for (int it = 1;; ++it) {
+    if (it >= 2) {
+      const bool final_pass = it == P.max_it + 1;
+      unsigned long long dmax = 0, uf = ~0ull;
+      if (__syncthreads_or(alive)) {
+        if (alive)
+          for (int v = w0; v < P.V; v += wstride) sw_var(P, v, s, it, !final_pass, dmax, uf);
+      }
+      red[warp][lane] = dmax;
+      __syncthreads();
+      if (warp == 0) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < kSwWarps; ++w) m = red[w][lane] > m ? red[w][lane] : m;
+        if (alive) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + s], m);
+      }
+      if (alive && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
+        P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
+      sw_grid_sync(P.bar, expected, nblocks);
+      // stop decision for iteration done = it - 1: every thread of set s reads
+      // the same final values, so the decision is identical across CTAs
+      const int done = it - 1;
+      int stop = 0;
+      if (alive) {
+        const size_t i = (size_t)done * P.S + s;
+        const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
+        const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
+        const int um = ((const volatile int *)P.ufmarg)[i];
+        const int tf = ((const volatile int *)P.tflag)[done];
+        if (uk != ~0ull || um != kNoVar) stop = 4;
+        else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
+        else if (done == P.max_it) stop = 2;
+        else if (tf) stop = 3;
+      }
+      if (stop) {
+        alive = false;
+        if (blockIdx.x == 0 && warp == 0) {
+          P.res_it[s] = done;
+          P.res_stop[s] = stop;
+          atomicAdd(P.nstop, 1u);
+        }
+      }
+    }
+    {
+      unsigned long long uf = ~0ull;
+      if (__syncthreads_or(alive)) {
+        if (alive)
+          for (int f = w0; f < P.F; f += wstride) sw_fac(P, f, s, it, uf);
+      }
+      if (alive && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+    }
+    sw_grid_sync(P.bar, expected, nblocks);
+    if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
+  }
+}
+
+// ---- evidence table + outputs ----------------------------------------------------------------
+
+// ev[vinv[var]][set] |= 1 (false) / 2 (true); byte OR through the containing word
+__global__ void sweep_evidence_kernel(unsigned char *ev, const int *vinv, const int *ev_set,
+                                      const int *ev_var, const signed char *ev_val, int n, int S) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t pos = (size_t)vinv[ev_var[i]] * S + ev_set[i];
+  const unsigned bit = ev_val[i] ? 2u : 1u;
+  unsigned *word = (unsigned *)(ev + (pos & ~(size_t)3));
+  atomicOr(word, bit << (8 * (pos & 3)));
+}
+
+// out[set][k][2] = (P0, 1 - P0) of original variable sel[k] (sel == null: k itself);
+// 32 x 32 tiles: coalesced reads along sets, coalesced writes along variables
+__global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const int *sel, int nsel,
+                                       int S, int nsets, int set_base, double *out_pair,
+                                       double *out_p1) {
+  __shared__ double tile[32][33];
+  const int k0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // blockDim 256: 8 rows per step
+  for (int r = ty; r < 32; r += 8) {
+    const int k = k0 + r, s = s0 + tx;
+    double v = 0.0;
+    if (k < nsel && s < nsets) {
+      const int var = sel ? sel[k] : k;
+      v = p0[(size_t)vinv[var] * S + s];
+    }
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int s = s0 + r, k = k0 + tx;
+    if (k < nsel && s < nsets) {
+      const double q = tile[tx][r];
+      const size_t o = (size_t)(set_base + s) * nsel + k;
+      if (out_pair) {
+        out_pair[2 * o] = q;
+        out_pair[2 * o + 1] = sub(1.0, q);
+      }
+      if (out_p1) out_p1[o] = sub(1.0, q);
+    }
+  }
+}
+
+// Top-k alarms per set (ranking.py:83-91): unlabeled alarms by descending P1,
+// ties by ascending id. One CTA per set; bitonic sort of (~bits(P1), position)
+// in shared memory -- P1 >= 0, so its bit pattern orders like its value, and
+// positions index the id-sorted selection. Labeled = clamped in this set.
+__global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, const unsigned char *ev,
+                                                           const int *vinv, const int *sel,
+                                                           int nsel, int npow2, int S,
+                                                           int set_base, int topk, int *ranked) {
+  extern __shared__ unsigned char smem[];
+  unsigned long long *key = (unsigned long long *)smem;
+  int *pos = (int *)(key + npow2);
+  const int s = blockIdx.x;
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    unsigned long long k = ~0ull;
+    if (i < nsel) {
+      const size_t at = (size_t)vinv[sel[i]] * S + s;
+      if (ev[at] == 0) {
+        const double p1 = sub(1.0, p0[at]);
+        k = ~(unsigned long long)__double_as_longlong(p1);
+      }
+    }
+    key[i] = k;
+    pos[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < npow2 / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long ka = key[lo], kb = key[hi];
+        const int pa = pos[lo], pb = pos[hi];
+        const bool gt = ka > kb || (ka == kb && pa > pb);
+        if (gt == up) {
+          key[lo] = kb;
+          key[hi] = ka;
+          pos[lo] = pb;
+          pos[hi] = pa;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < topk; i += blockDim.x)
+    ranked[(size_t)(set_base + s) * topk + i] = (i < nsel && key[i] != ~0ull) ? sel[pos[i]] : -1;
+}
+
+}  // namespace hbp
+
+// ======================================================================================
+// handle + C ABI
+
+struct hbp_sweep {
+  hbp_graph *g = nullptr;
+  int cap = 0;           // sets per pass (multiple of 32)
+  int grid_x_max = 0;    // co-resident CTAs for the cooperative launch
+  int *d_vinv = nullptr;
+  double2 *d_vtof = nullptr, *d_ftov = nullptr;
+  double *d_p0 = nullptr;
+  unsigned char *d_ev = nullptr;
+  void *d_ctrl = nullptr;
+  size_t ctrl_bytes = 0;
+  void *d_scratch = nullptr;  // evidence lists, selection, staging outputs
+  size_t scratch_bytes = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, k0 = nullptr, k1 = nullptr;
+  ~hbp_sweep() {
+    cudaSetDevice(g->device);
+    for (void *p : {(void *)d_vinv, (void *)d_vtof, (void *)d_ftov, (void *)d_p0, (void *)d_ev,
+                    d_ctrl, d_scratch})
+      if (p) cudaFree(p);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (k0) cudaEventDestroy(k0);
+    if (k1) cudaEventDestroy(k1);
+  }
+};
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+hbp_status ensure(void **p, size_t *cap, size_t need) {
+  if (*cap >= need) return HBP_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  HBP_CUDA(cudaMalloc(p, need));
+  *cap = need;
+  return HBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep **out) {
+  if (!g || !out || max_sets_per_pass < 0) {
+    hbp::set_error("bad sweep arguments");
+    return HBP_EINVAL;
+  }
+  *out = nullptr;
+  HBP_CUDA(cudaSetDevice(g->device));
+  std::unique_ptr<hbp_sweep> sw(new (std::nothrow) hbp_sweep());
+  if (!sw) return HBP_ENOMEM;
+  sw->g = g;
+  const hbp::HostLayout &L = g->L;
+  int per_sm = 0;
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hbp::sweep_persistent,
+                                                         hbp::kSwThreads, 0));
+  sw->grid_x_max = std::max(1, per_sm) * g->num_sms;
+  // capacity: requested, else what fits in half of the free memory
+  const size_t per_set = (size_t)L.E * 32 + (size_t)L.V * 9;
+  size_t free_b = 0, total_b = 0;
+  HBP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int cap = max_sets_per_pass > 0 ? max_sets_per_pass : (int)std::min<size_t>(4096, free_b / 2 / per_set);
+  cap = std::max(32, (cap + 31) / 32 * 32);
+  cap = std::min(cap, 32 * sw->grid_x_max);
+  sw->cap = cap;
+  hbp_status st;
+  if ((st = upload(&sw->d_vinv, L.vinv, g->stream))) return st;
+  HBP_CUDA(cudaMalloc(&sw->d_vtof, (size_t)L.E * cap * sizeof(double2)));
+  HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
+  HBP_CUDA(cudaMalloc(&sw->d_p0, (size_t)std::max(1, L.V) * cap * sizeof(double)));
+  HBP_CUDA(cudaMalloc(&sw->d_ev, (size_t)std::max(1, L.V) * cap + 4));
+  HBP_CUDA(cudaEventCreate(&sw->e0));
+  HBP_CUDA(cudaEventCreate(&sw->e1));
+  HBP_CUDA(cudaEventCreate(&sw->k0));
+  HBP_CUDA(cudaEventCreate(&sw->k1));
+  HBP_CUDA(cudaStreamSynchronize(g->stream));
+  *out = sw.release();
+  return HBP_OK;
+}
+
+int32_t hbp_sweep_capacity(const hbp_sweep *sw) { return sw ? sw->cap : 0; }
+
+void hbp_sweep_destroy(hbp_sweep *sw) { delete sw; }
+
+hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_evidence *ev,
+                         hbp_sweep_outputs *out) {
+  auto wall0 = std::chrono::steady_clock::now();
+  if (!sw || !opt || !ev || !out || !out->sets || ev->num_sets < 0 ||
+      (ev->num_sets > 0 && !ev->offsets)) {
+    hbp::set_error("null sweep argument");
+    return HBP_EINVAL;
+  }
+  if (opt->max_iterations < 1) {
+    hbp::set_error("max_iterations must be at least 1");
+    return HBP_EINVAL;
+  }
+  if (!(opt->tolerance >= 0)) {
+    hbp::set_error("tolerance must be nonnegative");
+    return HBP_EINVAL;
+  }
+  if (opt->record_history) {
+    hbp::set_error("record_history is not supported by the sweep");
+    return HBP_EINVAL;
+  }
+  hbp_graph *g = sw->g;
+  const hbp::HostLayout &L = g->L;
+  const int n = ev->num_sets;
+  const int64_t nev = n ? ev->offsets[n] : 0;
+  if (n && (ev->offsets[0] != 0 || nev < 0 || (nev > 0 && (!ev->var || !ev->value)))) {
+    hbp::set_error("bad evidence offsets");
+    return HBP_EINVAL;
+  }
+  for (int j = 0; j < n; ++j)
+    if (ev->offsets[j + 1] < ev->offsets[j]) {
+      hbp::set_error("evidence offsets must be nondecreasing");
+      return HBP_EINVAL;
+    }
+  for (int64_t i = 0; i < nev; ++i) {
+    if (ev->var[i] < 0 || ev->var[i] >= L.V) {
+      hbp::set_error("evidence variable out of range");
+      return HBP_EINVAL;
+    }
+    if (ev->value[i] != 0 && ev->value[i] != 1) {
+      hbp::set_error("evidence value must be 0 or 1");
+      return HBP_EINVAL;
+    }
+  }
+  const int nsel = out->p1_select || out->ranked ? out->num_select : 0;
+  if (nsel < 0 || (nsel > 0 && !out->select)) {
+    hbp::set_error("bad selection");
+    return HBP_EINVAL;
+  }
+  for (int k = 0; k < nsel; ++k)
+    if (out->select[k] < 0 || out->select[k] >= L.V || (k && out->select[k] <= out->select[k - 1])) {
+      hbp::set_error("selection must be ascending variable ids");
+      return HBP_EINVAL;
+    }
+  int npow2 = 1;
+  while (npow2 < nsel) npow2 <<= 1;
+  if (out->ranked && (out->topk < 0 || (size_t)npow2 * 12 > 200 * 1024)) {
+    hbp::set_error("device ranking supports at most 16384 selected variables");
+    return HBP_EINVAL;
+  }
+  HBP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = g->stream;
+  const int max_it = opt->max_iterations;
+  const size_t nit = (size_t)max_it + 2;
+  const int cap = sw->cap;
+  // control block: dbits, ufkey [nit][cap] u64; ufmarg [nit][cap]; tflag [nit];
+  // res_it, res_stop [cap]; nstop, bar, t0
+  const size_t o_db = 0, o_uk = o_db + align256(nit * cap * 8), o_um = o_uk + align256(nit * cap * 8),
+               o_tf = o_um + align256(nit * cap * 4), o_ri = o_tf + align256(nit * 4),
+               o_rs = o_ri + align256((size_t)cap * 4), o_misc = o_rs + align256((size_t)cap * 4),
+               ctrl_need = o_misc + 256;
+  hbp_status s_;
+  if ((s_ = ensure(&sw->d_ctrl, &sw->ctrl_bytes, ctrl_need))) return s_;
+  char *cb = (char *)sw->d_ctrl;
+  unsigned long long *d_db = (unsigned long long *)(cb + o_db);
+  unsigned long long *d_uk = (unsigned long long *)(cb + o_uk);
+  int *d_um = (int *)(cb + o_um), *d_tf = (int *)(cb + o_tf), *d_ri = (int *)(cb + o_ri),
+      *d_rs = (int *)(cb + o_rs);
+  unsigned *d_nstop = (unsigned *)(cb + o_misc), *d_bar = d_nstop + 1;
+  unsigned long long *d_t0 = (unsigned long long *)(cb + o_misc + 64);
+  // scratch: evidence (set, var, val) for one pass, selection, output staging
+  const bool marg_dev = out->marginals && out->marginals_on_device;
+  const bool p1_dev = out->p1_select && out->p1_on_device;
+  const bool rk_dev = out->ranked && out->ranked_on_device;
+  const size_t pass_ev_max = [&] {
+    int64_t m = 0;
+    for (int b = 0; b < n; b += cap) m = std::max<int64_t>(m, ev->offsets[std::min(n, b + cap)] - ev->offsets[b]);
+    return (size_t)m;
+  }();
+  const size_t so_ev = 0, so_sel = so_ev + align256(pass_ev_max * 9 + 16),
+               so_marg = so_sel + align256((size_t)nsel * 4 + 4),
+               so_p1 = so_marg + ((out->marginals && !marg_dev) ? align256((size_t)cap * L.V * 16) : 0),
+               so_rk = so_p1 + ((out->p1_select && !p1_dev) ? align256((size_t)cap * nsel * 8) : 0),
+               scratch_need = so_rk + ((out->ranked && !rk_dev) ? align256((size_t)cap * out->topk * 4) : 0) + 256;
+  if ((s_ = ensure(&sw->d_scratch, &sw->scratch_bytes, scratch_need))) return s_;
+  char *sb = (char *)sw->d_scratch;
+  int *d_ev_set = (int *)(sb + so_ev);
+  int *d_ev_var = d_ev_set + pass_ev_max;
+  signed char *d_ev_val = (signed char *)(d_ev_var + pass_ev_max);
+  int *d_sel = (int *)(sb + so_sel);
+  double *stage_marg = (double *)(sb + so_marg);
+  double *stage_p1 = (double *)(sb + so_p1);
+  int *stage_rk = (int *)(sb + so_rk);
+  if (nsel) HBP_CUDA(cudaMemcpyAsync(d_sel, out->select, (size_t)nsel * 4, cudaMemcpyHostToDevice, st));
+
+  hbp::SweepParams P{};
+  P.vrow = g->d_vrow;
+  P.frow = g->d_frow;
+  P.vtof_twin = g->d_vtof_twin;
+  P.ftov_twin = g->d_ftov_twin;
+  P.fpar = g->d_fpar;
+  P.vorig = g->d_vorig;
+  P.V = L.V;
+  P.F = L.F;
+  P.f_or_light = L.f_or_light;
+  P.f_heavy = L.f_heavy;
+  P.f_or_heavy = L.f_or_heavy;
+  P.vtof = sw->d_vtof;
+  P.ftov = sw->d_ftov;
+  P.p0 = sw->d_p0;
+  P.ev = sw->d_ev;
+  P.dbits = d_db;
+  P.ufkey = d_uk;
+  P.ufmarg = d_um;
+  P.tflag = d_tf;
+  P.res_it = d_ri;
+  P.res_stop = d_rs;
+  P.nstop = d_nstop;
+  P.bar = d_bar;
+  P.t0 = d_t0;
+  P.max_it = max_it;
+  P.normalize = opt->normalize_messages ? 1 : 0;
+  P.tol = opt->tolerance;
+  P.time_limit_ns = opt->time_limit > 0 ? std::max<long long>(1, (long long)(opt->time_limit * 1e9)) : 0;
+
+  std::vector<unsigned long long> h_db, h_uk;
+  std::vector<int> h_um, h_ri, h_rs, h_set;
+  std::vector<int> h_ev_set, h_ev_var;
+  std::vector<signed char> h_ev_val;
+  int64_t launches = 0;
+  int passes = 0;
+  double dev_ms = 0, ker_ms = 0;
+  for (int base = 0; base < n; base += cap) {
+    const int ns = std::min(cap, n - base);
+    const int S = (ns + 31) / 32 * 32;
+    const int groups = S / 32;
+    const int nx = std::max(1, std::min(sw->grid_x_max / groups, (L.F + hbp::kSwWarps - 1) / hbp::kSwWarps));
+    P.S = S;
+    P.nsets = ns;
+    // evidence table of this pass
+    const int64_t e_lo = ev->offsets[base], e_hi = ev->offsets[base + ns];
+    const int64_t ne = e_hi - e_lo;
+    h_ev_set.resize(ne);
+    h_ev_var.assign(ev->var + e_lo, ev->var + e_hi);
+    h_ev_val.assign(ev->value + e_lo, ev->value + e_hi);
+    for (int j = 0; j < ns; ++j)
+      for (int64_t i = ev->offsets[base + j]; i < ev->offsets[base + j + 1]; ++i) h_ev_set[i - e_lo] = j;
+    HBP_CUDA(cudaEventRecord(sw->e0, st));
+    HBP_CUDA(cudaMemsetAsync(sw->d_ev, 0, (size_t)L.V * S, st));
+    if (ne) {
+      HBP_CUDA(cudaMemcpyAsync(d_ev_set, h_ev_set.data(), ne * 4, cudaMemcpyHostToDevice, st));
+      HBP_CUDA(cudaMemcpyAsync(d_ev_var, h_ev_var.data(), ne * 4, cudaMemcpyHostToDevice, st));
+      HBP_CUDA(cudaMemcpyAsync(d_ev_val, h_ev_val.data(), ne, cudaMemcpyHostToDevice, st));
+      hbp::sweep_evidence_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(
+          sw->d_ev, sw->d_vinv, d_ev_set, d_ev_var, d_ev_val, (int)ne, S);
+      ++launches;
+    }
+    // control reset
+    HBP_CUDA(cudaMemsetAsync(d_db, 0, nit * S * 8, st));
+    HBP_CUDA(cudaMemsetAsync(d_uk, 0xFF, nit * S * 8, st));
+    HBP_CUDA(cudaMemsetAsync(d_um, 0x7F, nit * S * 4, st));
+    HBP_CUDA(cudaMemsetAsync(d_tf, 0, nit * 4, st));
+    HBP_CUDA(cudaMemsetAsync(d_ri, 0, (size_t)S * 4, st));
+    HBP_CUDA(cudaMemsetAsync(d_rs, 0, (size_t)S * 4, st));
+    const unsigned misc[2] = {(unsigned)(S - ns), 0u};
+    HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
+    void *args[] = {&P};
+    HBP_CUDA(cudaEventRecord(sw->k0, st));
+    HBP_CUDA(cudaLaunchCooperativeKernel((const void *)hbp::sweep_persistent, dim3(nx, groups),
+                                         dim3(hbp::kSwThreads), args, 0, st));
+    HBP_CUDA(cudaEventRecord(sw->k1, st));
+    ++launches;
+    // outputs of this pass
+    if (out->marginals) {
+      double *dst = marg_dev ? out->marginals : stage_marg;
+      const int bbase = marg_dev ? base : 0;
+      hbp::sweep_marginals_kernel<<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
+          sw->d_p0, sw->d_vinv, nullptr, L.V, S, ns, bbase, dst, nullptr);
+      ++launches;
+      if (!marg_dev)
+        HBP_CUDA(cudaMemcpyAsync(out->marginals + (size_t)base * L.V * 2, stage_marg,
+                                 (size_t)ns * L.V * 16, cudaMemcpyDeviceToHost, st));
+    }
+    if (out->p1_select && nsel) {
+      double *dst = p1_dev ? out->p1_select : stage_p1;
+      const int bbase = p1_dev ? base : 0;
+      hbp::sweep_marginals_kernel<<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
+          sw->d_p0, sw->d_vinv, d_sel, nsel, S, ns, bbase, nullptr, dst);
+      ++launches;
+      if (!p1_dev)
+        HBP_CUDA(cudaMemcpyAsync(out->p1_select + (size_t)base * nsel, stage_p1,
+                                 (size_t)ns * nsel * 8, cudaMemcpyDeviceToHost, st));
+    }
+    if (out->ranked && out->topk > 0) {
+      int *dst = rk_dev ? out->ranked : stage_rk;
+      const int bbase = rk_dev ? base : 0;
+      const size_t smem = (size_t)std::max(npow2, 2) * 12;
+      if (smem > 48 * 1024)
+        HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      hbp::sweep_rank_kernel<<<ns, 1024, smem, st>>>(sw->d_p0, sw->d_ev, sw->d_vinv, d_sel, nsel,
+                                                     std::max(npow2, 2), S, bbase, out->topk, dst);
+      ++launches;
+      if (!rk_dev)
+        HBP_CUDA(cudaMemcpyAsync(out->ranked + (size_t)base * out->topk, stage_rk,
+                                 (size_t)ns * out->topk * 4, cudaMemcpyDeviceToHost, st));
+    }
+    HBP_CUDA(cudaGetLastError());
+    HBP_CUDA(cudaEventRecord(sw->e1, st));
+    // per-set results of this pass
+    h_db.resize(nit * S);
+    h_uk.resize(nit * S);
+    h_um.resize(nit * S);
+    h_ri.resize(S);
+    h_rs.resize(S);
+    HBP_CUDA(cudaMemcpyAsync(h_ri.data(), d_ri, (size_t)S * 4, cudaMemcpyDeviceToHost, st));
+    HBP_CUDA(cudaMemcpyAsync(h_rs.data(), d_rs, (size_t)S * 4, cudaMemcpyDeviceToHost, st));
+    HBP_CUDA(cudaStreamSynchronize(st));
+    {
+      float a = 0, b = 0;
+      HBP_CUDA(cudaEventElapsedTime(&a, sw->e0, sw->e1));
+      HBP_CUDA(cudaEventElapsedTime(&b, sw->k0, sw->k1));
+      dev_ms += a;
+      ker_ms += b;
+    }
+    int maxit_seen = 0;
+    for (int j = 0; j < ns; ++j) maxit_seen = std::max(maxit_seen, h_ri[j]);
+    const size_t rows = (size_t)maxit_seen + 2;
+    HBP_CUDA(cudaMemcpyAsync(h_db.data(), d_db, rows * S * 8, cudaMemcpyDeviceToHost, st));
+    HBP_CUDA(cudaMemcpyAsync(h_uk.data(), d_uk, rows * S * 8, cudaMemcpyDeviceToHost, st));
+    HBP_CUDA(cudaMemcpyAsync(h_um.data(), d_um, rows * S * 4, cudaMemcpyDeviceToHost, st));
+    HBP_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < ns; ++j) {
+      hbp_set_result &r = out->sets[base + j];
+      std::memset(&r, 0, sizeof(r));
+      const int it = h_ri[j];
+      r.iterations = it;
+      r.converged = h_rs[j] == 1;
+      std::memcpy(&r.last_delta, &h_db[(size_t)it * S + j], 8);
+      if (out->deltas)
+        for (int i = 1; i <= it; ++i)
+          std::memcpy(&out->deltas[(size_t)(base + j) * max_it + (i - 1)], &h_db[(size_t)i * S + j], 8);
+      if (h_rs[j] == 4) {
+        r.underflow_iteration = it;
+        const unsigned long long key = h_uk[(size_t)it * S + j];
+        if (key != ~0ull) {
+          const int kind = (int)(key >> 32);
+          const int32_t pos = (int32_t)(key & 0xffffffffu);
+          r.underflow_kind = kind == 0 ? 1 : 2;
+          r.underflow_index = kind == 0 ? L.vtof2canon[pos] : L.ftov2canon[pos];
+        } else {
+          r.underflow_kind = 3;
+          r.underflow_index = h_um[(size_t)it * S + j];
+        }
+      }
+    }
+    ++passes;
+  }
+  out->device_ms = dev_ms;
+  out->kernel_ms = ker_ms;
+  out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+  out->launches = (int32_t)launches;
+  out->passes = passes;
+  hbp::set_last_launches(launches);
+  return HBP_OK;
+}
+
+}  // extern "C"

@@ -182,6 +182,23 @@ class _Plan:
             device_ms=float(res.device_ms), updates_per_iteration=self.updates)
 
 
+class _Sweep:
+    def __init__(self, dg: "_DeviceGraph", capacity: int):
+        self.dg = dg
+        h = C.c_void_p()
+        st = _native.lib().hbp_sweep_create(dg.handle, int(capacity), C.byref(h))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_sweep_create")
+        self.handle = h
+        self.capacity = int(_native.lib().hbp_sweep_capacity(h))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _native.lib().hbp_sweep_destroy(h)
+            self.handle = None
+
+
 class _DeviceGraph:
     """Device layout of one FactorGraph plus its compiled plans."""
 
@@ -196,6 +213,7 @@ class _DeviceGraph:
             _raise_status(st, "hbp_graph_create")
         self.handle = h
         self._plans: "OrderedDict[int, tuple[weakref.ref, _Plan]]" = OrderedDict()
+        self._sweeps: dict = {}
 
     def plan(self, schedule: Schedule, graph: FactorGraph) -> _Plan:
         key = id(schedule)
@@ -209,7 +227,23 @@ class _DeviceGraph:
             self._plans.popitem(last=False)
         return p
 
+    def sweep(self, capacity: int = 0) -> "_Sweep":
+        """Multi-evidence sweep buffers for this graph (cached per capacity)."""
+        sw = self._sweeps.get(capacity)
+        if sw is None:
+            self._sweeps.clear()  # one set of sweep buffers per graph
+            sw = _Sweep(self, capacity)
+            self._sweeps[capacity] = sw
+        return sw
+
+    def parall_updates(self, graph: FactorGraph) -> int:
+        """sum |s_0| + |t_0| of the PARALL schedule: every edge plus every
+        slot of a non-unary factor (schedule.py:293-312)."""
+        deg = np.diff(np.asarray(graph.rowptr, dtype=np.int64))
+        return int(graph.num_edges + deg[deg > 1].sum())
+
     def __del__(self):
+        self._sweeps = {}
         self._plans = OrderedDict()
         h = getattr(self, "handle", None)
         if h:

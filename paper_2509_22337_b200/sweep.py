@@ -1,0 +1,226 @@
+"""Multi-evidence sweep: many evidence / feedback sets over one graph.
+
+The reference answers "what would the ranking be under feedback set j?" one
+set at a time: ``clamp_evidence`` per observed alarm, ``Strategy.compile`` on
+the clamped graph, ``run`` from uniform (``ranking.py:94-135``,
+``graph.py:189-200``, ``engine.py:531``). ``run_many`` answers it for many
+sets at once on the device: under PARALL, set j's result is bitwise identical
+to ``run(G_j, Strategy.parall().compile(G_j), options)`` with ``G_j`` the base
+graph clamped to set j's observations in order (csrc/sweep.cu explains why a
+shared CSR with per-set evidence codes is exact). Each set stops at its own
+convergence iteration.
+
+Other strategies have no shared-CSR form for every clamp pattern (an explicit
+SEQFIX order cannot even be recompiled after a clamp, schedule.py:184-185),
+so ``run_many`` materialises the clamped graph per set and runs it on the
+single-graph device executor -- the reference's own semantics, still on the
+GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from .engine import EngineOptions, UnderflowError, device_graph, run
+from .graph import FactorGraph, GraphError, clamp_evidence
+from .schedule import Strategy
+
+
+@dataclass
+class SweepResult:
+    """Per-set outputs of ``run_many`` (set j in row j)."""
+
+    iterations: np.ndarray                 # (n,) int32
+    converged: np.ndarray                  # (n,) bool
+    last_delta: np.ndarray                 # (n,) float64
+    deltas: Optional[list[list[float]]]    # per set, like InferenceResult.deltas
+    marginals: Optional[np.ndarray]        # (n, V, 2) float64 (P0, P1)
+    p1_select: Optional[np.ndarray]        # (n, len(select)) float64
+    ranked: Optional[np.ndarray]           # (n, topk) int32, -1 padded
+    select: Optional[np.ndarray]           # the selection (ascending variable ids)
+    errors: list[Optional[UnderflowError]] = field(default_factory=list)
+    updates_per_iteration: Optional[np.ndarray] = None  # (n,) sum|s_i| + |t_i| of G_j
+    device_ms: Optional[float] = None      # stream time of the sweep (all passes)
+    kernel_ms: Optional[float] = None      # persistent sweep kernel(s) only
+    launches: int = 0
+    passes: int = 0
+
+    def __len__(self) -> int:
+        return len(self.iterations)
+
+    def total_updates(self) -> int:
+        """Edge-message updates over all sets (cli.py:337-344 per set)."""
+        return int(np.dot(self.updates_per_iteration.astype(np.int64),
+                          self.iterations.astype(np.int64)))
+
+
+def _normalise_sets(graph: FactorGraph, evidence_sets) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Evidence sets -> (offsets, var, value). A set is an iterable of
+    (variable, observed) pairs or an (ids, labels) pair of arrays."""
+    offsets = [0]
+    var: list[int] = []
+    val: list[int] = []
+    for ev in evidence_sets:
+        if isinstance(ev, tuple) and len(ev) == 2 and all(isinstance(x, np.ndarray) for x in ev):
+            pairs = zip(ev[0].tolist(), ev[1].tolist())
+        else:
+            pairs = ev
+        for v, o in pairs:
+            v = int(v)
+            if not 0 <= v < graph.num_variables:
+                raise GraphError(f"variable {v} out of range")
+            var.append(v)
+            val.append(1 if bool(o) else 0)
+        offsets.append(len(var))
+    return (np.asarray(offsets, dtype=np.int64), np.asarray(var, dtype=np.int32),
+            np.asarray(val, dtype=np.int8))
+
+
+def _underflow(kind: int, idx: int, graph: FactorGraph) -> UnderflowError:
+    if kind == 1:
+        return UnderflowError(f"variable-to-factor message degenerated to zero mass at {idx} "
+                              "(contradictory evidence?)")
+    if kind == 2:
+        rp, ved = graph._var_csr()
+        inv = np.empty(len(ved), dtype=np.int64)
+        inv[ved] = np.arange(len(ved))
+        return UnderflowError(f"factor-to-variable message degenerated to zero mass at "
+                              f"{int(inv[idx])} (contradictory evidence?)")
+    return UnderflowError(f"marginal of variable {idx} degenerated to zero mass "
+                          "(contradictory evidence?)")
+
+
+def _is_parall(strategy) -> bool:
+    return strategy is None or getattr(strategy, "kind", None) == "PARALL"
+
+
+def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Strategy] = None,
+             options: Optional[EngineOptions] = None, *, marginals: bool = True,
+             deltas: bool = True, select: Optional[Sequence[int]] = None, topk: int = 0,
+             capacity: int = 0, device_out: Optional[dict] = None) -> SweepResult:
+    """Run every evidence set from uniform messages; see the module docstring.
+
+    select / topk: also return P1 of the selected variables (ascending ids)
+    and, if topk > 0, the top-k of the selection ranked like
+    ``rank_alarms(marginals, alarms, already_labeled=set's variables)``.
+    device_out: optional {"marginals"|"p1_select"|"ranked": tensor} device
+    buffers (anything with ``data_ptr()``) on the graph's GPU that receive
+    those outputs instead of host arrays (used by the multi-GPU gather).
+    """
+    options = options or EngineOptions()
+    options.validate()
+    if options.record_history:
+        raise ValueError("record_history is not supported by run_many")
+    off, var, val = _normalise_sets(graph, evidence_sets)
+    n = len(off) - 1
+    sel = None if select is None else np.ascontiguousarray(np.asarray(select, dtype=np.int32))
+    if sel is not None and len(sel) > 1 and np.any(np.diff(sel) <= 0):
+        raise ValueError("select must be strictly ascending variable ids")
+    if topk and sel is None:
+        raise ValueError("topk needs a selection (the alarm variables)")
+    if not _is_parall(strategy):
+        return _run_materialised(graph, off, var, val, strategy, options, marginals, deltas, sel,
+                                 topk)
+    device_out = device_out or {}
+    dg = device_graph(graph)
+    sw = dg.sweep(capacity)
+    V = graph.num_variables
+    res = (_native.SetResult * max(1, n))()
+    outs = _native.SweepOutputs()
+    outs.sets = C.cast(res, C.POINTER(_native.SetResult))
+    dl = np.zeros((n, options.max_iterations), dtype=np.float64) if deltas else None
+    outs.deltas = None if dl is None else _native.ptr(dl, C.c_double)
+    mg = None
+    if "marginals" in device_out:
+        outs.marginals = C.cast(C.c_void_p(device_out["marginals"].data_ptr()), _native.f64p)
+        outs.marginals_on_device = 1
+    elif marginals:
+        mg = np.empty((n, V, 2), dtype=np.float64)
+        outs.marginals = _native.ptr(mg, C.c_double)
+    p1 = rk = None
+    if sel is not None:
+        outs.num_select = len(sel)
+        outs.select = _native.ptr(sel, C.c_int32)
+        if "p1_select" in device_out:
+            outs.p1_select = C.cast(C.c_void_p(device_out["p1_select"].data_ptr()), _native.f64p)
+            outs.p1_on_device = 1
+        else:
+            p1 = np.empty((n, len(sel)), dtype=np.float64)
+            outs.p1_select = _native.ptr(p1, C.c_double)
+        if topk:
+            outs.topk = int(topk)
+            if "ranked" in device_out:
+                outs.ranked = C.cast(C.c_void_p(device_out["ranked"].data_ptr()), _native.i32p)
+                outs.ranked_on_device = 1
+            else:
+                rk = np.empty((n, topk), dtype=np.int32)
+                outs.ranked = _native.ptr(rk, C.c_int32)
+    ev = _native.Evidence(n, _native.ptr(off, C.c_int64), _native.ptr(var, C.c_int32),
+                          _native.ptr(val, C.c_int8))
+    opt = _native.Options(int(options.max_iterations), int(bool(options.normalize_messages)), 0,
+                          0, float(options.tolerance),
+                          float(options.time_limit) if options.time_limit else 0.0)
+    st = _native.lib().hbp_sweep_run(sw.handle, C.byref(opt), C.byref(ev), C.byref(outs))
+    if st != _native.HBP_OK:
+        if st == _native.HBP_EINVAL:
+            raise ValueError(f"hbp_sweep_run: {_native.last_error()}")
+        raise RuntimeError(f"hbp_sweep_run: {_native.last_error()}")
+    its = np.array([res[j].iterations for j in range(n)], dtype=np.int32)
+    errors: list[Optional[UnderflowError]] = []
+    for j in range(n):
+        k = res[j].underflow_kind
+        errors.append(None if k == 0 else _underflow(k, int(res[j].underflow_index), graph))
+    base_upd = dg.parall_updates(graph)
+    return SweepResult(
+        iterations=its,
+        converged=np.array([bool(res[j].converged) for j in range(n)]),
+        last_delta=np.array([res[j].last_delta for j in range(n)], dtype=np.float64),
+        deltas=None if dl is None else [dl[j, :its[j]].tolist() for j in range(n)],
+        marginals=mg, p1_select=p1, ranked=rk, select=sel, errors=errors,
+        updates_per_iteration=base_upd + np.diff(off),
+        device_ms=float(outs.device_ms), kernel_ms=float(outs.kernel_ms),
+        launches=int(outs.launches), passes=int(outs.passes))
+
+
+def _run_materialised(graph, off, var, val, strategy, options, want_marg, want_deltas, sel, topk):
+    """Non-PARALL strategies: clamp + compile + run per set on the device."""
+    from .ranking import AlarmSet, rank_alarms
+
+    n = len(off) - 1
+    its, conv, last, dls, margs, p1s, rks, errs, upd = [], [], [], [], [], [], [], [], []
+    for j in range(n):
+        cur = graph
+        for v, o in zip(var[off[j]:off[j + 1]].tolist(), val[off[j]:off[j + 1]].tolist()):
+            cur = clamp_evidence(cur, int(v), bool(o))
+        sched = strategy.compile(cur)
+        upd.append(sched.updates_per_iteration())
+        try:
+            r = run(cur, sched, options)
+        except UnderflowError as exc:
+            its.append(0), conv.append(False), last.append(np.nan), dls.append([])
+            margs.append(np.full((graph.num_variables, 2), np.nan))
+            errs.append(exc)
+            if sel is not None:
+                p1s.append(np.full(len(sel), np.nan))
+                rks.append(np.full(topk, -1, dtype=np.int32))
+            continue
+        its.append(r.iterations), conv.append(r.converged), last.append(r.last_delta)
+        dls.append(r.deltas), margs.append(r.marginals), errs.append(None)
+        if sel is not None:
+            p1s.append(r.marginals[sel, 1])
+            if topk:
+                alarms = AlarmSet(tuple(sel.tolist()), tuple([False] * len(sel)))
+                ranked = rank_alarms(r.marginals, alarms, var[off[j]:off[j + 1]].tolist())[:topk]
+                rks.append(np.array(ranked + [-1] * (topk - len(ranked)), dtype=np.int32))
+    return SweepResult(
+        iterations=np.array(its, dtype=np.int32), converged=np.array(conv, dtype=bool),
+        last_delta=np.array(last, dtype=np.float64), deltas=dls if want_deltas else None,
+        marginals=np.stack(margs) if want_marg and n else None,
+        p1_select=np.stack(p1s) if sel is not None and n else None,
+        ranked=np.stack(rks) if topk and n else None, select=sel, errors=errs,
+        updates_per_iteration=np.array(upd, dtype=np.int64))

@@ -1,0 +1,151 @@
+"""GPU parity of the multi-evidence sweep (csrc/sweep.cu) against the
+reference semantics: set j == run(clamp_evidence(G, set j), PARALL), bit for
+bit, checked through the C oracle and the reference's golden C5 sets."""
+
+import numpy as np
+import pytest
+
+from builders import random_graph
+from conftest import sha
+from oracle import orc
+import paper_2509_22337_b200 as P
+from paper_2509_22337_b200 import EngineOptions, Strategy, clamp_evidence, rank_alarms
+from paper_2509_22337_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def clamp_all(g, pairs):
+    for v, o in pairs:
+        g = clamp_evidence(g, int(v), bool(o))
+    return g
+
+
+def oracle_set(g, pairs, opts):
+    cur = clamp_all(g, pairs)
+    sched = Strategy.parall().compile(cur)
+    return orc.run(cur, sched.arrays(cur), opts.max_iterations, opts.tolerance,
+                   opts.normalize_messages, threads=4), sched
+
+
+def random_sets(rng, V, n, max_size=8, allow_dup=False):
+    sets = []
+    for _ in range(n):
+        k = int(rng.integers(0, max_size + 1))
+        vs = rng.choice(V, size=min(k, V), replace=allow_dup)
+        sets.append([(int(v), bool(rng.integers(0, 2))) for v in vs])
+    return sets
+
+
+def check_against_oracle(g, sets, opts, res):
+    for j, pairs in enumerate(sets):
+        o, sched = oracle_set(g, pairs, opts)
+        if o["underflow"] is not None:
+            assert res.errors[j] is not None, j
+            continue
+        assert res.errors[j] is None, (j, res.errors[j])
+        assert res.iterations[j] == o["iterations"], j
+        assert bool(res.converged[j]) == o["converged"], j
+        assert res.marginals[j].tobytes() == o["marginals"].tobytes(), j
+        assert np.asarray(res.deltas[j]).tobytes() == o["deltas"].tobytes(), j
+        assert res.updates_per_iteration[j] == sched.updates_per_iteration()
+
+
+@pytest.mark.parametrize("name", ["weblech", "hedc"])
+def test_sweep_bitwise_vs_oracle_baseline_graphs(name):
+    g, alarms = W.graph(name)
+    rng = np.random.default_rng(11)
+    sets = random_sets(rng, g.num_variables, 40)
+    sets[0] = []  # no evidence == plain run
+    opts = EngineOptions(1000, 1e-9)
+    res = P.run_many(g, sets, Strategy.parall(), opts)
+    check_against_oracle(g, sets, opts, res)
+    plain = P.run(g, Strategy.parall().compile(g), opts)
+    assert res.marginals[0].tobytes() == plain.marginals.tobytes()
+
+
+def test_sweep_random_graphs_all_options():
+    rng = np.random.default_rng(77)
+    for trial in range(30):
+        g = random_graph(rng, max_vars=14, max_factors=14, max_body=4, or_prob=0.5)
+        sets = random_sets(rng, g.num_variables, int(rng.integers(1, 70)), max_size=4,
+                           allow_dup=trial % 3 == 0)
+        opts = EngineOptions(max_iterations=int(rng.integers(1, 40)),
+                             tolerance=float(rng.choice([0.0, 1e-9, 1e-5])),
+                             normalize_messages=bool(trial % 5 != 2))
+        res = P.run_many(g, sets, None, opts)
+        check_against_oracle(g, sets, opts, res)
+
+
+def test_sweep_contradictory_evidence_is_a_per_set_underflow():
+    g, _ = W.graph("weblech")
+    v = 5
+    sets = [[(v, True)], [(v, True), (v, False)], []]
+    res = P.run_many(g, sets)
+    assert res.errors[0] is None and res.errors[2] is None
+    assert isinstance(res.errors[1], P.UnderflowError)
+    o, _ = oracle_set(g, sets[1], EngineOptions())
+    assert o["underflow"] is not None and o["underflow"][0] == 3  # marginal, like the reference
+
+
+def test_sweep_passes_equal_single_pass():
+    g, _ = W.graph("hedc")
+    rng = np.random.default_rng(5)
+    sets = random_sets(rng, g.num_variables, 70)
+    a = P.run_many(g, sets, capacity=32)
+    assert a.passes == 3
+    b = P.run_many(g, sets, capacity=96)
+    assert b.passes == 1
+    assert a.marginals.tobytes() == b.marginals.tobytes()
+    assert (a.iterations == b.iterations).all()
+
+
+def test_sweep_selection_and_device_ranking():
+    g, alarms = W.graph("avrora")
+    rng = np.random.default_rng(9)
+    ids = np.asarray(alarms.alarms)
+    labels = np.asarray(alarms.labels)
+    sets = []
+    for j in range(24):
+        pick = np.sort(rng.choice(len(ids), 8, replace=False))
+        sets.append(list(zip(ids[pick].tolist(), labels[pick].tolist())))
+    sel = np.sort(ids)
+    res = P.run_many(g, sets, select=sel, topk=50)
+    for j, pairs in enumerate(sets):
+        assert res.p1_select[j].tobytes() == res.marginals[j][sel, 1].tobytes()
+        want = rank_alarms(res.marginals[j], alarms, [v for v, _ in pairs])[:50]
+        assert res.ranked[j].tolist() == want, j
+
+
+def test_sweep_golden_c5_sets(golden):
+    g, alarms = W.graph("ftp")
+    sets = [W.evidence_set(alarms, j) for j in range(4)]
+    sel = np.sort(np.asarray(alarms.alarms))
+    res = P.run_many(g, sets, Strategy.parall(), EngineOptions(1000, 1e-9), select=sel, topk=100)
+    for j in range(4):
+        want = golden["sweep"][str(j)]
+        assert res.iterations[j] == want["iterations"]
+        assert sha(res.marginals[j]) == want["marginals_sha"]
+        ranked = res.ranked[j].tolist()
+        assert ranked[:10] == want["top10"]
+        assert sha(np.asarray(ranked[:100], dtype=np.int64)) == want["top100_sha"]
+
+
+def test_sweep_time_limit_and_max_iterations():
+    g, _ = W.graph("hedc")
+    sets = [[], [(1, True)]]
+    res = P.run_many(g, sets, options=EngineOptions(max_iterations=3, tolerance=0.0))
+    assert list(res.iterations) == [3, 3] and not res.converged.any()
+    res = P.run_many(g, sets, options=EngineOptions(max_iterations=1000, tolerance=0.0,
+                                                   time_limit=1e-6))
+    assert (res.iterations >= 1).all() and (res.iterations < 1000).all()
+
+
+def test_sweep_non_parall_strategy_materialises():
+    g, _ = W.graph("weblech")
+    sets = [[(3, True)], [(7, False), (9, True)]]
+    res = P.run_many(g, sets, Strategy.seqfix(), EngineOptions(1000, 1e-9))
+    for j, pairs in enumerate(sets):
+        cur = clamp_all(g, pairs)
+        r = P.run(cur, Strategy.seqfix().compile(cur), EngineOptions(1000, 1e-9))
+        assert res.marginals[j].tobytes() == r.marginals.tobytes()
