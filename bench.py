@@ -1,30 +1,42 @@
 """Benchmark: edge-message updates/sec and time-to-convergence (BASELINE.json).
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c4|c4-seqfix|sweep]
+                [--workload sweep|c4|c4-seqfix] [--sets 1024]
 
-Workload at N=1 (default ``c4``): configs[3] of BASELINE.json -- the
-ftp-scale synthetic graph (211,175 V / 476,915 E, SynthSpec(101583, 109592,
-8, 0)), PARALL schedule, tolerance 1e-9, run to convergence from uniform
-messages (23 iterations). A step is one full inference run.
+Default workload, every N: configs[4] of BASELINE.json -- the ftp-scale
+interactive-ranking sweep. The graph is SynthSpec(101583, 109592, 8, 0)
+(211,175 V / 476,915 E, pinned by sha256 in tests/test_synth.py); evidence
+set j clamps 8 alarms drawn with default_rng(j) to their ground-truth labels
+(SURVEY.md 8(d) C5); PARALL, tol 1e-9, every set run to its own convergence
+from uniform messages. The 1,024 sets are partitioned across the N ranks
+(contiguous slices, one GPU each, graph replicated, no per-iteration
+collective) and the per-set outputs -- iterations, P1 of the 8,152 alarms and
+the device top-100 alarm ranking -- are gathered to rank 0 with NCCL at the
+end of every step. A step is the whole sweep (strong scaling: total work
+fixed as N grows).
 
-  value       updates/s = (sum|s_i| + sum|t_i|) x iterations / device time,
-              the reference's own definition (cli.py:337-344), with the graph
-              and schedule resident on the device; device time = CUDA events
-              around the persistent kernel on its launch stream, summed over
-              the K steps. L2 is flushed (256 MiB write) between steps.
-  e2e         the same metric through the public API ``run(graph, schedule)``
-              with a fresh device layout every step: host layout build, H2D
-              upload of graph + schedule, the run, D2H of marginals + deltas.
-  roofline    algorithmic bytes per launch (iterations x B +
-              message init) / average kernel time vs the measured HBM copy
-              bandwidth (MEASURED_PEAKS.json).
-  cpu_baseline the C oracle (a bit-exact restatement of hornbp.engine.run)
-              single-threaded on a bounded sample of the same workload.
+  value       edge-message updates/s = sum over sets of (sum|s_i| + |t_i|) x
+              iterations (cli.py:337-344 per set) / device time of the step,
+              CUDA events on the stream the sweep and the gather run on, max
+              over ranks. Inputs (graph, evidence) resident in HBM. The
+              working set (~17 GB at N=1) is far larger than L2.
+  e2e         the same metric through the public API every step:
+              run_many (N=1) / run_many_distributed (N>1) with the evidence
+              lists on the host -- H2D of the evidence, the sweep, the gather,
+              D2H of the gathered results to rank 0 -- wall clock, max over ranks.
+  roofline    the persistent sweep kernel: algorithmic bytes per launch
+               / its CUDA-event duration, against the
+              measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline (rank 0, N=1) the C oracle, a bit-exact restatement of
+              hornbp's clamp + compile + run, one set per host core in
+              parallel, on a bounded sample of the same sets.
+  single_graph (rank 0, N=1) configs[3]: the ftp graph alone, PARALL, time
+              to convergence (the persistent single-graph executor).
 
---impl reference: times the reference CPU implementation of the path -- the
-C oracle port, all host threads -- on the same workload, rank 0 only.
-N > 1 (torchrun): the multi-evidence sweep (C5), sets sharded across ranks.
+--workload c4 / c4-seqfix: the single-graph line as the headline instead.
+--impl reference: the reference's CPU path (the C oracle port -- the
+reference is pure Python/numpy and cannot run on the GPU box), all host
+cores, on a bounded sample of the same sets; rank 0 only.
 """
 
 from __future__ import annotations
@@ -37,6 +49,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -45,6 +58,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "edge-message updates/sec and time-to-convergence on ftp-scale graph (477k edges)"
 UNIT = "edge-message updates/s"
+TOPK = 100
 
 
 def load_peaks() -> tuple[float, str]:
@@ -111,7 +125,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes_per_iteration(graph, updates: int) -> int:
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---- algorithmic bytes -------------------------------------------------
+
+def single_bytes_per_iteration(graph, updates: int) -> int:
     """16(|S|+|T|) message writes + 3*16*E message reads
     + 16*V marginal write/prev read + 8*E int32 indices + 4(V+1) + 4(F+1)
     rowptrs + 17*F factor params."""
@@ -119,101 +142,292 @@ def algorithmic_bytes_per_iteration(graph, updates: int) -> int:
     return 16 * updates + 48 * E + 16 * V + 8 * E + 4 * (V + 1) + 4 * (F + 1) + 17 * F
 
 
-def traffic_from_profile() -> float | None:
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        with open(path) as fh:
-            return float(json.load(fh)["dram_bytes_per_launch"])
-    except (OSError, KeyError, ValueError):
-        return None
+def sweep_set_bytes(graph, iterations: np.ndarray, max_iterations: int) -> np.ndarray:
+    """Algorithmic DRAM bytes the persistent sweep kernel moves for one set
+    that stops after n iterations (csrc/sweep.cu): factor side n times
+    (iteration 1 writes every ftov message and reads nothing; later ones read
+    and write the T non-unary slots), variable side n times (reads every ftov
+    message, the evidence byte and -- after the first -- the previous P0,
+    writes P0 and, unless the run hit max_iterations, the T vtof messages),
+    plus the row / twin / parameter indices shared by the 32 sets of a warp."""
+    V, F, E = graph.num_variables, graph.num_factors, graph.num_edges
+    deg = np.diff(np.asarray(graph.rowptr, dtype=np.int64))
+    T = int(deg[deg > 1].sum())
+    n = np.asarray(iterations, dtype=np.int64)
+    fac = 16 * E + (n - 1) * 32 * T
+    var = n * (16 * E + V + 8 * V) + (n - 1) * 8 * V + (n - (n == max_iterations)) * 16 * T
+    idx = n * ((4 * (V + 1) + 4 * E) + (4 * (F + 1) + 4 * E + 16 * F)) / 32.0
+    return fac + var + idx
 
 
-def dist_setup(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+# ---- reference arm -------------------------------------------------------------------------
+
+def oracle_sets(graph, sets, cores: int, max_it: int, tol: float):
+    """Run evidence sets on the C oracle, one single-threaded run per host
+    core concurrently (ctypes releases the GIL). Returns (updates, seconds)."""
+    from oracle import orc
+
+    def one(ev):
+        fg = orc.clamp(graph, ev[0], ev[1])
+        arrs = orc.parall_arrays(fg)
+        o = orc.run(fg, arrs, max_it, tol, threads=1)
+        return (len(arrs[1]) + len(arrs[3])) * o["iterations"]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        upd = sum(pool.map(one, sets))
+    return upd, time.perf_counter() - t0
 
 
-# ------------------------------------------------------------------------------------------
-# reference arm: the CPU implementation (C oracle port), all host threads
-
-def run_reference(args, workload: str) -> None:
-    world, rank, _ = dist_setup(args)
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import orc
     from paper_2509_22337_b200 import workloads as W
 
-    key = "C4-SEQFIX" if workload == "c4-seqfix" else "C4-PARALL"
-    w = W.build(key)
-    sched = w.strategy.compile(w.graph)
-    arrs = sched.arrays(w.graph)
     cores = os.cpu_count() or 1
-    upd = sched.updates_per_iteration()
-    for _ in range(args.warmup):
-        orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
-    times, iters = [], []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        o = orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
-        times.append(time.perf_counter() - t0)
-        iters.append(o["iterations"])
-    total = sum(times)
-    value = upd * sum(iters) / total
+    if args.workload in ("c4", "c4-seqfix"):
+        key = "C4-SEQFIX" if args.workload == "c4-seqfix" else "C4-PARALL"
+        w = W.build(key)
+        sched = w.strategy.compile(w.graph)
+        arrs = sched.arrays(w.graph)
+        upd = sched.updates_per_iteration()
+        for _ in range(args.warmup):
+            orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
+        times, iters = [], []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            o = orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
+            times.append(time.perf_counter() - t0)
+            iters.append(o["iterations"])
+        value = upd * sum(iters) / sum(times)
+        config = {"workload": f"{key}: ftp SynthSpec(101583,109592,8,0), {w.strategy.kind}, "
+                              f"tol {w.tolerance}, run to convergence",
+                  "iterations": iters[-1], "updates_per_iteration": upd}
+        sample = f"{args.steps} full {key} runs (C oracle, OpenMP over {cores} threads)"
+        ms = 1e3 * sum(times) / args.steps
+    else:
+        g, alarms = W.graph("ftp")
+        n = args.sets
+        per_step = cores  # one set per core per step: a bounded sample of the sweep
+        steps_sets = [[W.evidence_set(alarms, (k * per_step + i) % n) for i in range(per_step)]
+                      for k in range(args.warmup + args.steps)]
+        for k in range(args.warmup):
+            oracle_sets(g, steps_sets[k], cores, 1000, 1e-9)
+        tot_upd, tot_s = 0, 0.0
+        for k in range(args.warmup, args.warmup + args.steps):
+            u, s = oracle_sets(g, steps_sets[k], cores, 1000, 1e-9)
+            tot_upd += u
+            tot_s += s
+        value = tot_upd / tot_s
+        config = sweep_config(n, args.gpus)
+        sample = (f"{args.steps} steps x {per_step} evidence sets (sets "
+                  f"{args.warmup * per_step % n}..), one set per core, C oracle single-threaded runs")
+        ms = 1e3 * tot_s / args.steps
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{key}: ftp SynthSpec(101583,109592,8,0), "
-                               f"{w.strategy.kind}, tol {w.tolerance}, run to convergence",
-                   "iterations": iters[-1], "updates_per_iteration": upd},
-        "time_to_convergence_ms": 1e3 * total / args.steps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if args.workload == "sweep" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full {key} runs (C oracle, OpenMP)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------------------------------
-# our arm
-
-def l2_flush(torch, buf):
-    buf.fill_(1.0)
-
-
-def measure_l2_bandwidth(torch) -> float | None:
-    """Copy bandwidth with a 24 MiB working set (L2-resident), GB/s read+write."""
-    try:
-        n = 24 << 20
-        a = torch.empty(n // 4, dtype=torch.float32, device="cuda")
-        b = torch.empty_like(a)
-        for _ in range(5):
-            b.copy_(a)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        s.record()
-        reps = 200
-        for _ in range(reps):
-            b.copy_(a)
-        e.record()
-        torch.cuda.synchronize()
-        return 2 * n * reps / (s.elapsed_time(e) * 1e-3) / 1e9
-    except Exception:  # noqa: BLE001
-        return None
+def sweep_config(n_sets: int, n_gpus: int) -> dict:
+    return {"workload": f"C5 ftp interactive-ranking sweep: {n_sets} evidence sets x 8 clamped "
+                        "alarms over SynthSpec(101583,109592,8,0) (211,175 V / 476,915 E), "
+                        "PARALL, tol 1e-9, each set to its own convergence from uniform",
+            "sets": n_sets, "evidence_per_set": 8, "outputs": f"iterations + P1 of 8,152 alarms "
+            f"+ device top-{TOPK} ranking per set, NCCL-gathered to rank 0",
+            "parallelism": f"sets sharded over {n_gpus} GPU(s), graph replicated",
+            "l2": "working set > L2 (17 GB of messages at N=1); no flush needed"}
 
 
-def run_ours_single(args, workload: str) -> None:
+# ---- our arm: the sweep ------------------------------------------------------------------------
+
+def run_ours_sweep(args) -> None:
     import torch
+    import torch.distributed as dist
+
+    import paper_2509_22337_b200 as P
+    from paper_2509_22337_b200 import distributed as D
+    from paper_2509_22337_b200 import workloads as W
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    P.engine.set_device(local)
+    multi = world > 1
+    if multi:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    g, alarms = W.graph("ftp")
+    n = args.sets
+    sets = [W.evidence_set(alarms, j) for j in range(n)]
+    sel = np.sort(np.asarray(alarms.alarms, dtype=np.int32))
+    lo, hi = D.partition(n, world, rank)
+    mine = sets[lo:hi]
+    m = hi - lo
+    opts = P.EngineOptions(1000, 1e-9)
+    p1 = torch.empty((m, len(sel)), dtype=torch.float64, device=dev)
+    rk = torch.empty((m, TOPK), dtype=torch.int32, device=dev)
+    dg = P.engine.device_graph(g)
+    stream = torch.cuda.current_stream(dev)
+    dg.set_stream(stream)
+
+    def step():
+        r = P.run_many(g, mine, None, opts, marginals=False, deltas=False, select=sel, topk=TOPK,
+                       device_out={"p1_select": p1, "ranked": rk})
+        if multi:
+            D.gather_rows(torch, dist, p1, n, world, rank)
+            D.gather_rows(torch, dist, rk, n, world, rank)
+            st = torch.as_tensor(r.iterations, device=dev).reshape(-1, 1)
+            D.gather_rows(torch, dist, st, n, world, rank)
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    if multi:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    upd_local = sum(r.total_updates() for r in results)
+    kernel_ms = [r.kernel_ms for r in results]
+    launches = sum(r.launches for r in results) + (3 * args.steps if multi else 0)
+    t = torch.tensor([ms, float(upd_local)], dtype=torch.float64, device=dev)
+    if multi:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t[1:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, upd_total = float(mx.item()), float(sm.item())
+    else:
+        ms_max, upd_total = ms, float(upd_local)
+    value = upd_total / (ms_max * 1e-3)
+    dg.set_stream(None)
+
+    # parity of the benchmarked outputs against the reference's golden C5 sets
+    parity = None
+    if rank == 0:
+        try:
+            import hashlib
+            with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
+                gold = json.load(fh)["sweep"]
+            ok = True
+            for j in range(min(4, m)):
+                want = gold[str(j)]
+                ok &= int(results[-1].iterations[j]) == want["iterations"]
+                ok &= rk[j, :10].cpu().tolist() == want["top10"]
+                ok &= hashlib.sha256(rk[j].cpu().numpy().astype(np.int64).tobytes()
+                                     ).hexdigest() == want["top100_sha"]
+            parity = bool(ok)
+        except (OSError, KeyError):
+            pass
+
+    # ---- end to end through the public API (host evidence in, host results out) ----
+    e2e_s = []
+    h2d = d2h = 0
+    for i in range(args.warmup + args.steps):
+        if multi:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if multi:
+            out = D.run_many_distributed(g, sets, opts, select=sel, topk=TOPK)
+            upd_e2e = float(out.total_updates()) if rank == 0 else 0.0
+        else:
+            out = P.run_many(g, sets, None, opts, marginals=False, deltas=False, select=sel,
+                             topk=TOPK)
+            upd_e2e = float(out.total_updates())
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_s.append(dt)
+    tt = torch.tensor([sum(e2e_s)], dtype=torch.float64, device=dev)
+    if multi:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_value = upd_e2e * len(e2e_s) / float(tt.item())
+    nev = 8 * m
+    h2d = 8 * (m + 1) + 5 * nev + 4 * len(sel)
+    # per-set control words read back by every rank + (rank 0) the gathered results
+    max_it_seen = int(max(int(r.iterations.max()) for r in results)) if m else 0
+    ctrl = 8 * m + 20 * (max_it_seen + 2) * ((m + 31) // 32 * 32)
+    d2h = ctrl + (n * (8 * len(sel) + 4 * TOPK + 40) if rank == 0 else 0)
+
+    if rank != 0:
+        if multi:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the persistent sweep kernel (rank 0) ----
+    peak, peak_kind = load_peaks()
+    last = results[-1]
+    bytes_launch = float(sweep_set_bytes(g, last.iterations, 1000).sum())
+    achieved = bytes_launch / (statistics.mean(kernel_ms) * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tj = json.load(fh)
+        if tj.get("kernel") == "sweep_persistent" and tj.get("sets") == m:
+            traffic = float(tj["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": sweep_config(n, world),
+        "time_to_convergence_ms": ms_max / args.steps,
+        "iterations": {"min": int(last.iterations.min()), "max": int(last.iterations.max()),
+                       "mean": float(last.iterations.mean())},
+        "parity_vs_reference_golden": parity,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(tt.item()) / len(e2e_s),
+                "path": ("paper_2509_22337_b200.run_many_distributed" if multi else
+                         "paper_2509_22337_b200.run_many") + " with host evidence lists"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}), burst copy",
+                     "kernel": "hbp::sweep_persistent (rank 0's whole slice in one launch)",
+                     "bytes_per_launch": bytes_launch, "sets_per_launch": m,
+                     "kernel_ms": statistics.mean(kernel_ms)},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    if not multi:
+        cores = os.cpu_count() or 1
+        sample = [sets[j] for j in range(min(n, cores))]
+        u, s = oracle_sets(g, sample, cores, 1000, 1e-9)
+        line["cpu_baseline"] = {"value": u / s, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"sets 0..{len(sample) - 1}, one per core, C oracle "
+                                          "single-threaded runs (clamp + PARALL compile + run)"}
+        line["single_graph"] = measure_single(torch, "c4", steps=20, warmup=5)
+    print(json.dumps(line), flush=True)
+    if multi:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---- single graph (configs[3]) -------------------------------------------------------------
+
+def measure_single(torch, workload: str, steps: int, warmup: int) -> dict:
+    import ctypes as C
 
     import paper_2509_22337_b200 as P
     from paper_2509_22337_b200 import _native
     from paper_2509_22337_b200 import workloads as W
 
-    torch.cuda.set_device(0)
-    P.engine.set_device(0)
     key = "C4-SEQFIX" if workload == "c4-seqfix" else "C4-PARALL"
     w = W.build(key)
     g = w.graph
@@ -222,12 +436,9 @@ def run_ours_single(args, workload: str) -> None:
     upd = sched.updates_per_iteration()
     flush = torch.empty(256 << 20 >> 2, dtype=torch.float32, device="cuda")
     lib = _native.lib()
-
-    # ---- device-resident timing (graph + plan uploaded once) ----
     dg = P.engine.device_graph(g)
     plan = dg.plan(sched, g)
     copt = plan.options(opts)
-    import ctypes as C
 
     def step():
         res = _native.Result()
@@ -236,98 +447,99 @@ def run_ours_single(args, workload: str) -> None:
             raise RuntimeError(_native.last_error())
         return res
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     dev_ms, iters, launches = [], [], 0
     torch.cuda.synchronize()
-    with ClockSampler(0) as clk:
-        t_wall = time.perf_counter()
-        for _ in range(args.steps):
-            l2_flush(torch, flush)
-            torch.cuda.synchronize()
-            r = step()
-            dev_ms.append(r.device_ms)
-            iters.append(r.iterations)
-            launches += lib.hbp_last_launch_count()
+    for _ in range(steps):
+        flush.fill_(1.0)
         torch.cuda.synchronize()
-        wall = time.perf_counter() - t_wall
+        r = step()
+        dev_ms.append(r.device_ms)
+        iters.append(r.iterations)
+        launches += lib.hbp_last_launch_count()
     total_ms = sum(dev_ms)
     value = upd * sum(iters) / (total_ms * 1e-3)
-
-    # parity of the benchmarked run (bitwise vs oracle is in the tests; here: golden hash)
     res_check = P.run(g, sched, opts)
     parity = None
     try:
+        import hashlib
         with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
             gold = json.load(fh)["runs"][key]
-        import hashlib
         parity = (hashlib.sha256(res_check.marginals.tobytes()).hexdigest() == gold["marginals_sha"]
                   and res_check.iterations == gold["iterations"])
     except (OSError, KeyError):
         pass
-
-    # ---- end to end through the public API, fresh device layout per step ----
+    # end to end through run(): fresh device layout + plan every step
     e2e_s, e2e_iters = [], []
-    h2d = d2h = 0
-    for i in range(args.warmup + args.steps):
+    for i in range(warmup + steps):
         P.engine.clear_device_cache()
         t0 = time.perf_counter()
         r = P.run(g, sched, opts)
         dt = time.perf_counter() - t0
-        if i >= args.warmup:
+        if i >= warmup:
             e2e_s.append(dt)
             e2e_iters.append(r.iterations)
     E, V, F = g.num_edges, g.num_variables, g.num_factors
     s_off, s_e, t_off, t_e = sched.arrays(g)
-    # uploaded: slot words (2 x 8E), twins (2 x 4E), vorig 4V, factor params 16F, plan items + phases
     h2d = 16 * E + 8 * E + 4 * V + 16 * F + 4 * (len(s_e) + len(t_e)) + 64
     d2h = 16 * V + 8 * e2e_iters[-1]
-    e2e_value = upd * sum(e2e_iters) / sum(e2e_s)
-
-    # ---- roofline of the persistent kernel ----
     peak, peak_kind = load_peaks()
-    bpi = algorithmic_bytes_per_iteration(g, upd)
+    bpi = single_bytes_per_iteration(g, upd)
     bytes_per_launch = bpi * statistics.mean(iters) + 32 * E
     achieved = bytes_per_launch / (statistics.mean(dev_ms) * 1e-3) / 1e9
-    traffic = traffic_from_profile()
-
-    # ---- CPU baseline: oracle, one thread, bounded sample (one full run) ----
-    from oracle import orc
-
-    t0 = time.perf_counter()
-    o = orc.run(g, sched.arrays(g), w.max_iterations, w.tolerance, threads=1)
-    cpu_s = time.perf_counter() - t0
-    cpu_value = upd * o["iterations"] / cpu_s
-
-    l2 = measure_l2_bandwidth(torch)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{key}: ftp SynthSpec(101583,109592,8,0) "
-                               f"(211,175 V / 476,915 E), {w.strategy.kind}, tol {w.tolerance}, "
-                               "run to convergence from uniform messages",
-                   "iterations": iters[-1], "updates_per_iteration": upd,
-                   "k_batches": sched.num_batches, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": "single graph, 1 GPU"},
-        "time_to_convergence_ms": total_ms / args.steps,
-        "parity_vs_reference_golden": parity,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * statistics.mean(e2e_s),
+    return {
+        "workload": f"{key}: ftp SynthSpec(101583,109592,8,0), {w.strategy.kind}, "
+                    f"tol {w.tolerance}, to convergence, L2 flushed (256 MiB write) between runs",
+        "value": value, "unit": UNIT, "time_to_convergence_ms": total_ms / steps,
+        "iterations": iters[-1], "updates_per_iteration": upd, "k_batches": sched.num_batches,
+        "parity_vs_reference_golden": parity, "gpu_launches": launches,
+        "e2e": {"value": upd * sum(e2e_iters) / sum(e2e_s), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": 1e3 * statistics.mean(e2e_s),
                 "path": "paper_2509_22337_b200.run() with a fresh device layout every step"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": None,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "kernel": "hbp::lbp_persistent (whole run in one launch)",
-                     "bytes_per_launch": bytes_per_launch, "bytes_per_iteration": bpi,
-                     "l2_copy_gbs_measured": l2,
-                     "note": "single-graph working set (~28 MB) is L2-resident within a run"},
-        "cpu_baseline": {"value": cpu_value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"one full {key} run ({o['iterations']} iterations), "
-                                   "C oracle single-threaded"},
-        "clocks": clk.summary(),
-        "gpu_launches": launches,
-        "wall_s_timed_region": wall,
+                     "bytes_per_launch": bytes_per_launch,
+                     "note": "working set (~28 MB) is L2-resident within a run"},
+    }
+
+
+def run_ours_single(args) -> None:
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_2509_22337_b200 as P
+
+    P.engine.set_device(0)
+    with ClockSampler(0) as clk:
+        sg = measure_single(torch, args.workload, args.steps, args.warmup)
+    from oracle import orc
+    from paper_2509_22337_b200 import workloads as W
+
+    key = "C4-SEQFIX" if args.workload == "c4-seqfix" else "C4-PARALL"
+    w = W.build(key)
+    sched = w.strategy.compile(w.graph)
+    t0 = time.perf_counter()
+    o = orc.run(w.graph, sched.arrays(w.graph), w.max_iterations, w.tolerance, threads=1)
+    cpu_s = time.perf_counter() - t0
+    line = {
+        "metric": METRIC, "value": sg["value"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sg["time_to_convergence_ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": sg["workload"], "iterations": sg["iterations"],
+                   "updates_per_iteration": sg["updates_per_iteration"],
+                   "k_batches": sg["k_batches"], "parallelism": "single graph, 1 GPU"},
+        "time_to_convergence_ms": sg["time_to_convergence_ms"],
+        "parity_vs_reference_golden": sg["parity_vs_reference_golden"],
+        "e2e": sg["e2e"], "roofline": sg["roofline"],
+        "cpu_baseline": {"value": sched.updates_per_iteration() * o["iterations"] / cpu_s,
+                         "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"one full {key} run, C oracle single-threaded"},
+        "clocks": clk.summary(), "gpu_launches": sg["gpu_launches"],
     }
     print(json.dumps(line), flush=True)
 
@@ -335,22 +547,20 @@ def run_ours_single(args, workload: str) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c4", "c4-seqfix", "sweep"], default=None)
+    ap.add_argument("--workload", choices=["sweep", "c4", "c4-seqfix"], default="sweep")
+    ap.add_argument("--sets", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    workload = args.workload or ("c4" if args.gpus == 1 else "sweep")
     if args.impl == "reference":
-        run_reference(args, workload)
+        run_reference(args)
         return
-    if workload == "sweep":
-        from paper_2509_22337_b200 import sweep_bench
-
-        sweep_bench.main(args)
-        return
-    run_ours_single(args, workload)
+    if args.workload == "sweep":
+        run_ours_sweep(args)
+    else:
+        run_ours_single(args)
 
 
 if __name__ == "__main__":

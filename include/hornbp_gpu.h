@@ -96,6 +96,10 @@ typedef struct hbp_graph hbp_graph;
 
 hbp_status hbp_graph_create(const hbp_graph_desc *graph, int32_t device, hbp_graph **out);
 void hbp_graph_destroy(hbp_graph *g);
+/* Run this graph's work (runs, passes, sweeps) on an external CUDA stream
+ * (a cudaStream_t passed as void*, e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the graph's own stream. Calls stay host-synchronous. */
+hbp_status hbp_graph_set_stream(hbp_graph *g, void *stream);
 
 /* ---- compiled plan (device-resident level program) ---------------------------------- */
 

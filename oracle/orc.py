@@ -95,3 +95,44 @@ def run(graph, arrays, max_iterations: int = 1000, tolerance: float = 1e-9,
                 converged=bool(res.converged), last_delta=res.last_delta,
                 underflow=None if st == 0 else (res.underflow_kind, res.underflow_iteration,
                                                 res.underflow_index))
+
+
+# ---- restatements used by the reference arm of bench.py (sweep sets) ---------------------
+
+class FlatGraph:
+    """Plain-array factor graph (the attributes orc.run reads)."""
+
+    def __init__(self, num_variables, rowptr, vars_, kind, p1, p2):
+        self.num_variables = int(num_variables)
+        self.rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+        self.vars = np.ascontiguousarray(vars_, dtype=np.int32)
+        self.kind = np.ascontiguousarray(kind, dtype=np.int8)
+        self.p1 = np.ascontiguousarray(p1, dtype=np.float64)
+        self.p2 = np.ascontiguousarray(p2, dtype=np.float64)
+
+
+def clamp(graph, ids, labels) -> FlatGraph:
+    """clamp_evidence applied in order (graph.py:189-200): one appended
+    body-empty AND factor per observation, p1 = p2 = 1.0 (true) / 0.0 (false)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    p = np.where(np.asarray(labels, dtype=bool), 1.0, 0.0)
+    n = len(ids)
+    rp = np.asarray(graph.rowptr, dtype=np.int64)
+    return FlatGraph(graph.num_variables,
+                     np.concatenate([rp, rp[-1] + 1 + np.arange(n, dtype=np.int64)]),
+                     np.concatenate([np.asarray(graph.vars, dtype=np.int32), ids.astype(np.int32)]),
+                     np.concatenate([np.asarray(graph.kind, dtype=np.int8), np.zeros(n, np.int8)]),
+                     np.concatenate([np.asarray(graph.p1, dtype=np.float64), p]),
+                     np.concatenate([np.asarray(graph.p2, dtype=np.float64), p]))
+
+
+def parall_arrays(graph):
+    """Strategy.parall().compile(graph) as arrays: one batch, s_0 = every edge
+    in ascending EdgeId (schedule.py:271-272, the toposort of the empty
+    relation), t_0 = every slot of a non-unary factor (schedule.py:293-312)."""
+    rp = np.asarray(graph.rowptr, dtype=np.int64)
+    E = int(rp[-1])
+    deg = np.diff(rp)
+    s_e = np.arange(E, dtype=np.int32)
+    t_e = np.flatnonzero(np.repeat(deg > 1, deg)).astype(np.int32)
+    return (np.array([0, E], dtype=np.int64), s_e, np.array([0, len(t_e)], dtype=np.int64), t_e)

@@ -37,7 +37,8 @@ inline hbp_status upload(T **dst, const std::vector<T> &src, cudaStream_t s) {
 struct hbp_graph {
   hbp::HostLayout L;
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream all work of this graph runs on
+  cudaStream_t own_stream = nullptr;  // created with the graph
   int num_sms = 0, coop_blocks = 0, threads = 1024;
   const void *kernel = nullptr;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
@@ -63,7 +64,7 @@ struct hbp_graph {
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
 

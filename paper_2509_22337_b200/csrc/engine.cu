@@ -880,7 +880,8 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   if (st != HBP_OK) return st;
   g->device = device;
   HBP_CUDA(cudaSetDevice(device));
-  HBP_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  HBP_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  g->stream = g->own_stream;
   HBP_CUDA(cudaEventCreate(&g->ev0));
   HBP_CUDA(cudaEventCreate(&g->ev1));
   HBP_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -915,6 +916,15 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
 }
 
 void hbp_graph_destroy(hbp_graph *g) { delete g; }
+
+hbp_status hbp_graph_set_stream(hbp_graph *g, void *stream) {
+  if (!g) {
+    hbp::set_error("null graph");
+    return HBP_EINVAL;
+  }
+  g->stream = stream ? (cudaStream_t)stream : g->own_stream;
+  return HBP_OK;
+}
 
 hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to_vtof) {
   // reference layout (storage.py:55-63) recomputed from the device-side maps

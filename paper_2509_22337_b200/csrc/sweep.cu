@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -47,6 +48,7 @@ using namespace dev;
 
 constexpr int kSwWarps = 8;  // warps per CTA (blockDim = 256); lanes = 32 sets
 constexpr int kSwThreads = 32 * kSwWarps;
+constexpr int kSwMinBlocks = 4;  // default register budget: 4 CTAs (32 warps) per SM
 constexpr int kNoVar = 0x7f7f7f7f;  // ufmarg reset value (memset 0x7F)
 
 struct SweepParams {
@@ -55,12 +57,12 @@ struct SweepParams {
   const unsigned *ftov_twin;  // ftov slot -> vtof slot | kUnaryBit
   const double2 *fpar;        // per internal factor (p1, p2)
   const int *vorig;           // internal variable -> original id
-  int V, F, f_or_light, f_heavy, f_or_heavy;
+  int V, F, E, f_or_light, f_heavy, f_or_heavy;
   int S;                      // row stride (sets in this pass, multiple of 32)
   int nsets;                  // real sets in this pass
-  double2 *vtof, *ftov;       // [E][S]
-  double *p0;                 // [V][S] P(X=0) of the last marginal pass
-  const unsigned char *ev;    // [V][S] evidence code: bit0 observed false, bit1 observed true
+  double2 *vtof, *ftov;       // [S/32][E][32]
+  double *p0;                 // [S/32][V][32] P(X=0) of the last marginal pass
+  const unsigned char *ev;    // [S/32][V][32] evidence code: bit0 observed false, bit1 observed true
   // per-set control, [iteration][S]
   unsigned long long *dbits;  // |dP1| max, as ordered bits
   unsigned long long *ufkey;  // first underflowing message: kind << 32 | slot
@@ -100,7 +102,30 @@ __device__ __forceinline__ unsigned long long sw_globaltimer() {
   return t;
 }
 
-// ---- message output: normalise, record underflow (engine.py:155-165) ------------------------
+// ---- per-thread view of its set group ---------------------------------------------------
+// Arrays are tiled [group][row][32]: group g = sets 32g..32g+31, so a warp's
+// 32 lanes read one contiguous 512-byte segment per row and a node's d rows
+// are d consecutive segments (DRAM-page friendly streaming).
+
+struct SwLane {
+  double2 *vtof, *ftov;     // &X[g][0][lane]
+  double *p0;
+  const unsigned char *ev;
+  int s;                    // set index within the pass
+};
+
+__device__ __forceinline__ SwLane sw_lane(const SweepParams &P, int s, int E) {
+  const int g = s >> 5, lane = s & 31;
+  SwLane L;
+  L.vtof = P.vtof + (size_t)g * E * 32 + lane;
+  L.ftov = P.ftov + (size_t)g * E * 32 + lane;
+  L.p0 = P.p0 + (size_t)g * P.V * 32 + lane;
+  L.ev = P.ev + (size_t)g * P.V * 32 + lane;
+  L.s = s;
+  return L;
+}
+
+// ---- message output: normalise, record underflow (engine.py:155-165) ----------------------
 
 __device__ __forceinline__ void sw_put(const SweepParams &P, double2 *dst, double a0, double a1,
                                       unsigned kind, unsigned slot, unsigned long long &uf) {
@@ -127,39 +152,41 @@ __device__ __forceinline__ void sw_clamp(unsigned code, double &a0, double &a1) 
   }
 }
 
-// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572)
-__device__ __forceinline__ void sw_marginal(const SweepParams &P, int v, int s, int it, double q0,
-                                           double q1, unsigned long long &dmax) {
+// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572);
+// prev_p0 was loaded together with the row
+__device__ __forceinline__ void sw_marginal(const SweepParams &P, const SwLane &L, int v, int it,
+                                           double q0, double q1, double prev_p0,
+                                           unsigned long long &dmax) {
   const double t = add(q0, q1);
-  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + s], P.vorig[v]);
+  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], P.vorig[v]);
   const double p0 = div_rn(q0, t);
   const double p1 = sub(1.0, p0);
-  double *slot = P.p0 + (size_t)v * P.S + s;
-  const double prev = it == 2 ? 0.5 : sub(1.0, *slot);  // prev P1 starts at 0.5
+  const double prev = it == 2 ? 0.5 : sub(1.0, prev_p0);  // prev P1 starts at 0.5
   const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, prev));
   unsigned long long bits;
   asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
   dmax = bits > dmax ? bits : dmax;
-  *slot = p0;
+  L.p0[v * 32] = p0;
 }
 
 // ---- variable side: every outgoing vtof message of node v + its marginal ------------------
 
 template <int D>
-__device__ __forceinline__ void sw_var_fixed(const SweepParams &P, int v, int r, int s, int it,
-                                            bool write_vtof, unsigned long long &dmax,
+__device__ __forceinline__ void sw_var_fixed(const SweepParams &P, const SwLane &L, int v, int r,
+                                            int it, bool write_vtof, unsigned long long &dmax,
                                             unsigned long long &uf) {
-  const size_t S = (size_t)P.S;
+  // every load of the node first (one memory round trip), then the products
   double x0[D], x1[D];
   unsigned tw[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const double2 m = P.ftov[(size_t)(r + k) * S + s];
+    const double2 m = L.ftov[(r + k) * 32];
     x0[k] = m.x;
     x1[k] = m.y;
     tw[k] = __ldg(P.ftov_twin + r + k);
   }
-  const unsigned code = P.ev[(size_t)v * S + s];
+  const unsigned code = L.ev[v * 32];
+  const double prev_p0 = it > 2 ? L.p0[v * 32] : 0.5;
   double a0 = 1.0, a1 = 1.0;  // prefix x[0] * ... * x[j-1]: the reference's partial products
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -171,21 +198,21 @@ __device__ __forceinline__ void sw_var_fixed(const SweepParams &P, int v, int r,
         b1 = mul(b1, x1[k]);
       }
       if (code) sw_clamp(code, b0, b1);
-      sw_put(P, P.vtof + (size_t)tw[j] * S + s, b0, b1, 0u, tw[j], uf);
+      sw_put(P, L.vtof + tw[j] * 32, b0, b1, 0u, tw[j], uf);
     }
     a0 = mul(a0, x0[j]);
     a1 = mul(a1, x1[j]);
   }
   if (code) sw_clamp(code, a0, a1);
-  sw_marginal(P, v, s, it, a0, a1, dmax);
+  sw_marginal(P, L, v, it, a0, a1, prev_p0, dmax);
 }
 
-// rows longer than 8: per target, re-read the row (L1 hits), same left-to-right order
-__device__ __noinline__ void sw_var_long(const SweepParams &P, int v, int r, int d, int s, int it,
-                                         bool write_vtof, unsigned long long &dmax,
+// rows longer than 6: per target, re-read the row (L1 hits), same left-to-right order
+__device__ __noinline__ void sw_var_long(const SweepParams &P, const SwLane &L, int v, int r, int d,
+                                         int it, bool write_vtof, unsigned long long &dmax,
                                          unsigned long long &uf) {
-  const size_t S = (size_t)P.S;
-  const unsigned code = P.ev[(size_t)v * S + s];
+  const unsigned code = L.ev[v * 32];
+  const double prev_p0 = it > 2 ? L.p0[v * 32] : 0.5;
   if (write_vtof) {
     for (int j = 0; j < d; ++j) {
       const unsigned tw = __ldg(P.ftov_twin + r + j);
@@ -193,36 +220,35 @@ __device__ __noinline__ void sw_var_long(const SweepParams &P, int v, int r, int
       double b0 = 1.0, b1 = 1.0;
       for (int k = 0; k < d; ++k) {
         if (k == j) continue;
-        const double2 m = P.ftov[(size_t)(r + k) * S + s];
+        const double2 m = L.ftov[(r + k) * 32];
         b0 = mul(b0, m.x);
         b1 = mul(b1, m.y);
       }
       if (code) sw_clamp(code, b0, b1);
-      sw_put(P, P.vtof + (size_t)tw * S + s, b0, b1, 0u, tw, uf);
+      sw_put(P, L.vtof + tw * 32, b0, b1, 0u, tw, uf);
     }
   }
   double q0 = 1.0, q1 = 1.0;
   for (int k = 0; k < d; ++k) {
-    const double2 m = P.ftov[(size_t)(r + k) * S + s];
+    const double2 m = L.ftov[(r + k) * 32];
     q0 = mul(q0, m.x);
     q1 = mul(q1, m.y);
   }
   if (code) sw_clamp(code, q0, q1);
-  sw_marginal(P, v, s, it, q0, q1, dmax);
+  sw_marginal(P, L, v, it, q0, q1, prev_p0, dmax);
 }
 
-__device__ __forceinline__ void sw_var(const SweepParams &P, int v, int s, int it, bool write_vtof,
-                                      unsigned long long &dmax, unsigned long long &uf) {
-  const int r = __ldg(P.vrow + v);
-  const int d = __ldg(P.vrow + v + 1) - r;
+__device__ __forceinline__ void sw_var(const SweepParams &P, const SwLane &L, int v, int r, int d,
+                                      int it, bool write_vtof, unsigned long long &dmax,
+                                      unsigned long long &uf) {
   switch (d) {
-    case 1: sw_var_fixed<1>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    case 2: sw_var_fixed<2>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    case 3: sw_var_fixed<3>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    case 4: sw_var_fixed<4>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    case 5: sw_var_fixed<5>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    case 6: sw_var_fixed<6>(P, v, r, s, it, write_vtof, dmax, uf); break;
-    default: sw_var_long(P, v, r, d, s, it, write_vtof, dmax, uf); break;
+    case 1: sw_var_fixed<1>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    case 2: sw_var_fixed<2>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    case 3: sw_var_fixed<3>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    case 4: sw_var_fixed<4>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    case 5: sw_var_fixed<5>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    case 6: sw_var_fixed<6>(P, L, v, r, it, write_vtof, dmax, uf); break;
+    default: sw_var_long(P, L, v, r, d, it, write_vtof, dmax, uf); break;
   }
 }
 
@@ -233,9 +259,8 @@ __device__ __forceinline__ void sw_var(const SweepParams &P, int v, int s, int i
 // message is still the normalised uniform one.
 
 template <int D, int KIND>
-__device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r, int s, int it,
-                                            unsigned long long &uf) {
-  const size_t S = (size_t)P.S;
+__device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, const SwLane &L, int f, int r,
+                                            int it, unsigned long long &uf) {
   const double2 pp = __ldg(P.fpar + f);
   double m0[D], m1[D];
   int tw[D];
@@ -247,7 +272,7 @@ __device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r,
       m0[k] = c;
       m1[k] = c;
     } else {
-      const double2 m = P.vtof[(size_t)(r + k) * S + s];
+      const double2 m = L.vtof[(r + k) * 32];
       m0[k] = m.x;
       m1[k] = m.y;
     }
@@ -264,7 +289,7 @@ __device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r,
     }
     double o0, o1;
     head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    sw_put(P, P.ftov + (size_t)tw[0] * S + s, o0, o1, 1u, (unsigned)tw[0], uf);
+    sw_put(P, L.ftov + tw[0] * 32, o0, o1, 1u, (unsigned)tw[0], uf);
   }
   if (D > 1) {
     double a1, a2;
@@ -279,7 +304,7 @@ __device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r,
       }
       double o0, o1;
       body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-      sw_put(P, P.ftov + (size_t)tw[j] * S + s, o0, o1, 1u, (unsigned)tw[j], uf);
+      sw_put(P, L.ftov + tw[j] * 32, o0, o1, 1u, (unsigned)tw[j], uf);
       a1 = mul(a1, sm[j]);
       a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
     }
@@ -287,16 +312,15 @@ __device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, int f, int r,
 }
 
 template <int KIND>
-__device__ __noinline__ void sw_fac_long(const SweepParams &P, int f, int r, int d, int s, int it,
-                                         unsigned long long &uf) {
-  const size_t S = (size_t)P.S;
+__device__ __noinline__ void sw_fac_long(const SweepParams &P, const SwLane &L, int f, int r, int d,
+                                         int it, unsigned long long &uf) {
   const double2 pp = __ldg(P.fpar + f);
   const double c = P.normalize ? 0.5 : 1.0;
   for (int j = 0; j < d; ++j) {
     double b1 = 1.0, b2 = 1.0;
     for (int k = 0; k < d; ++k) {
       if (k == j) continue;
-      double2 m = it == 1 ? make_double2(c, c) : P.vtof[(size_t)(r + k) * S + s];
+      const double2 m = it == 1 ? make_double2(c, c) : L.vtof[(r + k) * 32];
       double f1, f2;
       if (k == 0) {
         head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
@@ -313,48 +337,50 @@ __device__ __noinline__ void sw_fac_long(const SweepParams &P, int f, int r, int
     else
       body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
     const int tw = __ldg(P.vtof_twin + r + j);
-    sw_put(P, P.ftov + (size_t)tw * S + s, o0, o1, 1u, (unsigned)tw, uf);
+    sw_put(P, L.ftov + tw * 32, o0, o1, 1u, (unsigned)tw, uf);
   }
 }
 
 template <int KIND>
-__device__ __forceinline__ void sw_fac_k(const SweepParams &P, int f, int r, int d, int s, int it,
-                                        unsigned long long &uf) {
+__device__ __forceinline__ void sw_fac_k(const SweepParams &P, const SwLane &L, int f, int r, int d,
+                                        int it, unsigned long long &uf) {
   switch (d) {
     case 1:  // prior / unary: a constant message, written once
-      if (it == 1) sw_fac_fixed<1, KIND>(P, f, r, s, it, uf);
+      if (it == 1) sw_fac_fixed<1, KIND>(P, L, f, r, it, uf);
       break;
-    case 2: sw_fac_fixed<2, KIND>(P, f, r, s, it, uf); break;
-    case 3: sw_fac_fixed<3, KIND>(P, f, r, s, it, uf); break;
-    case 4: sw_fac_fixed<4, KIND>(P, f, r, s, it, uf); break;
-    case 5: sw_fac_fixed<5, KIND>(P, f, r, s, it, uf); break;
-    default: sw_fac_long<KIND>(P, f, r, d, s, it, uf); break;
+    case 2: sw_fac_fixed<2, KIND>(P, L, f, r, it, uf); break;
+    case 3: sw_fac_fixed<3, KIND>(P, L, f, r, it, uf); break;
+    case 4: sw_fac_fixed<4, KIND>(P, L, f, r, it, uf); break;
+    case 5: sw_fac_fixed<5, KIND>(P, L, f, r, it, uf); break;
+    default: sw_fac_long<KIND>(P, L, f, r, d, it, uf); break;
   }
 }
 
-__device__ __forceinline__ void sw_fac(const SweepParams &P, int f, int s, int it,
-                                      unsigned long long &uf) {
-  const int r = __ldg(P.frow + f);
-  const int d = __ldg(P.frow + f + 1) - r;
+__device__ __forceinline__ void sw_fac(const SweepParams &P, const SwLane &L, int f, int r, int d,
+                                      int it, unsigned long long &uf) {
   const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
   if (!is_or)
-    sw_fac_k<0>(P, f, r, d, s, it, uf);
+    sw_fac_k<0>(P, L, f, r, d, it, uf);
   else
-    sw_fac_k<1>(P, f, r, d, s, it, uf);
+    sw_fac_k<1>(P, L, f, r, d, it, uf);
 }
 
 // ---- the persistent sweep kernel -----------------------------------------------------------
 // grid (NX, S/32), block 256 = 8 warps; lane = set blockIdx.y*32 + lane, warps
 // stride over nodes. Per iteration: [variable side: marginal(it-1) + delta +
 // vtof(it)] -> grid sync -> per-set stop decision -> [factor side: ftov(it)]
-// -> grid sync -> exit when every set has stopped.
+// -> grid sync -> exit when every set has stopped. The next node's row bounds
+// are fetched while the current node computes.
 
-__global__ void __launch_bounds__(kSwThreads, 4) sweep_persistent(const __grid_constant__ SweepParams P) {
+template <int MINB>
+__global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __grid_constant__ SweepParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int s = blockIdx.y * 32 + lane;
   const unsigned nblocks = gridDim.x * gridDim.y;
   const int wstride = gridDim.x * kSwWarps;
   const int w0 = blockIdx.x * kSwWarps + warp;
+  const int E = P.E;
+  const SwLane L = sw_lane(P, s, E);
   bool alive = s < P.nsets;
   unsigned expected = 0;
   __shared__ unsigned long long red[kSwWarps][32];
@@ -364,9 +390,22 @@ __global__ void __launch_bounds__(kSwThreads, 4) sweep_persistent(const __grid_c
     if (it >= 2) {
       const bool final_pass = it == P.max_it + 1;
       unsigned long long dmax = 0, uf = ~0ull;
-      if (__syncthreads_or(alive)) {
-        if (alive)
-          for (int v = w0; v < P.V; v += wstride) sw_var(P, v, s, it, !final_pass, dmax, uf);
+      if (__syncthreads_or(alive) && alive && w0 < P.V) {
+        int v = w0;
+        int r = __ldg(P.vrow + v), re = __ldg(P.vrow + v + 1);
+        while (true) {
+          const int vn = v + wstride;
+          int rn = 0, rne = 0;
+          if (vn < P.V) {
+            rn = __ldg(P.vrow + vn);
+            rne = __ldg(P.vrow + vn + 1);
+          }
+          sw_var(P, L, v, r, re - r, it, !final_pass, dmax, uf);
+          if (vn >= P.V) break;
+          v = vn;
+          r = rn;
+          re = rne;
+        }
       }
       red[warp][lane] = dmax;
       __syncthreads();
@@ -406,9 +445,22 @@ __global__ void __launch_bounds__(kSwThreads, 4) sweep_persistent(const __grid_c
     }
     {
       unsigned long long uf = ~0ull;
-      if (__syncthreads_or(alive)) {
-        if (alive)
-          for (int f = w0; f < P.F; f += wstride) sw_fac(P, f, s, it, uf);
+      if (__syncthreads_or(alive) && alive && w0 < P.F) {
+        int f = w0;
+        int r = __ldg(P.frow + f), re = __ldg(P.frow + f + 1);
+        while (true) {
+          const int fn = f + wstride;
+          int rn = 0, rne = 0;
+          if (fn < P.F) {
+            rn = __ldg(P.frow + fn);
+            rne = __ldg(P.frow + fn + 1);
+          }
+          sw_fac(P, L, f, r, re - r, it, uf);
+          if (fn >= P.F) break;
+          f = fn;
+          r = rn;
+          re = rne;
+        }
       }
       if (alive && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
     }
@@ -419,12 +471,16 @@ __global__ void __launch_bounds__(kSwThreads, 4) sweep_persistent(const __grid_c
 
 // ---- evidence table + outputs ----------------------------------------------------------------
 
+__device__ __forceinline__ size_t tile_pos(int row, int s, int rows) {
+  return ((size_t)(s >> 5) * rows + row) * 32 + (s & 31);
+}
+
 // ev[vinv[var]][set] |= 1 (false) / 2 (true); byte OR through the containing word
 __global__ void sweep_evidence_kernel(unsigned char *ev, const int *vinv, const int *ev_set,
-                                      const int *ev_var, const signed char *ev_val, int n, int S) {
+                                      const int *ev_var, const signed char *ev_val, int n, int V) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const size_t pos = (size_t)vinv[ev_var[i]] * S + ev_set[i];
+  const size_t pos = tile_pos(vinv[ev_var[i]], ev_set[i], V);
   const unsigned bit = ev_val[i] ? 2u : 1u;
   unsigned *word = (unsigned *)(ev + (pos & ~(size_t)3));
   atomicOr(word, bit << (8 * (pos & 3)));
@@ -433,7 +489,7 @@ __global__ void sweep_evidence_kernel(unsigned char *ev, const int *vinv, const 
 // out[set][k][2] = (P0, 1 - P0) of original variable sel[k] (sel == null: k itself);
 // 32 x 32 tiles: coalesced reads along sets, coalesced writes along variables
 __global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const int *sel, int nsel,
-                                       int S, int nsets, int set_base, double *out_pair,
+                                       int V, int nsets, int set_base, double *out_pair,
                                        double *out_p1) {
   __shared__ double tile[32][33];
   const int k0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
@@ -443,7 +499,7 @@ __global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const 
     double v = 0.0;
     if (k < nsel && s < nsets) {
       const int var = sel ? sel[k] : k;
-      v = p0[(size_t)vinv[var] * S + s];
+      v = p0[tile_pos(vinv[var], s, V)];
     }
     tile[r][tx] = v;
   }
@@ -468,7 +524,7 @@ __global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const 
 // positions index the id-sorted selection. Labeled = clamped in this set.
 __global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, const unsigned char *ev,
                                                            const int *vinv, const int *sel,
-                                                           int nsel, int npow2, int S,
+                                                           int nsel, int npow2, int V,
                                                            int set_base, int topk, int *ranked) {
   extern __shared__ unsigned char smem[];
   unsigned long long *key = (unsigned long long *)smem;
@@ -477,7 +533,7 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, cons
   for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
     unsigned long long k = ~0ull;
     if (i < nsel) {
-      const size_t at = (size_t)vinv[sel[i]] * S + s;
+      const size_t at = tile_pos(vinv[sel[i]], s, V);
       if (ev[at] == 0) {
         const double p1 = sub(1.0, p0[at]);
         k = ~(unsigned long long)__double_as_longlong(p1);
@@ -519,6 +575,7 @@ struct hbp_sweep {
   hbp_graph *g = nullptr;
   int cap = 0;           // sets per pass (multiple of 32)
   int grid_x_max = 0;    // co-resident CTAs for the cooperative launch
+  const void *kernel = nullptr;
   int *d_vinv = nullptr;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
   double *d_p0 = nullptr;
@@ -570,8 +627,15 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   sw->g = g;
   const hbp::HostLayout &L = g->L;
   int per_sm = 0;
-  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hbp::sweep_persistent,
-                                                         hbp::kSwThreads, 0));
+  {
+    // HBP_SWEEP_MINB: CTAs per SM the kernel is register-budgeted for (3 or 4)
+    const char *env = getenv("HBP_SWEEP_MINB");
+    const int minb = env ? atoi(env) : hbp::kSwMinBlocks;
+    sw->kernel = minb == 3 ? (const void *)hbp::sweep_persistent<3>
+               : minb == 2 ? (const void *)hbp::sweep_persistent<2>
+                           : (const void *)hbp::sweep_persistent<4>;
+  }
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kSwThreads, 0));
   sw->grid_x_max = std::max(1, per_sm) * g->num_sms;
   // capacity: requested, else what fits in half of the free memory
   const size_t per_set = (size_t)L.E * 32 + (size_t)L.V * 9;
@@ -713,6 +777,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.vorig = g->d_vorig;
   P.V = L.V;
   P.F = L.F;
+  P.E = (int)L.E;
   P.f_or_light = L.f_or_light;
   P.f_heavy = L.f_heavy;
   P.f_or_heavy = L.f_or_heavy;
@@ -763,7 +828,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       HBP_CUDA(cudaMemcpyAsync(d_ev_var, h_ev_var.data(), ne * 4, cudaMemcpyHostToDevice, st));
       HBP_CUDA(cudaMemcpyAsync(d_ev_val, h_ev_val.data(), ne, cudaMemcpyHostToDevice, st));
       hbp::sweep_evidence_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(
-          sw->d_ev, sw->d_vinv, d_ev_set, d_ev_var, d_ev_val, (int)ne, S);
+          sw->d_ev, sw->d_vinv, d_ev_set, d_ev_var, d_ev_val, (int)ne, L.V);
       ++launches;
     }
     // control reset
@@ -777,7 +842,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
-    HBP_CUDA(cudaLaunchCooperativeKernel((const void *)hbp::sweep_persistent, dim3(nx, groups),
+    HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups),
                                          dim3(hbp::kSwThreads), args, 0, st));
     HBP_CUDA(cudaEventRecord(sw->k1, st));
     ++launches;
@@ -786,7 +851,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       double *dst = marg_dev ? out->marginals : stage_marg;
       const int bbase = marg_dev ? base : 0;
       hbp::sweep_marginals_kernel<<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_vinv, nullptr, L.V, S, ns, bbase, dst, nullptr);
+          sw->d_p0, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
       ++launches;
       if (!marg_dev)
         HBP_CUDA(cudaMemcpyAsync(out->marginals + (size_t)base * L.V * 2, stage_marg,
@@ -796,7 +861,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       double *dst = p1_dev ? out->p1_select : stage_p1;
       const int bbase = p1_dev ? base : 0;
       hbp::sweep_marginals_kernel<<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_vinv, d_sel, nsel, S, ns, bbase, nullptr, dst);
+          sw->d_p0, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
       ++launches;
       if (!p1_dev)
         HBP_CUDA(cudaMemcpyAsync(out->p1_select + (size_t)base * nsel, stage_p1,
@@ -810,7 +875,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
         HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       hbp::sweep_rank_kernel<<<ns, 1024, smem, st>>>(sw->d_p0, sw->d_ev, sw->d_vinv, d_sel, nsel,
-                                                     std::max(npow2, 2), S, bbase, out->topk, dst);
+                                                     std::max(npow2, 2), L.V, bbase, out->topk, dst);
       ++launches;
       if (!rk_dev)
         HBP_CUDA(cudaMemcpyAsync(out->ranked + (size_t)base * out->topk, stage_rk,

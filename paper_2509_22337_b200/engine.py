@@ -227,6 +227,15 @@ class _DeviceGraph:
             self._plans.popitem(last=False)
         return p
 
+    def set_stream(self, stream) -> None:
+        """Run this graph's device work on an external stream (an int handle,
+        or anything with ``cuda_stream``, e.g. a torch.cuda.Stream); None =
+        the graph's own stream."""
+        handle = getattr(stream, "cuda_stream", stream)
+        st = _native.lib().hbp_graph_set_stream(self.handle, C.c_void_p(handle or None))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_graph_set_stream")
+
     def sweep(self, capacity: int = 0) -> "_Sweep":
         """Multi-evidence sweep buffers for this graph (cached per capacity)."""
         sw = self._sweeps.get(capacity)
