@@ -35,6 +35,7 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <string>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -58,6 +59,7 @@ struct SweepParams {
   const double2 *fpar;        // per internal factor (p1, p2)
   const int *vorig;           // internal variable -> original id
   int V, F, E, f_or_light, f_heavy, f_or_heavy;
+  int f_unary;                // internal factors [0, f_unary) are unary AND factors
   int S;                      // row stride (sets in this pass, multiple of 32)
   int nsets;                  // real sets in this pass
   double2 *vtof, *ftov;       // [S/32][E][32]
@@ -469,6 +471,502 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
   }
 }
 
+// ---- TMA-staged, warp-specialised sweep kernel (default) ------------------------------------
+// The persistent kernel above issues a node's loads and then computes, so a
+// warp has no memory in flight while it multiplies: HBM-latency bound at
+// ~54 % of peak (profiles/r1_sweep_ncu.md). Here each CTA streams its
+// contiguous, row-balanced node range through a 4-chunk shared-memory ring:
+// one producer warp cuts the range into chunks of <= 32 message rows / 16
+// nodes and fetches each chunk with 1-D bulk copies (cp.async.bulk -> UBLKCP,
+// completion counted on an mbarrier): the chunk's message rows (contiguous in
+// the [S/32][E][32] tiles), its row pointers and twins (16-byte aligned
+// windows), and per node the P0 / evidence rows (variable side) or the factor
+// parameters (factor side). Eight consumer warps take the chunk's nodes
+// round-robin, compute from shared memory exactly as before (same operation
+// order -> same bits) and release the slot through an "empty" mbarrier. The
+// producer runs up to four chunks ahead, so every SM keeps ~60 KB of loads in
+// flight regardless of how long the fp64 chains take.
+
+constexpr int kWsConsumers = 8;
+constexpr int kWsThreads = 32 * (kWsConsumers + 1);
+constexpr int kChR = 32;   // message rows per chunk
+constexpr int kChN = 16;   // nodes per chunk
+constexpr int kRing = 4;   // chunks in flight per CTA
+constexpr int kPad = 8;    // index arrays are padded so aligned windows stay in bounds
+
+struct __align__(16) WsChunk {
+  double2 msg[kChR][32];        // message rows of the chunk, one 512-byte row per slot
+  double p0[kChN][32];          // variable side: P0 of the previous iteration per node
+  unsigned char ev[kChN][32];   // variable side: evidence codes per node
+  double2 fpar[kChN];           // factor side: (p1, p2) per node
+  int rp[kChN + 8];             // row pointers, aligned window from (n0 & ~3)
+  int tw[kChR + 8];             // twins, aligned window from (r0 & ~3)
+  int n0, n1, r0, heavy;        // header written by the producer before arming
+};
+
+struct WsShared {
+  WsChunk ring[kRing];
+  unsigned long long full[kRing], empty[kRing];
+  unsigned long long red[kWsConsumers][32];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// variable node of degree D from shared memory (rows x[k*32], twins tw[k])
+template <int D, bool NORM>
+__device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane &L, int v,
+                                      const double2 *x, const int *tw, unsigned code,
+                                      double prev_p0, int it, bool write_vtof,
+                                      unsigned long long &dmax, unsigned long long &uf) {
+  double x0[D], x1[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double2 m = x[k * 32];
+    x0[k] = m.x;
+    x1[k] = m.y;
+  }
+  double a0 = 1.0, a1 = 1.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const unsigned t = (unsigned)tw[j];
+    if (write_vtof && !(t & kUnaryBit)) {
+      double b0 = a0, b1 = a1;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b0 = mul(b0, x0[k]);
+        b1 = mul(b1, x1[k]);
+      }
+      if (code) sw_clamp(code, b0, b1);
+      if (NORM) {
+        const double tt = add(b0, b1);
+        if (tt < kMinMessageSum) uf = min(uf, (unsigned long long)t);
+        div2_rn(b0, b1, tt, b0, b1);
+      }
+      L.vtof[t * 32] = make_double2(b0, b1);
+    }
+    a0 = mul(a0, x0[j]);
+    a1 = mul(a1, x1[j]);
+  }
+  if (code) sw_clamp(code, a0, a1);
+  sw_marginal(P, L, v, it, a0, a1, prev_p0, dmax);
+}
+
+// any degree, rows re-read per target (heavy nodes: global memory)
+template <bool NORM>
+__device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, int v,
+                                        const double2 *x, int d, const int *tw, unsigned code,
+                                        double prev_p0, int it, bool write_vtof,
+                                        unsigned long long &dmax, unsigned long long &uf) {
+  if (write_vtof) {
+    for (int j = 0; j < d; ++j) {
+      const unsigned t = (unsigned)tw[j];
+      if (t & kUnaryBit) continue;
+      double b0 = 1.0, b1 = 1.0;
+      for (int k = 0; k < d; ++k) {
+        if (k == j) continue;
+        const double2 m = x[k * 32];
+        b0 = mul(b0, m.x);
+        b1 = mul(b1, m.y);
+      }
+      if (code) sw_clamp(code, b0, b1);
+      if (NORM) {
+        const double tt = add(b0, b1);
+        if (tt < kMinMessageSum) uf = min(uf, (unsigned long long)t);
+        div2_rn(b0, b1, tt, b0, b1);
+      }
+      L.vtof[t * 32] = make_double2(b0, b1);
+    }
+  }
+  double q0 = 1.0, q1 = 1.0;
+  for (int k = 0; k < d; ++k) {
+    const double2 m = x[k * 32];
+    q0 = mul(q0, m.x);
+    q1 = mul(q1, m.y);
+  }
+  if (code) sw_clamp(code, q0, q1);
+  sw_marginal(P, L, v, it, q0, q1, prev_p0, dmax);
+}
+
+template <bool NORM>
+__device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double o1,
+                                      unsigned long long &uf) {
+  if (NORM) {
+    const double tt = add(o0, o1);
+    if (tt < kMinMessageSum) uf = min(uf, (1ull << 32) | (unsigned)t);
+    div2_rn(o0, o1, tt, o0, o1);
+  }
+  L.ftov[t * 32] = make_double2(o0, o1);
+}
+
+// factor node of degree D; FIRST: iteration 1 (every vtof message is uniform)
+template <int D, int KIND, bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_fac(const SwLane &L, const double2 *x, const int *tw,
+                                      double2 pp, unsigned long long &uf) {
+  double m0[D], m1[D];
+  const double c = NORM ? 0.5 : 1.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (FIRST) {
+      m0[k] = c;
+      m1[k] = c;
+    } else {
+      const double2 m = x[k * 32];
+      m0[k] = m.x;
+      m1[k] = m.y;
+    }
+  }
+  double sm[D];
+#pragma unroll
+  for (int k = 1; k < D; ++k) sm[k] = add(m0[k], m1[k]);
+  {
+    double h1 = 1.0, h2 = 1.0;
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+      h1 = mul(h1, sm[k]);
+      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
+    }
+    double o0, o1;
+    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
+    ws_put<NORM>(L, tw[0], o0, o1, uf);
+  }
+  if (D > 1) {
+    double a1, a2;
+    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+      double b1 = a1, b2 = a2;
+#pragma unroll
+      for (int k = j + 1; k < D; ++k) {
+        b1 = mul(b1, sm[k]);
+        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
+      }
+      double o0, o1;
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+      ws_put<NORM>(L, tw[j], o0, o1, uf);
+      a1 = mul(a1, sm[j]);
+      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
+    }
+  }
+}
+
+template <int KIND, bool NORM, bool FIRST>
+__device__ __noinline__ void ws_fac_any(const SwLane &L, const double2 *x, int d, const int *tw,
+                                        double2 pp, unsigned long long &uf) {
+  const double c = NORM ? 0.5 : 1.0;
+  for (int j = 0; j < d; ++j) {
+    double b1 = 1.0, b2 = 1.0;
+    for (int k = 0; k < d; ++k) {
+      if (k == j) continue;
+      const double2 m = FIRST ? make_double2(c, c) : x[k * 32];
+      double f1, f2;
+      if (k == 0) {
+        head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
+      } else {
+        f1 = add(m.x, m.y);
+        f2 = KIND == 0 ? m.y : m.x;
+      }
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
+    }
+    double o0, o1;
+    if (j == 0)
+      head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+    else
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+    ws_put<NORM>(L, tw[j], o0, o1, uf);
+  }
+}
+
+template <int KIND, bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int d, const int *tw,
+                                        double2 pp, unsigned long long &uf) {
+  switch (d) {
+    case 1: ws_fac<1, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 2: ws_fac<2, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 3: ws_fac<3, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 4: ws_fac<4, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 5: ws_fac<5, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    default: ws_fac_any<KIND, NORM, FIRST>(L, x, d, tw, pp, uf); break;
+  }
+}
+
+// first node whose row start is >= target (rows are nondecreasing)
+__device__ __forceinline__ int lower_node(const int *rowptr, int n, int target) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(rowptr + mid) < target)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Producer: stream nodes [nb, ne) of one phase through the ring.
+// side 0 = variables (rowptr vrow, rows ftov, + P0 rows if want_p0, + evidence),
+// side 1 = factors (rowptr frow, rows vtof unless FIRST, + factor parameters).
+__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, int side, int nb,
+                                           int ne, bool want_msg, bool want_p0, int g,
+                                           unsigned &seq) {
+  const int lane = threadIdx.x & 31;
+  const int *rowptr = side == 0 ? P.vrow : P.frow;
+  const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
+  const double2 *msg = (side == 0 ? P.ftov : P.vtof) + (size_t)g * P.E * 32;
+  const int rows_total = side == 0 ? P.V : P.F;
+  int n0 = nb;
+  int r0 = nb < ne ? __ldg(rowptr + n0) : 0;
+  while (n0 < ne) {
+    // chunk extent: the longest prefix of <= kChN nodes spanning <= kChR rows
+    const int i = n0 + 1 + lane;
+    const int ri = (lane < kChN && i <= ne) ? __ldg(rowptr + i) : 0x7fffffff;
+    const unsigned ok = __ballot_sync(0xffffffffu, ri - r0 <= kChR && lane < kChN && i <= ne);
+    int m = __popc(ok & ~(ok + 1));  // leading ones of a monotone mask
+    const int heavy = m == 0;
+    if (heavy) m = 1;
+    const int n1 = n0 + m;
+    const int r1 = __shfl_sync(0xffffffffu, ri, m - 1);
+    const unsigned slot = seq % kRing;
+    mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
+    if (lane == 0) {
+      WsChunk &c = sh.ring[slot];
+      c.n0 = n0;
+      c.n1 = n1;
+      c.r0 = r0;
+      c.heavy = heavy;
+      const int rp_lo = n0 & ~3, rp_hi = (n1 + 1 + 3) & ~3;
+      const int tw_lo = r0 & ~3, tw_hi = (r1 + 3) & ~3;
+      const unsigned b_rp = (rp_hi - rp_lo) * 4;
+      const unsigned b_tw = heavy ? 0u : (unsigned)(tw_hi - tw_lo) * 4;
+      const unsigned b_msg = (heavy || !want_msg) ? 0u : (unsigned)(r1 - r0) * 512;
+      const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 256 : 0u;
+      const unsigned b_ev = side == 0 ? (unsigned)m * 32 : 0u;
+      const unsigned b_fp = side == 1 ? (unsigned)m * 16 : 0u;
+      mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_msg + b_p0 + b_ev + b_fp);
+      bulk_g2s(c.rp, rowptr + rp_lo, b_rp, &sh.full[slot]);
+      if (b_tw) bulk_g2s(c.tw, twin + tw_lo, b_tw, &sh.full[slot]);
+      if (b_msg) bulk_g2s(c.msg, msg + (size_t)r0 * 32, b_msg, &sh.full[slot]);
+      if (b_p0) bulk_g2s(c.p0, P.p0 + ((size_t)g * P.V + n0) * 32, b_p0, &sh.full[slot]);
+      if (b_ev) bulk_g2s(c.ev, P.ev + ((size_t)g * P.V + n0) * 32, b_ev, &sh.full[slot]);
+      if (b_fp) bulk_g2s(c.fpar, P.fpar + n0, b_fp, &sh.full[slot]);
+    }
+    ++seq;
+    n0 = n1;
+    r0 = r1;
+  }
+  (void)rows_total;
+}
+
+template <bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &sh, const SwLane &L,
+                                               int cw, int nb, int ne, unsigned &seq,
+                                               unsigned long long &uf) {
+  const int lane = threadIdx.x & 31;
+  int n = nb;
+  while (n < ne) {
+    const unsigned slot = seq % kRing;
+    mbar_wait(&sh.full[slot], (seq / kRing) & 1);
+    const WsChunk &c = sh.ring[slot];
+    const int n0 = c.n0, n1 = c.n1, r0 = c.r0;
+    const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
+    for (int f = n0 + cw; f < n1; f += kWsConsumers) {
+      const int r = c.rp[f - rp_lo];
+      const int d = c.rp[f + 1 - rp_lo] - r;
+      if (!FIRST && d == 1) continue;  // unary: constant message, written in iteration 1
+      const double2 pp = c.fpar[f - n0];
+      const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
+      if (c.heavy) {
+        // rows not staged: read twins and messages from global memory
+        const int *tw = P.vtof_twin + r;
+        const double2 *x = L.vtof + (size_t)r * 32;
+        if (!is_or) ws_fac_any<0, NORM, FIRST>(L, x, d, tw, pp, uf);
+        else ws_fac_any<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+      } else {
+        const int *tw = c.tw + (r - tw_lo);
+        const double2 *x = &c.msg[r - r0][lane];
+        if (!is_or) ws_fac_k<0, NORM, FIRST>(L, x, d, tw, pp, uf);
+        else ws_fac_k<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[slot]);
+    ++seq;
+    n = n1;
+  }
+}
+
+template <bool NORM>
+__device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &sh, const SwLane &L,
+                                               int cw, int nb, int ne, int it, bool write_vtof,
+                                               unsigned &seq, unsigned long long &dmax,
+                                               unsigned long long &uf) {
+  const int lane = threadIdx.x & 31;
+  int n = nb;
+  while (n < ne) {
+    const unsigned slot = seq % kRing;
+    mbar_wait(&sh.full[slot], (seq / kRing) & 1);
+    const WsChunk &c = sh.ring[slot];
+    const int n0 = c.n0, n1 = c.n1, r0 = c.r0;
+    const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
+    for (int v = n0 + cw; v < n1; v += kWsConsumers) {
+      const int r = c.rp[v - rp_lo];
+      const int d = c.rp[v + 1 - rp_lo] - r;
+      const unsigned code = c.ev[v - n0][lane];
+      const double prev_p0 = it > 2 ? c.p0[v - n0][lane] : 0.5;
+      if (c.heavy) {
+        ws_var_any<NORM>(P, L, v, L.ftov + (size_t)r * 32, d, (const int *)P.ftov_twin + r, code,
+                         prev_p0, it, write_vtof, dmax, uf);
+        continue;
+      }
+      const int *tw = c.tw + (r - tw_lo);
+      const double2 *x = &c.msg[r - r0][lane];
+      switch (d) {
+        case 1: ws_var<1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        case 2: ws_var<2, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        case 3: ws_var<3, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        case 4: ws_var<4, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        case 5: ws_var<5, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        case 6: ws_var<6, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+        default:
+          ws_var_any<NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, dmax, uf);
+          break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[slot]);
+    ++seq;
+    n = n1;
+  }
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(kWsThreads, 2) sweep_ws(const __grid_constant__ SweepParams P) {
+  extern __shared__ __align__(128) unsigned char ws_smem[];
+  WsShared &sh = *reinterpret_cast<WsShared *>(ws_smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool producer = warp == kWsConsumers;
+  const int g = blockIdx.y;
+  const int s = g * 32 + lane;
+  const unsigned nblocks = gridDim.x * gridDim.y;
+  const SwLane L = sw_lane(P, s, P.E);
+  bool alive = s < P.nsets;
+  unsigned expected = 0, seq = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kWsConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // row-balanced node ranges of this CTA (fixed for the whole run); the
+  // factor range skips the unary AND factors (their message never changes)
+  // after iteration 1 -- they are the first f_unary internal factors
+  const int x = blockIdx.x, nx = gridDim.x;
+  const int vb = lower_node(P.vrow, P.V, (int)((long long)P.E * x / nx));
+  const int ve = lower_node(P.vrow, P.V, (int)((long long)P.E * (x + 1) / nx));
+  const int fb = lower_node(P.frow, P.F, (int)((long long)P.E * x / nx));
+  const int fe = lower_node(P.frow, P.F, (int)((long long)P.E * (x + 1) / nx));
+  const int u0 = __ldg(P.frow + P.f_unary);
+  const int ub = lower_node(P.frow, P.F, u0 + (int)((long long)(P.E - u0) * x / nx));
+  const int ue = lower_node(P.frow, P.F, u0 + (int)((long long)(P.E - u0) * (x + 1) / nx));
+  __syncthreads();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
+
+  for (int it = 1;; ++it) {
+    if (it >= 2) {
+      const bool final_pass = it == P.max_it + 1;
+      unsigned long long dmax = 0, uf = ~0ull;
+      if (__syncthreads_or(alive)) {
+        if (producer) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          ws_produce(P, sh, 0, vb, ve, true, it > 2, g, seq);
+        } else {
+          ws_consume_var<NORM>(P, sh, L, warp, vb, ve, it, !final_pass, seq, dmax, uf);
+        }
+      }
+      if (!producer) sh.red[warp][lane] = dmax;
+      __syncthreads();
+      if (warp == 0) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][lane] > m ? sh.red[w][lane] : m;
+        if (alive) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + s], m);
+      }
+      if (alive && !producer && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
+        P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
+      sw_grid_sync(P.bar, expected, nblocks);
+      const int done = it - 1;
+      int stop = 0;
+      if (alive) {
+        const size_t i = (size_t)done * P.S + s;
+        const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
+        const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
+        const int um = ((const volatile int *)P.ufmarg)[i];
+        const int tf = ((const volatile int *)P.tflag)[done];
+        if (uk != ~0ull || um != kNoVar) stop = 4;
+        else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
+        else if (done == P.max_it) stop = 2;
+        else if (tf) stop = 3;
+      }
+      if (stop) {
+        alive = false;
+        if (blockIdx.x == 0 && warp == 0) {
+          P.res_it[s] = done;
+          P.res_stop[s] = stop;
+          atomicAdd(P.nstop, 1u);
+        }
+      }
+    }
+    {
+      unsigned long long uf = ~0ull;
+      if (__syncthreads_or(alive)) {
+        const bool first = it == 1;
+        const int nb = first ? fb : ub, ne = first ? fe : ue;
+        if (producer) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          ws_produce(P, sh, 1, nb, ne, !first, false, g, seq);
+        } else if (first) {
+          ws_consume_fac<NORM, true>(P, sh, L, warp, nb, ne, seq, uf);
+        } else {
+          ws_consume_fac<NORM, false>(P, sh, L, warp, nb, ne, seq, uf);
+        }
+      }
+      if (alive && !producer && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+    }
+    sw_grid_sync(P.bar, expected, nblocks);
+    if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
+  }
+}
+
 // ---- evidence table + outputs ----------------------------------------------------------------
 
 __device__ __forceinline__ size_t tile_pos(int row, int s, int rows) {
@@ -575,8 +1073,13 @@ struct hbp_sweep {
   hbp_graph *g = nullptr;
   int cap = 0;           // sets per pass (multiple of 32)
   int grid_x_max = 0;    // co-resident CTAs for the cooperative launch
-  const void *kernel = nullptr;
+  const void *kernel = nullptr, *kernel_nonorm = nullptr;
   int *d_vinv = nullptr;
+  int *d_vrow = nullptr, *d_frow = nullptr, *d_vtof_twin = nullptr;  // padded copies (kPad)
+  unsigned *d_ftov_twin = nullptr;
+  int f_unary = 0;
+  size_t smem = 0;
+  bool ws = true;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
   double *d_p0 = nullptr;
   unsigned char *d_ev = nullptr;
@@ -588,7 +1091,8 @@ struct hbp_sweep {
   ~hbp_sweep() {
     cudaSetDevice(g->device);
     for (void *p : {(void *)d_vinv, (void *)d_vtof, (void *)d_ftov, (void *)d_p0, (void *)d_ev,
-                    d_ctrl, d_scratch})
+                    d_ctrl, d_scratch, (void *)d_vrow, (void *)d_frow, (void *)d_vtof_twin,
+                    (void *)d_ftov_twin})
       if (p) cudaFree(p);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -628,14 +1132,28 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   const hbp::HostLayout &L = g->L;
   int per_sm = 0;
   {
-    // HBP_SWEEP_MINB: CTAs per SM the kernel is register-budgeted for (3 or 4)
-    const char *env = getenv("HBP_SWEEP_MINB");
-    const int minb = env ? atoi(env) : hbp::kSwMinBlocks;
-    sw->kernel = minb == 3 ? (const void *)hbp::sweep_persistent<3>
-               : minb == 2 ? (const void *)hbp::sweep_persistent<2>
-                           : (const void *)hbp::sweep_persistent<4>;
+    // HBP_SWEEP_KERNEL=plain selects the register-pipelined kernel (A/B
+    // comparison); the default is the TMA-staged warp-specialised one.
+    const char *kenv = getenv("HBP_SWEEP_KERNEL");
+    sw->ws = !(kenv && std::string(kenv) == "plain");
+    if (sw->ws) {
+      sw->smem = sizeof(hbp::WsShared);
+      sw->kernel = (const void *)hbp::sweep_ws<true>;
+      sw->kernel_nonorm = (const void *)hbp::sweep_ws<false>;
+      for (const void *k : {sw->kernel, sw->kernel_nonorm})
+        HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem));
+      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kWsThreads,
+                                                             sw->smem));
+    } else {
+      const char *env = getenv("HBP_SWEEP_MINB");
+      const int minb = env ? atoi(env) : hbp::kSwMinBlocks;
+      sw->kernel = minb == 3 ? (const void *)hbp::sweep_persistent<3>
+                 : minb == 2 ? (const void *)hbp::sweep_persistent<2>
+                             : (const void *)hbp::sweep_persistent<4>;
+      sw->kernel_nonorm = sw->kernel;
+      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kSwThreads, 0));
+    }
   }
-  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kSwThreads, 0));
   sw->grid_x_max = std::max(1, per_sm) * g->num_sms;
   // capacity: requested, else what fits in half of the free memory
   const size_t per_set = (size_t)L.E * 32 + (size_t)L.V * 9;
@@ -647,6 +1165,25 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   sw->cap = cap;
   hbp_status st;
   if ((st = upload(&sw->d_vinv, L.vinv, g->stream))) return st;
+  {
+    // index arrays padded so the producer's 16-byte aligned windows stay in bounds
+    auto padded = [](const std::vector<int32_t> &v, int32_t fill) {
+      std::vector<int32_t> o(v);
+      o.resize(v.size() + hbp::kPad, fill);
+      return o;
+    };
+    std::vector<int32_t> ft(L.ftov_twin.begin(), L.ftov_twin.end());
+    std::vector<int32_t> vt_pad = padded(L.vtof_twin, 0), ft_pad = padded(ft, 0);
+    std::vector<uint32_t> ft_pad_u(ft_pad.begin(), ft_pad.end());
+    if ((st = upload(&sw->d_vrow, padded(L.vrow, (int32_t)L.E), g->stream)) ||
+        (st = upload(&sw->d_frow, padded(L.frow, (int32_t)L.E), g->stream)) ||
+        (st = upload(&sw->d_vtof_twin, vt_pad, g->stream)) ||
+        (st = upload(&sw->d_ftov_twin, ft_pad_u, g->stream)))
+      return st;
+    int32_t fu = 0;
+    while (fu < L.f_or_light && L.frow[fu + 1] - L.frow[fu] == 1) ++fu;
+    sw->f_unary = fu;
+  }
   HBP_CUDA(cudaMalloc(&sw->d_vtof, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_p0, (size_t)std::max(1, L.V) * cap * sizeof(double)));
@@ -769,10 +1306,11 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   if (nsel) HBP_CUDA(cudaMemcpyAsync(d_sel, out->select, (size_t)nsel * 4, cudaMemcpyHostToDevice, st));
 
   hbp::SweepParams P{};
-  P.vrow = g->d_vrow;
-  P.frow = g->d_frow;
-  P.vtof_twin = g->d_vtof_twin;
-  P.ftov_twin = g->d_ftov_twin;
+  P.vrow = sw->d_vrow;
+  P.frow = sw->d_frow;
+  P.vtof_twin = sw->d_vtof_twin;
+  P.ftov_twin = sw->d_ftov_twin;
+  P.f_unary = sw->f_unary;
   P.fpar = g->d_fpar;
   P.vorig = g->d_vorig;
   P.V = L.V;
@@ -842,8 +1380,15 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
-    HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups),
-                                         dim3(hbp::kSwThreads), args, 0, st));
+    if (sw->ws) {
+      const int nxw = std::max(1, std::min(sw->grid_x_max / groups, (int)(L.E / (4 * hbp::kChR)) + 1));
+      HBP_CUDA(cudaLaunchCooperativeKernel(P.normalize ? sw->kernel : sw->kernel_nonorm,
+                                           dim3(nxw, groups), dim3(hbp::kWsThreads), args, sw->smem,
+                                           st));
+    } else {
+      HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups), dim3(hbp::kSwThreads), args,
+                                           0, st));
+    }
     HBP_CUDA(cudaEventRecord(sw->k1, st));
     ++launches;
     // outputs of this pass
