@@ -60,6 +60,8 @@ struct SweepParams {
   const int *vorig;           // internal variable -> original id
   int V, F, E, f_or_light, f_heavy, f_or_heavy;
   int f_unary;                // internal factors [0, f_unary) are unary AND factors
+  const int4 *vchunks, *fchunks;  // {n0, n1, r0, r1} node chunks (TMA-staged kernel)
+  int n_vchunks, n_fchunks, fchunk_nonunary;
   int S;                      // row stride (sets in this pass, multiple of 32)
   int nsets;                  // real sets in this pass
   double2 *vtof, *ftov;       // [S/32][E][32]
@@ -718,50 +720,42 @@ __device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int 
   }
 }
 
-// first node whose row start is >= target (rows are nondecreasing)
-__device__ __forceinline__ int lower_node(const int *rowptr, int n, int target) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(rowptr + mid) < target)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// Producer: stream nodes [nb, ne) of one phase through the ring.
-// side 0 = variables (rowptr vrow, rows ftov, + P0 rows if want_p0, + evidence),
-// side 1 = factors (rowptr frow, rows vtof unless FIRST, + factor parameters).
-__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, int side, int nb,
-                                           int ne, bool want_msg, bool want_p0, int g,
-                                           unsigned &seq) {
+// Producer: stream the chunks c = first, first + stride, ... < count of one
+// phase's chunk list through the ring. Chunks (host-built, hbp_sweep_create)
+// are runs of consecutive nodes with <= kChR rows and <= kChN nodes; a node
+// with more rows forms a "heavy" chunk whose rows stay in global memory.
+// Interleaving the chunks over the CTAs gives every CTA the same mix of
+// degrees, so the phases stay balanced without atomics.
+// side 0 = variables (ftov rows + P0 rows if want_p0 + evidence rows),
+// side 1 = factors (vtof rows unless iteration 1, + factor parameters).
+__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, int side,
+                                           const int4 *chunks, int first, int count, int stride,
+                                           bool want_msg, bool want_p0, int g, unsigned &seq) {
   const int lane = threadIdx.x & 31;
   const int *rowptr = side == 0 ? P.vrow : P.frow;
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
   const double2 *msg = (side == 0 ? P.ftov : P.vtof) + (size_t)g * P.E * 32;
-  const int rows_total = side == 0 ? P.V : P.F;
-  int n0 = nb;
-  int r0 = nb < ne ? __ldg(rowptr + n0) : 0;
-  while (n0 < ne) {
-    // chunk extent: the longest prefix of <= kChN nodes spanning <= kChR rows
-    const int i = n0 + 1 + lane;
-    const int ri = (lane < kChN && i <= ne) ? __ldg(rowptr + i) : 0x7fffffff;
-    const unsigned ok = __ballot_sync(0xffffffffu, ri - r0 <= kChR && lane < kChN && i <= ne);
-    int m = __popc(ok & ~(ok + 1));  // leading ones of a monotone mask
-    const int heavy = m == 0;
-    if (heavy) m = 1;
-    const int n1 = n0 + m;
-    const int r1 = __shfl_sync(0xffffffffu, ri, m - 1);
+  // descriptors of the next 32 chunks of this CTA, one per lane
+  int k = 0;
+  int4 desc = first + lane * stride < count ? __ldg(chunks + first + lane * stride)
+                                            : make_int4(0, 0, 0, 0);
+  for (int c = first; c < count; c += stride, ++k) {
+    if (k == 32) {
+      k = 0;
+      desc = c + lane * stride < count ? __ldg(chunks + c + lane * stride) : make_int4(0, 0, 0, 0);
+    }
+    const int n0 = __shfl_sync(0xffffffffu, desc.x, k), n1 = __shfl_sync(0xffffffffu, desc.y, k);
+    const int r0 = __shfl_sync(0xffffffffu, desc.z, k), r1 = __shfl_sync(0xffffffffu, desc.w, k);
     const unsigned slot = seq % kRing;
-    mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
     if (lane == 0) {
-      WsChunk &c = sh.ring[slot];
-      c.n0 = n0;
-      c.n1 = n1;
-      c.r0 = r0;
-      c.heavy = heavy;
+      mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
+      WsChunk &ch = sh.ring[slot];
+      const int m = n1 - n0;
+      const int heavy = r1 - r0 > kChR;
+      ch.n0 = n0;
+      ch.n1 = n1;
+      ch.r0 = r0;
+      ch.heavy = heavy;
       const int rp_lo = n0 & ~3, rp_hi = (n1 + 1 + 3) & ~3;
       const int tw_lo = r0 & ~3, tw_hi = (r1 + 3) & ~3;
       const unsigned b_rp = (rp_hi - rp_lo) * 4;
@@ -771,99 +765,104 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, i
       const unsigned b_ev = side == 0 ? (unsigned)m * 32 : 0u;
       const unsigned b_fp = side == 1 ? (unsigned)m * 16 : 0u;
       mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_msg + b_p0 + b_ev + b_fp);
-      bulk_g2s(c.rp, rowptr + rp_lo, b_rp, &sh.full[slot]);
-      if (b_tw) bulk_g2s(c.tw, twin + tw_lo, b_tw, &sh.full[slot]);
-      if (b_msg) bulk_g2s(c.msg, msg + (size_t)r0 * 32, b_msg, &sh.full[slot]);
-      if (b_p0) bulk_g2s(c.p0, P.p0 + ((size_t)g * P.V + n0) * 32, b_p0, &sh.full[slot]);
-      if (b_ev) bulk_g2s(c.ev, P.ev + ((size_t)g * P.V + n0) * 32, b_ev, &sh.full[slot]);
-      if (b_fp) bulk_g2s(c.fpar, P.fpar + n0, b_fp, &sh.full[slot]);
+      bulk_g2s(ch.rp, rowptr + rp_lo, b_rp, &sh.full[slot]);
+      if (b_tw) bulk_g2s(ch.tw, twin + tw_lo, b_tw, &sh.full[slot]);
+      if (b_msg) bulk_g2s(ch.msg, msg + (size_t)r0 * 32, b_msg, &sh.full[slot]);
+      if (b_p0) bulk_g2s(ch.p0, P.p0 + ((size_t)g * P.V + n0) * 32, b_p0, &sh.full[slot]);
+      if (b_ev) bulk_g2s(ch.ev, P.ev + ((size_t)g * P.V + n0) * 32, b_ev, &sh.full[slot]);
+      if (b_fp) bulk_g2s(ch.fpar, P.fpar + n0, b_fp, &sh.full[slot]);
     }
     ++seq;
-    n0 = n1;
-    r0 = r1;
   }
-  (void)rows_total;
 }
 
+// Consumers: node i of the phase's node stream goes to warp (i mod 8), so the
+// warps stay balanced across chunks of any size.
 template <bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &sh, const SwLane &L,
-                                               int cw, int nb, int ne, unsigned &seq,
+                                               int cw, int first, int count, int stride,
+                                               bool alive, unsigned &seq,
                                                unsigned long long &uf) {
   const int lane = threadIdx.x & 31;
-  int n = nb;
-  while (n < ne) {
+  int base = 0;
+  for (int c = first; c < count; c += stride) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk &c = sh.ring[slot];
-    const int n0 = c.n0, n1 = c.n1, r0 = c.r0;
+    const WsChunk &ch = sh.ring[slot];
+    const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    for (int f = n0 + cw; f < n1; f += kWsConsumers) {
-      const int r = c.rp[f - rp_lo];
-      const int d = c.rp[f + 1 - rp_lo] - r;
-      if (!FIRST && d == 1) continue;  // unary: constant message, written in iteration 1
-      const double2 pp = c.fpar[f - n0];
-      const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
-      if (c.heavy) {
-        // rows not staged: read twins and messages from global memory
-        const int *tw = P.vtof_twin + r;
-        const double2 *x = L.vtof + (size_t)r * 32;
-        if (!is_or) ws_fac_any<0, NORM, FIRST>(L, x, d, tw, pp, uf);
-        else ws_fac_any<1, NORM, FIRST>(L, x, d, tw, pp, uf);
-      } else {
-        const int *tw = c.tw + (r - tw_lo);
-        const double2 *x = &c.msg[r - r0][lane];
-        if (!is_or) ws_fac_k<0, NORM, FIRST>(L, x, d, tw, pp, uf);
-        else ws_fac_k<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+    const int start = (cw - base) & (kWsConsumers - 1);
+    if (alive) {
+      for (int f = n0 + start; f < n1; f += kWsConsumers) {
+        const int r = ch.rp[f - rp_lo];
+        const int d = ch.rp[f + 1 - rp_lo] - r;
+        if (!FIRST && d == 1) continue;  // unary: constant message, written in iteration 1
+        const double2 pp = ch.fpar[f - n0];
+        const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
+        if (ch.heavy) {
+          const int *tw = P.vtof_twin + r;
+          const double2 *x = L.vtof + (size_t)r * 32;
+          if (!is_or) ws_fac_any<0, NORM, FIRST>(L, x, d, tw, pp, uf);
+          else ws_fac_any<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+        } else {
+          const int *tw = ch.tw + (r - tw_lo);
+          const double2 *x = &ch.msg[r - r0][lane];
+          if (!is_or) ws_fac_k<0, NORM, FIRST>(L, x, d, tw, pp, uf);
+          else ws_fac_k<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+        }
       }
     }
+    base += n1 - n0;
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[slot]);
     ++seq;
-    n = n1;
   }
 }
 
 template <bool NORM>
 __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &sh, const SwLane &L,
-                                               int cw, int nb, int ne, int it, bool write_vtof,
-                                               unsigned &seq, unsigned long long &dmax,
-                                               unsigned long long &uf) {
+                                               int cw, int first, int count, int stride, int it,
+                                               bool write_vtof, bool alive, unsigned &seq,
+                                               unsigned long long &dmax, unsigned long long &uf) {
   const int lane = threadIdx.x & 31;
-  int n = nb;
-  while (n < ne) {
+  int base = 0;
+  for (int c = first; c < count; c += stride) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk &c = sh.ring[slot];
-    const int n0 = c.n0, n1 = c.n1, r0 = c.r0;
+    const WsChunk &ch = sh.ring[slot];
+    const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    for (int v = n0 + cw; v < n1; v += kWsConsumers) {
-      const int r = c.rp[v - rp_lo];
-      const int d = c.rp[v + 1 - rp_lo] - r;
-      const unsigned code = c.ev[v - n0][lane];
-      const double prev_p0 = it > 2 ? c.p0[v - n0][lane] : 0.5;
-      if (c.heavy) {
-        ws_var_any<NORM>(P, L, v, L.ftov + (size_t)r * 32, d, (const int *)P.ftov_twin + r, code,
-                         prev_p0, it, write_vtof, dmax, uf);
-        continue;
-      }
-      const int *tw = c.tw + (r - tw_lo);
-      const double2 *x = &c.msg[r - r0][lane];
-      switch (d) {
-        case 1: ws_var<1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        case 2: ws_var<2, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        case 3: ws_var<3, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        case 4: ws_var<4, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        case 5: ws_var<5, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        case 6: ws_var<6, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-        default:
-          ws_var_any<NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, dmax, uf);
-          break;
+    const int start = (cw - base) & (kWsConsumers - 1);
+    if (alive) {
+      for (int v = n0 + start; v < n1; v += kWsConsumers) {
+        const int r = ch.rp[v - rp_lo];
+        const int d = ch.rp[v + 1 - rp_lo] - r;
+        const unsigned code = ch.ev[v - n0][lane];
+        const double prev_p0 = it > 2 ? ch.p0[v - n0][lane] : 0.5;
+        if (ch.heavy) {
+          ws_var_any<NORM>(P, L, v, L.ftov + (size_t)r * 32, d, (const int *)P.ftov_twin + r, code,
+                           prev_p0, it, write_vtof, dmax, uf);
+          continue;
+        }
+        const int *tw = ch.tw + (r - tw_lo);
+        const double2 *x = &ch.msg[r - r0][lane];
+        switch (d) {
+          case 1: ws_var<1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          case 2: ws_var<2, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          case 3: ws_var<3, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          case 4: ws_var<4, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          case 5: ws_var<5, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          case 6: ws_var<6, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+          default:
+            ws_var_any<NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, dmax, uf);
+            break;
+        }
       }
     }
+    base += n1 - n0;
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[slot]);
     ++seq;
-    n = n1;
   }
 }
 
@@ -886,17 +885,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) sweep_ws(const __grid_constant_
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // row-balanced node ranges of this CTA (fixed for the whole run); the
-  // factor range skips the unary AND factors (their message never changes)
-  // after iteration 1 -- they are the first f_unary internal factors
   const int x = blockIdx.x, nx = gridDim.x;
-  const int vb = lower_node(P.vrow, P.V, (int)((long long)P.E * x / nx));
-  const int ve = lower_node(P.vrow, P.V, (int)((long long)P.E * (x + 1) / nx));
-  const int fb = lower_node(P.frow, P.F, (int)((long long)P.E * x / nx));
-  const int fe = lower_node(P.frow, P.F, (int)((long long)P.E * (x + 1) / nx));
-  const int u0 = __ldg(P.frow + P.f_unary);
-  const int ub = lower_node(P.frow, P.F, u0 + (int)((long long)(P.E - u0) * x / nx));
-  const int ue = lower_node(P.frow, P.F, u0 + (int)((long long)(P.E - u0) * (x + 1) / nx));
   __syncthreads();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
 
@@ -907,9 +896,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) sweep_ws(const __grid_constant_
       if (__syncthreads_or(alive)) {
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce(P, sh, 0, vb, ve, true, it > 2, g, seq);
+          ws_produce(P, sh, 0, P.vchunks, x, P.n_vchunks, nx, true, it > 2, g, seq);
         } else {
-          ws_consume_var<NORM>(P, sh, L, warp, vb, ve, it, !final_pass, seq, dmax, uf);
+          ws_consume_var<NORM>(P, sh, L, warp, x, P.n_vchunks, nx, it, !final_pass, alive, seq,
+                               dmax, uf);
         }
       }
       if (!producer) sh.red[warp][lane] = dmax;
@@ -950,14 +940,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) sweep_ws(const __grid_constant_
       unsigned long long uf = ~0ull;
       if (__syncthreads_or(alive)) {
         const bool first = it == 1;
-        const int nb = first ? fb : ub, ne = first ? fe : ue;
+        // after iteration 1 the unary factors' chunks are skipped (constant messages)
+        const int c0 = (first ? 0 : P.fchunk_nonunary) + x;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce(P, sh, 1, nb, ne, !first, false, g, seq);
+          ws_produce(P, sh, 1, P.fchunks, c0, P.n_fchunks, nx, !first, false, g, seq);
         } else if (first) {
-          ws_consume_fac<NORM, true>(P, sh, L, warp, nb, ne, seq, uf);
+          ws_consume_fac<NORM, true>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
         } else {
-          ws_consume_fac<NORM, false>(P, sh, L, warp, nb, ne, seq, uf);
+          ws_consume_fac<NORM, false>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
         }
       }
       if (alive && !producer && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
@@ -1078,6 +1069,8 @@ struct hbp_sweep {
   int *d_vrow = nullptr, *d_frow = nullptr, *d_vtof_twin = nullptr;  // padded copies (kPad)
   unsigned *d_ftov_twin = nullptr;
   int f_unary = 0;
+  int4 *d_vchunks = nullptr, *d_fchunks = nullptr;
+  int n_vchunks = 0, n_fchunks = 0, fchunk_nonunary = 0;
   size_t smem = 0;
   bool ws = true;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
@@ -1092,7 +1085,7 @@ struct hbp_sweep {
     cudaSetDevice(g->device);
     for (void *p : {(void *)d_vinv, (void *)d_vtof, (void *)d_ftov, (void *)d_p0, (void *)d_ev,
                     d_ctrl, d_scratch, (void *)d_vrow, (void *)d_frow, (void *)d_vtof_twin,
-                    (void *)d_ftov_twin})
+                    (void *)d_ftov_twin, (void *)d_vchunks, (void *)d_fchunks})
       if (p) cudaFree(p);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -1183,6 +1176,31 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
     int32_t fu = 0;
     while (fu < L.f_or_light && L.frow[fu + 1] - L.frow[fu] == 1) ++fu;
     sw->f_unary = fu;
+    // node chunks for the TMA-staged kernel: runs of consecutive nodes with
+    // <= kChR rows and <= kChN nodes (a node with more rows is a chunk alone);
+    // the factor list breaks at f_unary so iterations > 1 can skip the unary ones
+    auto chunks = [](const std::vector<int32_t> &row, int32_t n, int32_t brk,
+                     std::vector<int4> &out, int32_t *brk_chunk) {
+      int32_t n0 = 0;
+      while (n0 < n) {
+        if (n0 == brk) *brk_chunk = (int32_t)out.size();
+        int32_t n1 = n0 + 1;
+        while (n1 < n && n1 != brk && n1 - n0 < hbp::kChN && row[n1 + 1] - row[n0] <= hbp::kChR) ++n1;
+        out.push_back(make_int4(n0, n1, row[n0], row[n1]));
+        n0 = n1;
+      }
+      if (brk >= n) *brk_chunk = (int32_t)out.size();
+    };
+    std::vector<int4> vc, fc;
+    int32_t unused = 0, fnu = 0;
+    chunks(L.vrow, L.V, -1, vc, &unused);
+    chunks(L.frow, L.F, fu, fc, &fnu);
+    if (fu == 0) fnu = 0;
+    sw->n_vchunks = (int)vc.size();
+    sw->n_fchunks = (int)fc.size();
+    sw->fchunk_nonunary = fnu;
+    if ((st = upload(&sw->d_vchunks, vc, g->stream)) || (st = upload(&sw->d_fchunks, fc, g->stream)))
+      return st;
   }
   HBP_CUDA(cudaMalloc(&sw->d_vtof, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
@@ -1311,6 +1329,11 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.vtof_twin = sw->d_vtof_twin;
   P.ftov_twin = sw->d_ftov_twin;
   P.f_unary = sw->f_unary;
+  P.vchunks = sw->d_vchunks;
+  P.fchunks = sw->d_fchunks;
+  P.n_vchunks = sw->n_vchunks;
+  P.n_fchunks = sw->n_fchunks;
+  P.fchunk_nonunary = sw->fchunk_nonunary;
   P.fpar = g->d_fpar;
   P.vorig = g->d_vorig;
   P.V = L.V;
@@ -1381,7 +1404,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
     if (sw->ws) {
-      const int nxw = std::max(1, std::min(sw->grid_x_max / groups, (int)(L.E / (4 * hbp::kChR)) + 1));
+      const int nxw = std::max(1, std::min(sw->grid_x_max / groups, sw->n_vchunks));
       HBP_CUDA(cudaLaunchCooperativeKernel(P.normalize ? sw->kernel : sw->kernel_nonorm,
                                            dim3(nxw, groups), dim3(hbp::kWsThreads), args, sw->smem,
                                            st));
