@@ -43,6 +43,9 @@ constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 
 struct Ctrl {
   unsigned int bar;  // grid barrier arrivals (monotonic)
+  unsigned int pad0[31];
+  unsigned int gen;  // last completed sync point (own 128-byte line: polled, never atomically added)
+  unsigned int pad1[31];
   int iterations;
   int converged;
   int stop;          // 1 converged, 2 max_iterations, 3 time limit, 4 underflow
@@ -61,7 +64,13 @@ struct KParams {
   const int *vorig;           // internal variable -> original id
   int V, F, E, f_or_light, f_heavy, f_or_heavy;
   double2 *vtof, *ftov, *marg;
-  double *prev;
+  double *p0;                 // [V] P(X=0) of the last marginal pass (prev P1 = 1 - p0)
+  int marg_direct;            // 1: put_marginal also writes marg[orig] (single-pass API)
+  // degree classes of the light nodes (rows computed, not loaded):
+  // [vc_node[d], vc_node[d+1]) are the light variables of degree d, first row vc_row[d]
+  int vc_node[kNodeMax + 2], vc_row[kNodeMax + 2];
+  int fa_node[kNodeMax + 2], fa_row[kNodeMax + 2];  // light AND factors
+  int fo_node[kNodeMax + 2], fo_row[kNodeMax + 2];  // light OR factors
   // plan
   const Phase *phases;
   int nphases;
@@ -91,16 +100,29 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   return v;
 }
 
-__device__ __forceinline__ void bar_arrive(Ctrl *c) {
-  __syncthreads();
-  if (threadIdx.x == 0)  // release: the CTA's writes (ordered by bar.sync) before the arrival
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&c->bar) : "memory");
-}
+// Sync point k (counted identically by every CTA): arrivers add 1 to the
+// arrival counter; the arrival that reaches the point's cumulative target
+// publishes gen = k (release), and waiters spin on gen (acquire) -- a line
+// nobody adds to, so polling does not slow the arrivals down.
+struct Sync {
+  unsigned k = 0, target = 0;
+};
 
-__device__ __forceinline__ void bar_wait(Ctrl *c, unsigned target) {
+__device__ __forceinline__ void sync_point(Ctrl *c, Sync &s, unsigned arrivals, bool arrive,
+                                           bool wait) {
+  __syncthreads();
+  s.k += 1;
+  s.target += arrivals;
   if (threadIdx.x == 0) {
-    while (ld_acquire(&c->bar) < target) {
+    if (arrive) {
+      unsigned old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&c->bar) : "memory");
+      if (old + 1 == s.target)
+        asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(&c->gen), "r"(s.k) : "memory");
     }
+    if (wait)
+      while (ld_acquire(&c->gen) < s.k) {
+      }
   }
   __syncthreads();
 }
@@ -133,11 +155,11 @@ __device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsign
   }
 }
 
-// marginal of iteration it-1 + its |dP1| (engine.py:510-523, :572)
+// marginal of iteration it-1 + its |dP1| (engine.py:510-523, :572); prev_p0 and
+// orig are loaded by the caller together with the row
 __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
-                                             unsigned long long &dmax) {
+                                             unsigned long long &dmax, double prev_p0, int orig) {
   double t = add(q0, q1);
-  const int orig = P.vorig[v];
   if (t < kMinMessageSum) {
     atomicOr(&P.uf_marg[it - 1], 1);
     atomicMin(&P.uf_mwhere[it - 1], orig);
@@ -147,12 +169,13 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
   // |P1 - prev| as np.abs does it: clear the sign bit, keep any NaN payload
   // (integer AND in PTX: the compiler would otherwise turn it into an FP abs,
   // which canonicalises NaN payloads differently from numpy)
-  const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, P.prev[v]));
+  const unsigned long long raw =
+      (unsigned long long)__double_as_longlong(sub(p1, sub(1.0, prev_p0)));
   unsigned long long bits;
   asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
   dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
-  P.prev[v] = p1;
-  P.marg[orig] = make_double2(p0, p1);
+  P.p0[v] = p0;
+  if (P.marg_direct) P.marg[orig] = make_double2(p0, p1);
   if (P.hist) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
 }
 
@@ -205,16 +228,18 @@ __device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg,
   }
 }
 
+// uniform: iteration 1, phase 0 -- every factor-to-variable message is still
+// the initial (1, 1), so the products are exactly 1 and nothing is loaded
 __device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned tw, int write,
                                        bool want_marg, int it, int phase, unsigned long long &dmax,
-                                       unsigned long long &ufkey) {
+                                       unsigned long long &ufkey, bool uniform = false) {
   const int d = w.y >> 16, j = w.y & 0xffff;
   const bool marg = want_marg && j == 0;
   const bool wr = write > 0 || (write < 0 && !(tw & kUnaryBit));
   if (!wr && !marg) return;
   const int r = q - j;
   double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
-  switch (d) {
+  if (!uniform) switch (d) {
     case 1: v_row<1>(P, r, j, marg, a0, a1, q0, q1); break;
     case 2: v_row<2>(P, r, j, marg, a0, a1, q0, q1); break;
     case 3: v_row<3>(P, r, j, marg, a0, a1, q0, q1); break;
@@ -229,7 +254,7 @@ __device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned
     const int out = (int)(tw & ~kUnaryBit);
     put_message(P, P.vtof + out, a0, a1, phase, 0, out, ufkey);
   }
-  if (marg) put_marginal(P, w.x, q0, q1, it, dmax);
+  if (marg) put_marginal(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
 }
 
 // --------------------------------------------------------------------------------------
@@ -334,12 +359,18 @@ __device__ __forceinline__ void f_item(const KParams &P, int p, int2 w, int tw, 
 template <int D>
 __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool marg, bool vt,
                                             int it, int phase, unsigned long long &dmax,
-                                            unsigned long long &ufkey) {
+                                            unsigned long long &ufkey, bool uniform) {
   double x0[D], x1[D];
   unsigned tw[D];
+  double prev_p0 = 0.0;
+  int orig = 0;
+  if (marg) {  // issued with the row loads: one memory round trip per node
+    prev_p0 = P.p0[v];
+    orig = __ldg(P.vorig + v);
+  }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const double2 m = P.ftov[r + k];
+    const double2 m = uniform ? make_double2(1.0, 1.0) : P.ftov[r + k];
     x0[k] = m.x;
     x1[k] = m.y;
   }
@@ -362,21 +393,28 @@ __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool
     a0 = mul(a0, x0[j]);
     a1 = mul(a1, x1[j]);
   }
-  if (marg) put_marginal(P, v, a0, a1, it, dmax);
+  if (marg) put_marginal(P, v, a0, a1, it, dmax, prev_p0, orig);
 }
 
-
+// degree class of a light node: rows of class d are contiguous with stride d
+__device__ __forceinline__ void light_row(const int *cls_node, const int *cls_row, int n, int &r,
+                                          int &d) {
+  d = 1;
+#pragma unroll
+  for (int k = 2; k <= kNodeMax; ++k) d += n >= cls_node[k];
+  r = cls_row[d] + (n - cls_node[d]) * d;
+}
 
 __device__ __forceinline__ void vnode(const KParams &P, int v, bool marg, bool vt, int it,
                                       int phase, unsigned long long &dmax,
-                                      unsigned long long &ufkey) {
-  const int r = __ldg(P.vrow + v);
-  const int d = __ldg(P.vrow + v + 1) - r;
+                                      unsigned long long &ufkey, bool uniform) {
+  int r, d;
+  light_row(P.vc_node, P.vc_row, v, r, d);
   switch (d) {
-    case 1: vnode_fixed<1>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
-    case 2: vnode_fixed<2>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
-    case 3: vnode_fixed<3>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
-    default: vnode_fixed<4>(P, v, r, marg, vt, it, phase, dmax, ufkey); break;
+    case 1: vnode_fixed<1>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+    case 2: vnode_fixed<2>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+    case 3: vnode_fixed<3>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+    default: vnode_fixed<4>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
   }
 }
 
@@ -440,14 +478,17 @@ __device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, i
   }
 }
 
-__device__ __forceinline__ void fnode(const KParams &P, int f, int phase,
+// first: iteration 1 -- afterwards the unary factors' messages are constants
+__device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool first,
                                       unsigned long long &ufkey) {
-  const int r = __ldg(P.frow + f);
-  const int d = __ldg(P.frow + f + 1) - r;
-  if (f < P.f_or_light)
-    fnode_k<0>(P, f, r, d, phase, ufkey);
-  else
-    fnode_k<1>(P, f, r, d, phase, ufkey);
+  int r, d;
+  if (f < P.f_or_light) {
+    light_row(P.fa_node, P.fa_row, f, r, d);
+    if (d > 1 || first) fnode_k<0>(P, f, r, d, phase, ufkey);
+  } else {
+    light_row(P.fo_node, P.fo_row, f, r, d);
+    if (d > 1 || first) fnode_k<1>(P, f, r, d, phase, ufkey);
+  }
 }
 
 // --------------------------------------------------------------------------------------
@@ -492,11 +533,11 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
           const int i = c * 32 + lane;
           if (i >= total) break;
           if (i < nn) {
-            vnode(P, ph.begin + i, marg, do_vtof, it, pidx, dmax, ufkey);
+            vnode(P, ph.begin + i, marg, do_vtof, it, pidx, dmax, ufkey, it == 1 && pidx == 0);
           } else {
             const int q = ph.sbegin + (i - nn);
             v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
-                   pidx, dmax, ufkey);
+                   pidx, dmax, ufkey, it == 1 && pidx == 0);
           }
         }
     } else {
@@ -504,7 +545,7 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
         const int i = c * 32 + lane;
         if (i >= total) break;
         if (i < nn) {
-          fnode(P, ph.begin + i, pidx, ufkey);
+          fnode(P, ph.begin + i, pidx, it == 1, ufkey);
         } else {
           const int p = ph.sbegin + (i - nn);
           f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
@@ -540,7 +581,7 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
       int2 wn = make_int2(0, 0);
       unsigned twn = 0;
       if (i + stride < n) fetch(i + stride, qn, writen, wn, twn);
-      v_item(P, q, w, tw, do_vtof ? write : 0, marg, it, pidx, dmax, ufkey);
+      v_item(P, q, w, tw, do_vtof ? write : 0, marg, it, pidx, dmax, ufkey, it == 1 && pidx == 0);
       q = qn;
       write = writen;
       w = wn;
@@ -603,28 +644,41 @@ __device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int 
     P.trace[(((size_t)(it - 2) * P.nphases + p) * gridDim.x + blockIdx.x) * 2 + which] = globaltimer();
 }
 
+// marginals of the stopping iteration in the reference's variable order
+__device__ __forceinline__ void write_marginals(const KParams &P) {
+  const int gs = gridDim.x * blockDim.x;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < P.V; v += gs) {
+    const double p0 = P.p0[v];
+    P.marg[__ldg(P.vorig + v)] = make_double2(p0, sub(1.0, p0));
+  }
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
   const bool multi = gridDim.x > 1;
-  unsigned expected = 0;  // arrivals every CTA has seen so far (same on all CTAs)
+  const unsigned G = gridDim.x;
+  Sync sy;  // sync points passed so far (identical on every CTA)
+  // PARALL (two whole-graph phases): iteration 1 needs no initial messages --
+  // its variable side writes the normalised uniform message directly, and its
+  // factor side then writes every factor-to-variable message
+  const bool parall = P.nphases == 2 && P.phases[0].list == 2 && P.phases[1].list == 2;
+  auto grid_sync = [&]() {
+    if (multi) sync_point(C, sy, G, true, true);
+    else __syncthreads();
+  };
 
   // uniform start: all messages (1, 1), prev P1 = 0.5 (storage.py:91-94, engine.py:557)
   {
     const int gs = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.E; i += gs) {
-      P.vtof[i] = make_double2(1.0, 1.0);
-      P.ftov[i] = make_double2(1.0, 1.0);
-    }
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.prev[i] = 0.5;
+    if (!parall)
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.E; i += gs) {
+        P.vtof[i] = make_double2(1.0, 1.0);
+        P.ftov[i] = make_double2(1.0, 1.0);
+      }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.p0[i] = 0.5;
     if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
-    if (multi) {
-      bar_arrive(C);
-      expected += gridDim.x;
-      bar_wait(C, expected);
-    } else {
-      __syncthreads();
-    }
+    grid_sync();
   }
 
   for (int it = 1;; ++it) {
@@ -641,13 +695,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
           P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
       }
     }
-    if (multi) {
-      bar_arrive(C);
-      expected += gridDim.x;
-      bar_wait(C, expected);
-    } else {
-      __syncthreads();
-    }
+    grid_sync();
     // Stop decision for iteration it-1 (all CTAs passed the barrier, so the
     // flags and delta are final). With two phases per iteration (PARALL)
     // the decision is applied at the end of this iteration instead, so its
@@ -676,6 +724,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
           C->converged = s_stop == 1;
           C->stop = s_stop;
         }
+        write_marginals(P);
         return;
       }
     }
@@ -687,19 +736,13 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         if (!multi) {
           __syncthreads();
         } else if (prev_grid && ph.grid) {
-          bar_arrive(C);
-          expected += gridDim.x;
-          bar_wait(C, expected);
+          sync_point(C, sy, G, true, true);
         } else if (prev_grid && !ph.grid) {
-          bar_arrive(C);
-          expected += gridDim.x;
-          if (blockIdx.x == 0) bar_wait(C, expected);
+          sync_point(C, sy, G, true, blockIdx.x == 0);
         } else if (!prev_grid && !ph.grid) {
           if (blockIdx.x == 0) __syncthreads();
         } else {  // CTA 0 -> grid
-          if (blockIdx.x == 0) bar_arrive(C);
-          expected += 1;
-          bar_wait(C, expected);
+          sync_point(C, sy, 1, blockIdx.x == 0, true);
         }
       }
       unsigned long long unused = 0;
@@ -713,13 +756,9 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
       if (!multi) {
         __syncthreads();
       } else if (last_grid) {
-        bar_arrive(C);
-        expected += gridDim.x;
-        bar_wait(C, expected);
+        sync_point(C, sy, G, true, true);
       } else {
-        if (blockIdx.x == 0) bar_arrive(C);
-        expected += 1;
-        bar_wait(C, expected);
+        sync_point(C, sy, 1, blockIdx.x == 0, true);
       }
     }
     if (it > 1 && defer) {
@@ -731,6 +770,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
           C->converged = s_stop == 1;
           C->stop = s_stop;
         }
+        write_marginals(P);
         return;
       }
     }
@@ -790,6 +830,9 @@ void add_last_launches(int64_t n) { g_last_launches += n; }
 
 namespace {
 
+constexpr size_t kCtrlHeader = 512;
+static_assert(sizeof(hbp::Ctrl) <= kCtrlHeader, "control header");
+
 struct CtrlView {
   hbp::Ctrl *ctrl;
   unsigned long long *delta_bits, *uf_where;
@@ -800,7 +843,7 @@ CtrlView ctrl_view(void *base, size_t n) {
   CtrlView c;
   char *p = (char *)base;
   c.ctrl = (hbp::Ctrl *)p;
-  p += 256;
+  p += kCtrlHeader;
   c.delta_bits = (unsigned long long *)p;
   p += n * 8;
   c.uf_where = (unsigned long long *)p;
@@ -815,7 +858,7 @@ CtrlView ctrl_view(void *base, size_t n) {
   return c;
 }
 
-size_t ctrl_bytes(size_t n) { return 256 + n * (8 + 8 + 4 + 4 + 4 + 4); }
+size_t ctrl_bytes(size_t n) { return kCtrlHeader + n * (8 + 8 + 4 + 4 + 4 + 4); }
 
 hbp::KParams base_params(hbp_graph *g) {
   hbp::KParams P{};
@@ -836,8 +879,16 @@ hbp::KParams base_params(hbp_graph *g) {
   P.vtof = g->d_vtof;
   P.ftov = g->d_ftov;
   P.marg = g->d_marg;
-  P.prev = g->d_prev;
+  P.p0 = g->d_prev;
   P.normalize = 1;
+  for (int k = 0; k <= hbp::kNodeMax + 1; ++k) {
+    P.vc_node[k] = g->L.vc_node[k];
+    P.vc_row[k] = g->L.vc_row[k];
+    P.fa_node[k] = g->L.fa_node[k];
+    P.fa_row[k] = g->L.fa_row[k];
+    P.fo_node[k] = g->L.fo_node[k];
+    P.fo_row[k] = g->L.fo_row[k];
+  }
   return P;
 }
 
@@ -854,7 +905,7 @@ hbp_status ensure_ctrl(hbp_graph *g, size_t n) {
 hbp_status reset_ctrl(hbp_graph *g, size_t n) {
   CtrlView c = ctrl_view(g->d_ctrl, g->ctrl_cap);
   cudaStream_t s = g->stream;
-  HBP_CUDA(cudaMemsetAsync(c.ctrl, 0, 256, s));
+  HBP_CUDA(cudaMemsetAsync(c.ctrl, 0, kCtrlHeader, s));
   HBP_CUDA(cudaMemsetAsync(c.delta_bits, 0, n * 8, s));
   HBP_CUDA(cudaMemsetAsync(c.uf_where, 0xFF, n * 8, s));
   HBP_CUDA(cudaMemsetAsync(c.uf_msg, 0, n * 4, s));

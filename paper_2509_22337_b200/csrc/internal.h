@@ -93,6 +93,11 @@ struct HostLayout {
     return (fi >= f_or_light && fi < f_heavy) || fi >= f_or_heavy;
   }
   int32_t max_fdeg = 0, max_vdeg = 0;
+  // degree classes of the light nodes: [x_node[d], x_node[d+1]) have degree d
+  // (d = 1..kNodeMax), first row x_row[d]; x_node[kNodeMax + 1] ends the light range
+  int32_t vc_node[kNodeMax + 2] = {}, vc_row[kNodeMax + 2] = {};
+  int32_t fa_node[kNodeMax + 2] = {}, fa_row[kNodeMax + 2] = {};  // light AND factors
+  int32_t fo_node[kNodeMax + 2] = {}, fo_row[kNodeMax + 2] = {};  // light OR factors
 };
 
 hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L);

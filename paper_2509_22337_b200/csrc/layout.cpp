@@ -112,7 +112,13 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     if (L.rowptr[f + 1] - L.rowptr[f] > 1) L.nonunary[L.edge_var[e]]++;
   }
   int32_t maxv = 0;
-  for (int32_t v = 0; v < V; ++v) maxv = std::max(maxv, vdeg[v]);
+  for (int32_t v = 0; v < V; ++v) {
+    if (vdeg[v] == 0) {  // graph.py:114 rejects it too
+      set_error("variable " + std::to_string(v) + " appears in no factor");
+      return HBP_EINVAL;
+    }
+    maxv = std::max(maxv, vdeg[v]);
+  }
   if (maxv > 65535) {
     set_error("variable degree above 65535");
     return HBP_EINVAL;
@@ -139,6 +145,23 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
       L.v_heavy = i;
       break;
     }
+
+  // degree classes of the light nodes (computed rows in the PARALL kernels)
+  auto classes = [](const std::vector<int32_t> &row, int32_t lo, int32_t hi, int32_t *node,
+                    int32_t *rowstart) {
+    // node[d] = first node in [lo, hi) of degree >= d (nodes sorted by degree)
+    int32_t n = lo;
+    for (int32_t d = 1; d <= kNodeMax + 1; ++d) {
+      while (n < hi && row[n + 1] - row[n] < d) ++n;
+      node[d] = d == kNodeMax + 1 ? hi : n;
+      rowstart[d] = row[node[d]];
+    }
+    node[0] = lo;
+    rowstart[0] = row[lo];
+  };
+  classes(L.vrow, 0, L.v_heavy, L.vc_node, L.vc_row);
+  classes(L.frow, 0, L.f_or_light, L.fa_node, L.fa_row);
+  classes(L.frow, L.f_or_light, L.f_heavy, L.fo_node, L.fo_row);
 
   // ftov rows: canonical order within each variable == (factor, slot) order,
   // which is the reference's product order (storage.py:59-61)
