@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhbp.so")
+LIB_PATH = os.environ.get("HBP_LIB_PATH") or os.path.join(_HERE, "_lib", "libhbp.so")
 
 HBP_OK = 0
 HBP_EINVAL = 1

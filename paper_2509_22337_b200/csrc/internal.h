@@ -46,7 +46,10 @@ struct Phase {
 
 // Nodes up to this degree are processed whole by one thread (row in
 // registers); the rows of larger nodes are processed one slot per thread.
-constexpr int32_t kNodeMax = 4;
+#ifndef HBP_NODE_MAX
+#define HBP_NODE_MAX 4
+#endif
+constexpr int32_t kNodeMax = HBP_NODE_MAX;
 
 // List items: slot id | kWriteBit (type 0 only: also write the vtof message;
 // items without it exist only to produce a marginal).
