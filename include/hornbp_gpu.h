@@ -157,6 +157,21 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t num_targets,
 hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
                          double *out, int64_t *underflow_var);
 
+/* Evidence for the following runs of this graph: variable var[i] observed
+ * value[i] (0/1). Equivalent to clamp_evidence(graph, var[i], value[i]) applied
+ * in order (graph.py:189-200) when the plan's schedule is the base graph's
+ * PARALL or canonical SEQFIX schedule -- the two whose batches do not change
+ * under clamping (the clamp edges only join s_0 / s_{k-1}). n = 0 clears it.
+ * Replaces the per-round graph rebuild + recompile of interaction_loop
+ * (ranking.py:122-127). */
+hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var, const int8_t *value);
+
+/* Rank a selection (ascending variable ids, e.g. the alarms) by the last run's
+ * P1, skipping variables with evidence: rank_alarms order (ranking.py:83-91),
+ * computed on the device. ranked [topk] (-1 padded), p1 [topk] or NULL. */
+hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *select, int32_t topk,
+                          int32_t *ranked, double *p1);
+
 /* Device introspection for the parity tests: copy the device layout back in
  * reference order (rowptr_ftov [V+1], ftov_to_vtof [E]). */
 hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to_vtof);

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -63,6 +64,11 @@ struct KParams {
   double2 *vtof, *ftov, *marg;
   double *p0;                 // [V] P(X=0) of the last marginal pass (prev P1 = 1 - p0)
   int marg_direct;            // 1: put_marginal also writes marg[orig] (single-pass API)
+  // evidence codes per internal variable (null: none): bit0 observed false,
+  // bit1 observed true -- the clamp factors of clamp_evidence, multiplied in
+  // after the row product (their slot is last in the row) for every marginal
+  // and, from iteration 2 on, for every variable-to-factor message
+  const unsigned char *ev;
   // degree classes of the light nodes (rows computed, not loaded):
   // [vc_node[d], vc_node[d+1]) are the light variables of degree d, first row vc_row[d]
   int vc_node[kNodeMax + 2], vc_row[kNodeMax + 2];
@@ -171,6 +177,18 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
   if (P.hist) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
 }
 
+// the clamp factors' messages (1,0) / (0,1), exact multiplications by 0 and 1
+__device__ __forceinline__ void apply_clamp(unsigned code, double &a0, double &a1) {
+  if (code & 1u) {
+    a0 = mul(a0, 1.0);
+    a1 = mul(a1, 0.0);
+  }
+  if (code & 2u) {
+    a0 = mul(a0, 0.0);
+    a1 = mul(a1, 1.0);
+  }
+}
+
 // --------------------------------------------------------------------------------------
 // variable side, one ftov slot q: the vtof message of the same edge (product of
 // the row without q, engine.py:186-195) and, at a row start, the marginal
@@ -242,11 +260,16 @@ __device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned
     case 8: v_row<8>(P, r, j, marg, a0, a1, q0, q1); break;
     default: v_row_long(P, r, d, j, marg, a0, a1, q0, q1); break;
   }
+  const unsigned code = P.ev ? P.ev[w.x] : 0u;
   if (wr) {
     const int out = (int)(tw & ~kUnaryBit);
+    if (code && it > 1) apply_clamp(code, a0, a1);
     put_message(P, P.vtof + out, a0, a1, phase, 0, out, ufkey);
   }
-  if (marg) put_marginal(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
+  if (marg) {
+    if (code) apply_clamp(code, q0, q1);
+    put_marginal(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
+  }
 }
 
 // --------------------------------------------------------------------------------------
@@ -360,6 +383,7 @@ __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool
     prev_p0 = P.p0[v];
     orig = __ldg(P.vorig + v);
   }
+  const unsigned code = P.ev ? P.ev[v] : 0u;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const double2 m = uniform ? make_double2(1.0, 1.0) : P.ftov[r + k];
@@ -380,12 +404,16 @@ __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool
         b0 = mul(b0, x0[k]);
         b1 = mul(b1, x1[k]);
       }
+      if (code && it > 1) apply_clamp(code, b0, b1);
       put_message(P, P.vtof + tw[j], b0, b1, phase, 0, (int)tw[j], ufkey);
     }
     a0 = mul(a0, x0[j]);
     a1 = mul(a1, x1[j]);
   }
-  if (marg) put_marginal(P, v, a0, a1, it, dmax, prev_p0, orig);
+  if (marg) {
+    if (code) apply_clamp(code, a0, a1);
+    put_marginal(P, v, a0, a1, it, dmax, prev_p0, orig);
+  }
 }
 
 // degree class of a light node: rows of class d are contiguous with stride d
@@ -813,6 +841,108 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   flush_underflow(P, 1, ufkey);
 }
 
+// Alarm ranking of the last run (ranking.py:83-91): the selection's unlabeled
+// variables (no evidence code) by descending P1, ties by ascending position
+// in the id-sorted selection. One CTA. topk == 1: an argmax reduction;
+// otherwise a bitonic sort of (~bits(P1), position) in shared memory.
+__global__ void __launch_bounds__(1024) rank_kernel(const double2 *marg, const unsigned char *ev,
+                                                    const int *vinv, const int *sel, int nsel,
+                                                    int npow2, int topk, int *ranked,
+                                                    double *p1_out) {
+  extern __shared__ unsigned char smem[];
+  unsigned long long *key = (unsigned long long *)smem;
+  int *pos = (int *)(key + npow2);
+  auto key_of = [&](int i) -> unsigned long long {
+    if (i >= nsel) return ~0ull;
+    const int v = sel[i];
+    if (ev && ev[vinv[v]]) return ~0ull;
+    return ~(unsigned long long)__double_as_longlong(marg[v].y);
+  };
+  if (topk == 1) {
+    unsigned long long best = ~0ull;
+    int bpos = 0x7fffffff;
+    for (int i = threadIdx.x; i < nsel; i += blockDim.x) {
+      const unsigned long long k = key_of(i);
+      if (k < best || (k == best && i < bpos)) {
+        best = k;
+        bpos = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int p2 = __shfl_xor_sync(0xffffffffu, bpos, o);
+      if (k2 < best || (k2 == best && p2 < bpos)) {
+        best = k2;
+        bpos = p2;
+      }
+    }
+    __shared__ unsigned long long wk[32];
+    __shared__ int wp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+      wk[warp] = best;
+      wp[warp] = bpos;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < (int)(blockDim.x >> 5) ? wk[lane] : ~0ull;
+      bpos = lane < (int)(blockDim.x >> 5) ? wp[lane] : 0x7fffffff;
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const int p2 = __shfl_xor_sync(0xffffffffu, bpos, o);
+        if (k2 < best || (k2 == best && p2 < bpos)) {
+          best = k2;
+          bpos = p2;
+        }
+      }
+      if (lane == 0) {
+        const bool any = best != ~0ull;
+        ranked[0] = any ? sel[bpos] : -1;
+        if (p1_out) p1_out[0] = any ? marg[sel[bpos]].y : 0.0;
+      }
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    key[i] = key_of(i);
+    pos[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < npow2 / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long ka = key[lo], kb = key[hi];
+        const int pa = pos[lo], pb = pos[hi];
+        const bool gt = ka > kb || (ka == kb && pa > pb);
+        if (gt == up) {
+          key[lo] = kb;
+          key[hi] = ka;
+          pos[lo] = pb;
+          pos[hi] = pa;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < topk; i += blockDim.x) {
+    const bool ok = i < nsel && key[i] != ~0ull;
+    ranked[i] = ok ? sel[pos[i]] : -1;
+    if (p1_out) p1_out[i] = ok ? marg[sel[pos[i]]].y : 0.0;
+  }
+}
+
+__global__ void evidence_kernel(unsigned char *ev, const int *vinv, const int *var,
+                                const signed char *val, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t pos = (size_t)vinv[var[i]];
+  unsigned *word = (unsigned *)(ev + (pos & ~(size_t)3));
+  atomicOr(word, (val[i] ? 2u : 1u) << (8 * (pos & 3)));
+}
+
 __global__ void division_selftest_kernel(const double *a, const double *b, double *qf, double *qr,
                                          long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1083,6 +1213,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.uf_where = c.uf_where;
   P.tflag = c.tflag;
   P.hist = hist;
+  P.ev = g->has_ev ? g->d_ev : nullptr;
   P.trace = nullptr;
   if (getenv("HBP_TRACE")) {
     const size_t n_tr = (size_t)hbp::kTraceIters * P.nphases * p->grid * 2;
@@ -1309,6 +1440,93 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
     hbp::set_error("underflow");
     return HBP_EUNDERFLOW;
   }
+  return HBP_OK;
+}
+
+hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var,
+                                  const int8_t *value) {
+  if (!g || n < 0 || (n > 0 && (!var || !value))) {
+    hbp::set_error("bad evidence arguments");
+    return HBP_EINVAL;
+  }
+  const hbp::HostLayout &L = g->L;
+  for (int32_t i = 0; i < n; ++i) {
+    if (var[i] < 0 || var[i] >= L.V) {
+      hbp::set_error("evidence variable out of range");
+      return HBP_EINVAL;
+    }
+    if (value[i] != 0 && value[i] != 1) {
+      hbp::set_error("evidence value must be 0 or 1");
+      return HBP_EINVAL;
+    }
+  }
+  HBP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = g->stream;
+  hbp_status st;
+  if (!g->d_vinv && (st = upload(&g->d_vinv, L.vinv, s))) return st;
+  if (!g->d_ev) HBP_CUDA(cudaMalloc(&g->d_ev, (size_t)L.V + 4));
+  HBP_CUDA(cudaMemsetAsync(g->d_ev, 0, (size_t)L.V + 4, s));
+  g->has_ev = n > 0;
+  if (n > 0) {
+    void *buf = nullptr;
+    HBP_CUDA(cudaMallocAsync(&buf, (size_t)n * 5 + 16, s));
+    int *d_var = (int *)buf;
+    signed char *d_val = (signed char *)(d_var + n);
+    HBP_CUDA(cudaMemcpyAsync(d_var, var, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    HBP_CUDA(cudaMemcpyAsync(d_val, value, (size_t)n, cudaMemcpyHostToDevice, s));
+    hbp::evidence_kernel<<<(n + 255) / 256, 256, 0, s>>>(g->d_ev, g->d_vinv, d_var, d_val, n);
+    HBP_CUDA(cudaGetLastError());
+    HBP_CUDA(cudaFreeAsync(buf, s));
+  }
+  HBP_CUDA(cudaStreamSynchronize(s));
+  return HBP_OK;
+}
+
+hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *select, int32_t topk,
+                          int32_t *ranked, double *p1) {
+  if (!g || num_select < 0 || topk < 1 || (num_select > 0 && !select) || !ranked) {
+    hbp::set_error("bad rank arguments");
+    return HBP_EINVAL;
+  }
+  const hbp::HostLayout &L = g->L;
+  for (int32_t k = 0; k < num_select; ++k)
+    if (select[k] < 0 || select[k] >= L.V || (k && select[k] <= select[k - 1])) {
+      hbp::set_error("selection must be ascending variable ids");
+      return HBP_EINVAL;
+    }
+  int npow2 = 2;
+  while (npow2 < num_select) npow2 <<= 1;
+  if (topk > 1 && (size_t)npow2 * 12 > 200 * 1024) {
+    hbp::set_error("device ranking supports at most 16384 selected variables");
+    return HBP_EINVAL;
+  }
+  HBP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = g->stream;
+  hbp_status st;
+  if (!g->d_vinv && (st = upload(&g->d_vinv, L.vinv, s))) return st;
+  const size_t need = (size_t)num_select * 4 + (size_t)topk * 12 + 64;
+  if (g->rank_cap < need) {
+    if (g->d_rank) cudaFree(g->d_rank);
+    g->d_rank = nullptr;
+    g->rank_cap = 0;
+    HBP_CUDA(cudaMalloc(&g->d_rank, need));
+    g->rank_cap = need;
+  }
+  int *d_sel = (int *)g->d_rank;
+  int *d_out = d_sel + num_select;
+  double *d_p1 = (double *)(((uintptr_t)(d_out + topk) + 15) & ~(uintptr_t)15);
+  if (num_select)
+    HBP_CUDA(cudaMemcpyAsync(d_sel, select, (size_t)num_select * 4, cudaMemcpyHostToDevice, s));
+  const size_t smem = topk == 1 ? 0 : (size_t)npow2 * 12;
+  if (smem > 48 * 1024)
+    HBP_CUDA(cudaFuncSetAttribute(hbp::rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  hbp::rank_kernel<<<1, 1024, smem, s>>>(g->d_marg, g->has_ev ? g->d_ev : nullptr, g->d_vinv,
+                                         d_sel, num_select, npow2, topk, d_out, d_p1);
+  HBP_CUDA(cudaGetLastError());
+  HBP_CUDA(cudaMemcpyAsync(ranked, d_out, (size_t)topk * 4, cudaMemcpyDeviceToHost, s));
+  if (p1) HBP_CUDA(cudaMemcpyAsync(p1, d_p1, (size_t)topk * 8, cudaMemcpyDeviceToHost, s));
+  HBP_CUDA(cudaStreamSynchronize(s));
   return HBP_OK;
 }
 

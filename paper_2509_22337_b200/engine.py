@@ -182,6 +182,16 @@ class _Plan:
             device_ms=float(res.device_ms), updates_per_iteration=self.updates)
 
 
+    def run_device(self, options: EngineOptions, graph: FactorGraph) -> _native.Result:
+        """Run with the marginals left on the device (hbp_run_device)."""
+        opt = self.options(options)
+        res = _native.Result()
+        st = _native.lib().hbp_run_device(self.handle, C.byref(opt), C.byref(res), None)
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_run_device", res, graph)
+        return res
+
+
 class _Sweep:
     def __init__(self, dg: "_DeviceGraph", capacity: int):
         self.dg = dg
@@ -235,6 +245,29 @@ class _DeviceGraph:
         st = _native.lib().hbp_graph_set_stream(self.handle, C.c_void_p(handle or None))
         if st != _native.HBP_OK:
             _raise_status(st, "hbp_graph_set_stream")
+
+    def set_evidence(self, variables, values) -> None:
+        """Clamp ``variables`` to ``values`` for the following runs
+        (hbp_graph_set_evidence); empty clears."""
+        var = np.ascontiguousarray(np.asarray(variables, dtype=np.int32))
+        val = np.ascontiguousarray(np.asarray(values, dtype=np.int8))
+        st = _native.lib().hbp_graph_set_evidence(self.handle, len(var), _native.ptr(var, C.c_int32),
+                                                   _native.ptr(val, C.c_int8))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_graph_set_evidence")
+
+    def rank(self, select: np.ndarray, topk: int) -> tuple[np.ndarray, np.ndarray]:
+        """Top-k of ``select`` (ascending ids) by the last run's P1, variables
+        with evidence excluded (hbp_graph_rank)."""
+        sel = np.ascontiguousarray(select, dtype=np.int32)
+        out = np.empty(topk, dtype=np.int32)
+        p1 = np.empty(topk, dtype=np.float64)
+        st = _native.lib().hbp_graph_rank(self.handle, len(sel), _native.ptr(sel, C.c_int32),
+                                          int(topk), _native.ptr(out, C.c_int32),
+                                          _native.ptr(p1, C.c_double))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_graph_rank")
+        return out, p1
 
     def sweep(self, capacity: int = 0) -> "_Sweep":
         """Multi-evidence sweep buffers for this graph (cached per capacity)."""
