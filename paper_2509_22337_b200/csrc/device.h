@@ -52,6 +52,8 @@ struct hbp_graph {
   int *d_vinv = nullptr;
   void *d_rank = nullptr;
   size_t rank_cap = 0;
+  void *d_ev_list = nullptr;
+  size_t ev_list_cap = 0;
   // control block sized for max_iterations
   void *d_ctrl = nullptr;
   size_t ctrl_cap = 0;  // entries per array
@@ -65,7 +67,7 @@ struct hbp_graph {
     cudaSetDevice(device);
     for (void *p : {(void *)d_vslot, (void *)d_vtof_twin, (void *)d_fslot, (void *)d_ftov_twin,
                     (void *)d_vorig, (void *)d_fpar, (void *)d_vtof, (void *)d_ftov,
-                    (void *)d_marg, (void *)d_prev, (void *)d_ev, (void *)d_vinv, d_rank, d_ctrl, (void *)d_hist, (void *)d_trace,
+                    (void *)d_marg, (void *)d_prev, (void *)d_ev, (void *)d_vinv, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace,
                     (void *)d_vrow, (void *)d_frow})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);

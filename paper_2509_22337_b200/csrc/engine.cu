@@ -1468,15 +1468,20 @@ hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var,
   HBP_CUDA(cudaMemsetAsync(g->d_ev, 0, (size_t)L.V + 4, s));
   g->has_ev = n > 0;
   if (n > 0) {
-    void *buf = nullptr;
-    HBP_CUDA(cudaMallocAsync(&buf, (size_t)n * 5 + 16, s));
-    int *d_var = (int *)buf;
+    const size_t need = (size_t)n * 5 + 16;
+    if (g->ev_list_cap < need) {
+      if (g->d_ev_list) cudaFree(g->d_ev_list);
+      g->d_ev_list = nullptr;
+      g->ev_list_cap = 0;
+      HBP_CUDA(cudaMalloc(&g->d_ev_list, std::max<size_t>(need, 1 << 16)));
+      g->ev_list_cap = std::max<size_t>(need, 1 << 16);
+    }
+    int *d_var = (int *)g->d_ev_list;
     signed char *d_val = (signed char *)(d_var + n);
     HBP_CUDA(cudaMemcpyAsync(d_var, var, (size_t)n * 4, cudaMemcpyHostToDevice, s));
     HBP_CUDA(cudaMemcpyAsync(d_val, value, (size_t)n, cudaMemcpyHostToDevice, s));
     hbp::evidence_kernel<<<(n + 255) / 256, 256, 0, s>>>(g->d_ev, g->d_vinv, d_var, d_val, n);
     HBP_CUDA(cudaGetLastError());
-    HBP_CUDA(cudaFreeAsync(buf, s));
   }
   HBP_CUDA(cudaStreamSynchronize(s));
   return HBP_OK;

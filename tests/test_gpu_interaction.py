@@ -48,12 +48,13 @@ def test_loop_prefix_matches_reference_semantics(name, strategy, rounds):
 
 
 def test_loop_matches_host_path():
-    """Device path == the generic host path (explicit-order strategies use it)."""
+    """Device path == the generic host path (clamp + compile + run per round),
+    which CUSTOM strategies take; an empty CUSTOM relation compiles to PARALL's
+    single batch."""
     g, alarms = W.graph("weblech")
-    order = g.edge_list()  # the canonical order, given explicitly -> host path
     opts = EngineOptions(1000, 1e-9)
-    a = P.interaction_loop(g, alarms, Strategy.seqfix(), opts)
-    b = P.interaction_loop(g, alarms, Strategy.seqfix(order), opts)
+    a = P.interaction_loop(g, alarms, Strategy.parall(), opts)
+    b = P.interaction_loop(g, alarms, Strategy.custom([]), opts)
     assert [(r.alarm, r.label, r.p_true) for r in a.rounds] == \
            [(r.alarm, r.label, r.p_true) for r in b.rounds]
 
@@ -75,3 +76,11 @@ def test_evidence_run_equals_clamped_graph_run():
         assert got.iterations == want.iterations
         assert got.marginals.tobytes() == want.marginals.tobytes()
         assert got.deltas == want.deltas
+
+
+def test_explicit_seqfix_order_fails_like_the_reference():
+    """An explicit SEQFIX order is no longer a permutation of the clamped
+    graph's edges, so the reference's second round raises (schedule.py:184-185)."""
+    g, alarms = W.graph("weblech")
+    with pytest.raises(P.ScheduleError):
+        P.interaction_loop(g, alarms, Strategy.seqfix(g.edge_list()), EngineOptions(1000, 1e-9))
