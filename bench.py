@@ -258,11 +258,19 @@ def run_ours_sweep(args) -> None:
     from paper_2509_22337_b200 import workloads as W
 
     world, rank, local = dist_env()
+    # HBP_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 with gloo --
+    # exercises the multi-rank path on a one-GPU box; NCCL refuses shared GPUs
+    shared = os.environ.get("HBP_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     P.engine.set_device(local)
     multi = world > 1
     if multi:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     g, alarms = W.graph("ftp")
     n = args.sets

@@ -489,11 +489,20 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
 // producer runs up to four chunks ahead, so every SM keeps ~60 KB of loads in
 // flight regardless of how long the fp64 chains take.
 
-constexpr int kWsConsumers = 8;
+#ifndef HBP_WS_CONSUMERS
+#define HBP_WS_CONSUMERS 8
+#endif
+constexpr int kWsConsumers = HBP_WS_CONSUMERS;
 constexpr int kWsThreads = 32 * (kWsConsumers + 1);
 constexpr int kChR = 32;   // message rows per chunk
 constexpr int kChN = 16;   // nodes per chunk
-constexpr int kRing = 4;   // chunks in flight per CTA
+#ifndef HBP_WS_RING
+#define HBP_WS_RING 4
+#endif
+#ifndef HBP_WS_MINB
+#define HBP_WS_MINB 2
+#endif
+constexpr int kRing = HBP_WS_RING;  // chunks in flight per CTA
 constexpr int kPad = 8;    // index arrays are padded so aligned windows stay in bounds
 
 struct __align__(16) WsChunk {
@@ -791,7 +800,7 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &s
     const WsChunk &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    const int start = (cw - base) & (kWsConsumers - 1);
+    const int start = (cw + kWsConsumers - base % kWsConsumers) % kWsConsumers;
     if (alive) {
       for (int f = n0 + start; f < n1; f += kWsConsumers) {
         const int r = ch.rp[f - rp_lo];
@@ -832,7 +841,7 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &s
     const WsChunk &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    const int start = (cw - base) & (kWsConsumers - 1);
+    const int start = (cw + kWsConsumers - base % kWsConsumers) % kWsConsumers;
     if (alive) {
       for (int v = n0 + start; v < n1; v += kWsConsumers) {
         const int r = ch.rp[v - rp_lo];
@@ -867,7 +876,7 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &s
 }
 
 template <bool NORM>
-__global__ void __launch_bounds__(kWsThreads, 2) sweep_ws(const __grid_constant__ SweepParams P) {
+__global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid_constant__ SweepParams P) {
   extern __shared__ __align__(128) unsigned char ws_smem[];
   WsShared &sh = *reinterpret_cast<WsShared *>(ws_smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
