@@ -556,7 +556,7 @@ template <int D, bool NORM>
 __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane &L, int v,
                                       const double2 *x, const int *tw, unsigned code,
                                       double prev_p0, int it, bool write_vtof,
-                                      unsigned long long &dmax, unsigned long long &uf) {
+                                      unsigned long long &dmax, unsigned &uf) {
   double x0[D], x1[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -578,7 +578,7 @@ __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane &L, in
       if (code) sw_clamp(code, b0, b1);
       if (NORM) {
         const double tt = add(b0, b1);
-        if (tt < kMinMessageSum) uf = min(uf, (unsigned long long)t);
+        uf = tt < kMinMessageSum ? t + 1 : uf;  // last underflowing slot + 1 (rare)
         div2_rn(b0, b1, tt, b0, b1);
       }
       L.vtof[t * 32] = make_double2(b0, b1);
@@ -595,7 +595,7 @@ template <bool NORM>
 __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, int v,
                                         const double2 *x, int d, const int *tw, unsigned code,
                                         double prev_p0, int it, bool write_vtof,
-                                        unsigned long long &dmax, unsigned long long &uf) {
+                                        unsigned long long &dmax, unsigned &uf) {
   if (write_vtof) {
     for (int j = 0; j < d; ++j) {
       const unsigned t = (unsigned)tw[j];
@@ -610,7 +610,7 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, i
       if (code) sw_clamp(code, b0, b1);
       if (NORM) {
         const double tt = add(b0, b1);
-        if (tt < kMinMessageSum) uf = min(uf, (unsigned long long)t);
+        uf = tt < kMinMessageSum ? t + 1 : uf;  // last underflowing slot + 1 (rare)
         div2_rn(b0, b1, tt, b0, b1);
       }
       L.vtof[t * 32] = make_double2(b0, b1);
@@ -628,10 +628,10 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, i
 
 template <bool NORM>
 __device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double o1,
-                                      unsigned long long &uf) {
+                                      unsigned &uf) {
   if (NORM) {
     const double tt = add(o0, o1);
-    if (tt < kMinMessageSum) uf = min(uf, (1ull << 32) | (unsigned)t);
+    uf = tt < kMinMessageSum ? (unsigned)t + 1 : uf;
     div2_rn(o0, o1, tt, o0, o1);
   }
   L.ftov[t * 32] = make_double2(o0, o1);
@@ -640,7 +640,7 @@ __device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double
 // factor node of degree D; FIRST: iteration 1 (every vtof message is uniform)
 template <int D, int KIND, bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_fac(const SwLane &L, const double2 *x, const int *tw,
-                                      double2 pp, unsigned long long &uf) {
+                                      double2 pp, unsigned &uf) {
   double m0[D], m1[D];
   const double c = NORM ? 0.5 : 1.0;
 #pragma unroll
@@ -690,7 +690,7 @@ __device__ __forceinline__ void ws_fac(const SwLane &L, const double2 *x, const 
 
 template <int KIND, bool NORM, bool FIRST>
 __device__ __noinline__ void ws_fac_any(const SwLane &L, const double2 *x, int d, const int *tw,
-                                        double2 pp, unsigned long long &uf) {
+                                        double2 pp, unsigned &uf) {
   const double c = NORM ? 0.5 : 1.0;
   for (int j = 0; j < d; ++j) {
     double b1 = 1.0, b2 = 1.0;
@@ -718,7 +718,7 @@ __device__ __noinline__ void ws_fac_any(const SwLane &L, const double2 *x, int d
 
 template <int KIND, bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int d, const int *tw,
-                                        double2 pp, unsigned long long &uf) {
+                                        double2 pp, unsigned &uf) {
   switch (d) {
     case 1: ws_fac<1, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
     case 2: ws_fac<2, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
@@ -791,7 +791,7 @@ template <bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &sh, const SwLane &L,
                                                int cw, int first, int count, int stride,
                                                bool alive, unsigned &seq,
-                                               unsigned long long &uf) {
+                                               unsigned &uf) {
   const int lane = threadIdx.x & 31;
   int base = 0;
   for (int c = first; c < count; c += stride) {
@@ -832,7 +832,7 @@ template <bool NORM>
 __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &sh, const SwLane &L,
                                                int cw, int first, int count, int stride, int it,
                                                bool write_vtof, bool alive, unsigned &seq,
-                                               unsigned long long &dmax, unsigned long long &uf) {
+                                               unsigned long long &dmax, unsigned &uf) {
   const int lane = threadIdx.x & 31;
   int base = 0;
   for (int c = first; c < count; c += stride) {
@@ -901,7 +901,8 @@ __global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid
   for (int it = 1;; ++it) {
     if (it >= 2) {
       const bool final_pass = it == P.max_it + 1;
-      unsigned long long dmax = 0, uf = ~0ull;
+      unsigned long long dmax = 0;
+      unsigned uf = 0;  // last underflowing vtof slot + 1 of this thread's set
       if (__syncthreads_or(alive)) {
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -919,7 +920,7 @@ __global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid
         for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][lane] > m ? sh.red[w][lane] : m;
         if (alive) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + s], m);
       }
-      if (alive && !producer && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+      if (alive && !producer && uf) atomicMin(&P.ufkey[(size_t)it * P.S + s], (unsigned long long)(uf - 1));
       if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
         P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
       sw_grid_sync(P.bar, expected, nblocks);
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid
       }
     }
     {
-      unsigned long long uf = ~0ull;
+      unsigned uf = 0;  // last underflowing ftov slot + 1
       if (__syncthreads_or(alive)) {
         const bool first = it == 1;
         // after iteration 1 the unary factors' chunks are skipped (constant messages)
@@ -960,7 +961,8 @@ __global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid
           ws_consume_fac<NORM, false>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
         }
       }
-      if (alive && !producer && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
+      if (alive && !producer && uf)
+        atomicMin(&P.ufkey[(size_t)it * P.S + s], (1ull << 32) | (unsigned long long)(uf - 1));
     }
     sw_grid_sync(P.bar, expected, nblocks);
     if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
