@@ -489,6 +489,9 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
 // producer runs up to four chunks ahead, so every SM keeps ~60 KB of loads in
 // flight regardless of how long the fp64 chains take.
 
+#ifndef HBP_WS_DMAX
+#define HBP_WS_DMAX 6  // largest node degree computed from registers (larger: loop path)
+#endif
 #ifndef HBP_WS_CONSUMERS
 #define HBP_WS_CONSUMERS 8
 #endif
@@ -724,7 +727,9 @@ __device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int 
     case 2: ws_fac<2, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
     case 3: ws_fac<3, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
     case 4: ws_fac<4, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+#if HBP_WS_DMAX > 4
     case 5: ws_fac<5, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+#endif
     default: ws_fac_any<KIND, NORM, FIRST>(L, x, d, tw, pp, uf); break;
   }
 }
@@ -860,8 +865,10 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &s
           case 2: ws_var<2, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
           case 3: ws_var<3, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
           case 4: ws_var<4, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+#if HBP_WS_DMAX > 4
           case 5: ws_var<5, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
           case 6: ws_var<6, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
+#endif
           default:
             ws_var_any<NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, dmax, uf);
             break;
