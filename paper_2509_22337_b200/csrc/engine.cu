@@ -39,7 +39,6 @@ namespace hbp {
 using namespace dev;
 
 constexpr int kThreads = 1024;  // default block size (HBP_THREADS=512 selects the alternative)
-constexpr int kChunk = 8;       // row elements loaded per round trip
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 
 struct Ctrl {
@@ -195,7 +194,7 @@ __device__ __forceinline__ void apply_clamp(unsigned code, double &a0, double &a
 // (full row product). write: 1 = yes, 0 = no, -1 = unless the edge's factor
 // is unary (PARALL range mode).
 
-// rows longer than kChunk (rare): same left-to-right products, chunked loads
+// rows longer than 8 (rare): same left-to-right products, loads in groups of 4
 __device__ __noinline__ void v_row_long(const KParams &P, int r, int d, int j, bool marg,
                                         double &a0, double &a1, double &q0, double &q1) {
   for (int base = 0; base < d; base += 4) {
