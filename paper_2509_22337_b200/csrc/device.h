@@ -40,6 +40,9 @@ struct hbp_graph {
   cudaStream_t stream = nullptr;      // stream all work of this graph runs on
   cudaStream_t own_stream = nullptr;  // created with the graph
   int num_sms = 0, coop_blocks = 0, threads = 1024;
+  // cluster 0 runs the small levels: csize CTAs (1 = CTA 0 alone), and a
+  // cooperative cluster launch fits cluster_grid CTAs
+  int csize = 1, cluster_grid = 0;
   const void *kernel = nullptr;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
@@ -82,6 +85,7 @@ struct hbp_plan {
   hbp::Phase *d_phases = nullptr;
   int *d_items = nullptr;
   int grid = 1;
+  int csize = 1;  // CTAs of cluster 0 (small levels); 1 = no cluster launch
   ~hbp_plan() {
     cudaSetDevice(g->device);
     for (void *p : {(void *)d_phases, (void *)d_items})

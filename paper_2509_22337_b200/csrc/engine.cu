@@ -87,6 +87,7 @@ struct KParams {
   int *tflag;                      // [max_it + 2]
   double2 *hist;                   // [max_it][V] or null
   unsigned long long *trace;       // debug: [kTraceIters][nphases][grid][2] or null
+  int csize;                       // CTAs of cluster 0, which runs the small levels
   int max_it;
   int normalize;
   double tol;
@@ -540,9 +541,9 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     start = blockIdx.x * blockDim.x + threadIdx.x;
     stride = gridDim.x * blockDim.x;
   } else {
-    if (blockIdx.x != 0) return;
-    start = threadIdx.x;
-    stride = blockDim.x;
+    if ((int)blockIdx.x >= P.csize) return;
+    start = blockIdx.x * blockDim.x + threadIdx.x;
+    stride = P.csize * blockDim.x;
   }
   const int n = ph.end - ph.begin;
   unsigned long long ufkey = ~0ull;
@@ -561,8 +562,8 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
       c0 = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
       cstride = gridDim.x * (blockDim.x >> 5);
     } else {
-      c0 = threadIdx.x >> 5;
-      cstride = blockDim.x >> 5;
+      c0 = (threadIdx.x >> 5) * P.csize + blockIdx.x;
+      cstride = P.csize * (blockDim.x >> 5);
     }
     if (ph.type == 0) {
       const bool marg = do_marg && ph.marg;
@@ -682,6 +683,16 @@ __device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int 
     P.trace[(((size_t)(it - 2) * P.nphases + p) * gridDim.x + blockIdx.x) * 2 + which] = globaltimer();
 }
 
+// barrier of cluster 0 between two small levels (release/acquire at cluster
+// scope orders the global-memory messages too); csize 1: CTA 0 alone
+__device__ __forceinline__ void cluster0_sync(int csize) {
+  if (csize > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
 // marginals of the stopping iteration in the reference's variable order
 __device__ __forceinline__ void write_marginals(const KParams &P) {
   const int gs = gridDim.x * blockDim.x;
@@ -771,16 +782,17 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
       const Phase ph = P.phases[p];
       if (p > 1) {  // transition p-1 -> p (phase 0 -> 1 was the full barrier above)
         const int prev_grid = P.phases[p - 1].grid;
+        const bool in0 = (int)blockIdx.x < P.csize;
         if (!multi) {
           __syncthreads();
         } else if (prev_grid && ph.grid) {
           sync_point(C, sy, G, true, true);
         } else if (prev_grid && !ph.grid) {
-          sync_point(C, sy, G, true, blockIdx.x == 0);
+          sync_point(C, sy, G, true, in0);
         } else if (!prev_grid && !ph.grid) {
-          if (blockIdx.x == 0) __syncthreads();
-        } else {  // CTA 0 -> grid
-          sync_point(C, sy, 1, blockIdx.x == 0, true);
+          if (in0) cluster0_sync(P.csize);
+        } else {  // cluster 0 -> grid
+          sync_point(C, sy, P.csize, in0, true);
         }
       }
       unsigned long long unused = 0;
@@ -796,7 +808,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
       } else if (last_grid) {
         sync_point(C, sy, G, true, true);
       } else {
-        sync_point(C, sy, 1, blockIdx.x == 0, true);
+        sync_point(C, sy, P.csize, (int)blockIdx.x < P.csize, true);
       }
     }
     if (it > 1 && defer) {
@@ -1021,6 +1033,7 @@ hbp::KParams base_params(hbp_graph *g) {
   P.marg = g->d_marg;
   P.p0 = g->d_prev;
   P.normalize = 1;
+  P.csize = 1;
   for (int k = 0; k <= hbp::kNodeMax + 1; ++k) {
     P.vc_node[k] = g->L.vc_node[k];
     P.vc_row[k] = g->L.vc_row[k];
@@ -1085,6 +1098,35 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   }
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
+  // Largest cluster size whose cooperative cluster launch still covers >= 90 %
+  // of the SMs: small levels then run on one cluster (cluster barriers,
+  // ~0.2 us) with C SMs of issue bandwidth instead of one.
+  g->csize = 1;
+  g->cluster_grid = g->coop_blocks;
+  if (!getenv("HBP_NO_CLUSTER")) {
+    for (int c : {8, 4, 2}) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(g->coop_blocks / c * c);
+      cfg.blockDim = dim3(g->threads);
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, g->kernel, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (nclusters * c * 10 >= g->coop_blocks * 9) {
+        g->csize = c;
+        g->cluster_grid = nclusters * c;
+        break;
+      }
+    }
+  }
   const hbp::HostLayout &L = g->L;
   cudaStream_t s = g->stream;
   std::vector<double2> fpar((size_t)L.F);
@@ -1143,7 +1185,9 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   std::unique_ptr<hbp_plan> p(new (std::nothrow) hbp_plan());
   if (!p) return HBP_ENOMEM;
   p->g = g;
-  hbp_status st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host);
+  // levels smaller than two items per thread of cluster 0 run on cluster 0 only
+  const int32_t small = g->csize > 1 ? 2 * g->csize * g->threads : 3072;
+  hbp_status st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small);
   if (st != HBP_OK) return st;
   HBP_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
@@ -1156,7 +1200,16 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
       big = std::max<int64_t>(big, (ph.end - ph.begin) + (ph.list == 2 ? ph.send - ph.sbegin : 0));
   int64_t want = (big + g->threads - 1) / g->threads;
   if (big < 2 * g->threads) want = 1;
-  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
+  bool has_small = false;
+  for (const auto &ph : p->host.phases) has_small |= !ph.grid;
+  p->csize = (has_small && want > 1) ? g->csize : 1;
+  if (p->csize > 1) {
+    want = std::max<int64_t>(want, p->csize);
+    want = (want + p->csize - 1) / p->csize * p->csize;
+    p->grid = (int)std::min<int64_t>(want, g->cluster_grid);
+  } else {
+    p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
+  }
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();
   return HBP_OK;
@@ -1229,10 +1282,28 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.tol = opt->tolerance;
   P.time_limit_ns = opt->time_limit > 0 ? (long long)(opt->time_limit * 1e9) : 0;
   if (opt->time_limit > 0 && P.time_limit_ns == 0) P.time_limit_ns = 1;
+  P.csize = p->csize;
   void *args[] = {&P};
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
-  HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
-                                       g->stream));
+  if (p->csize > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = p->csize;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p->grid);
+    cfg.blockDim = dim3(g->threads);
+    cfg.stream = g->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    HBP_CUDA(cudaLaunchKernelExC(&cfg, g->kernel, args));
+  } else {
+    HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
+                                         g->stream));
+  }
   HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
   g_last_launches = 1;
   hbp::Ctrl hc;

@@ -35,7 +35,7 @@ hbp_status compile(const hbp_graph_desc &g, int64_t m, const int32_t *before,
 // item array (levelled schedules).
 struct Phase {
   int32_t type;   // 0 variable side, 1 factor side
-  int32_t grid;   // 1: whole grid; 0: CTA 0 only (small level)
+  int32_t grid;   // 1: whole grid; 0: cluster 0 only (small level)
   int32_t list;   // 0: slots [begin, end); 1: slot ids from the item list;
                   // 2: whole nodes [begin, end) (variables for type 0, factors for
                   //    type 1), every outgoing message of a node from one row read
@@ -114,6 +114,6 @@ struct PlanHost {
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P);
+                      PlanHost &P, int32_t small_threshold);
 
 }  // namespace hbp

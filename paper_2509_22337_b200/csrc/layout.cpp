@@ -10,7 +10,6 @@
 namespace hbp {
 
 namespace {
-constexpr int32_t kCta0Threshold = 3072;  // phases with fewer items run on CTA 0
 }
 
 hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
@@ -204,7 +203,7 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P) {
+                      PlanHost &P, int32_t small_threshold) {
   const int32_t V = L.V;
   const int64_t E = L.E;
   if (k < 0 || (k > 0 && (s_off[0] != 0 || t_off[0] != 0))) {
@@ -241,7 +240,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
   for (int32_t v = 0; v < V; ++v) nonunary_total += L.nonunary[v];
 
   auto push_phase = [&](Phase ph, int32_t n) {
-    ph.grid = n >= kCta0Threshold;
+    ph.grid = n >= small_threshold;  // smaller phases run on cluster 0 only
     P.max_items = std::max(P.max_items, n);
     P.phases.push_back(ph);
   };
