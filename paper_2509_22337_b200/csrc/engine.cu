@@ -1098,12 +1098,15 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   }
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
-  // Largest cluster size whose cooperative cluster launch still covers >= 90 %
-  // of the SMs: small levels then run on one cluster (cluster barriers,
-  // ~0.2 us) with C SMs of issue bandwidth instead of one.
+  // HBP_CLUSTER=1 (opt-in): small levels run on one thread-block cluster --
+  // the largest cluster size whose cooperative cluster launch still covers
+  // >= 90 % of the SMs -- with barrier.cluster between levels. Measured on
+  // B200 it is slower than CTA 0 alone (C4 SEQFIX 48.7 vs 41.5 ms): a small
+  // level is bound by its dependent-load chain, not by one SM's issue rate,
+  // and the cluster barrier costs more than __syncthreads.
   g->csize = 1;
   g->cluster_grid = g->coop_blocks;
-  if (!getenv("HBP_NO_CLUSTER")) {
+  if (getenv("HBP_CLUSTER")) {
     for (int c : {8, 4, 2}) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
