@@ -84,12 +84,11 @@ struct hbp_plan {
   hbp::PlanHost host;
   hbp::Phase *d_phases = nullptr;
   int *d_items = nullptr;
-  int4 *d_pitems = nullptr;
   int grid = 1;
   int csize = 1;  // CTAs of cluster 0 (small levels); 1 = no cluster launch
   ~hbp_plan() {
     cudaSetDevice(g->device);
-    for (void *p : {(void *)d_phases, (void *)d_items, (void *)d_pitems})
+    for (void *p : {(void *)d_phases, (void *)d_items})
       if (p) cudaFree(p);
   }
 };

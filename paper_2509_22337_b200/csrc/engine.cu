@@ -39,8 +39,7 @@ namespace hbp {
 using namespace dev;
 
 constexpr int kThreads = 1024;  // default block size (HBP_THREADS=512 selects the alternative)
-constexpr int kTraceIters = 4;
-constexpr int kSmemPhases = 1500;  // level programs up to 48 KB live in shared memory  // HBP_TRACE=1: timestamps for iterations 2..5
+constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 
 struct Ctrl {
   unsigned int bar;  // grid barrier arrivals (monotonic)
@@ -77,9 +76,7 @@ struct KParams {
   // plan
   const Phase *phases;
   int nphases;
-  int smem_phases;            // phase descriptors copied to shared memory (0: read from global)
   const int *items;
-  const int4 *pitems;         // list-mode items resolved: {item, slot word x, slot word y, twin}
   // control
   Ctrl *ctrl;
   unsigned long long *delta_bits;  // [max_it + 2]
@@ -538,8 +535,7 @@ __device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool f
 
 __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, int pidx, int it,
                                            bool do_marg, bool do_vtof,
-                                           unsigned long long &dmax,
-                                           const int4 *pre = nullptr) {
+                                           unsigned long long &dmax) {
   int start, stride;
   if (ph.grid) {
     start = blockIdx.x * blockDim.x + threadIdx.x;
@@ -606,26 +602,19 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     int q = 0, write = 0;
     int2 w = make_int2(0, 0);
     unsigned tw = 0;
-    auto unpack = [&](int4 r, int &q_, int &write_, int2 &w_, unsigned &tw_) {
-      q_ = r.x & (kWriteBit - 1);
-      write_ = (r.x & kWriteBit) ? 1 : 0;
-      w_ = make_int2(r.y, r.z);
-      tw_ = (unsigned)r.w;
-    };
     auto fetch = [&](int i, int &q_, int &write_, int2 &w_, unsigned &tw_) {
-      if (ph.list) {  // one 16-byte load: item, slot word and twin resolved at plan time
-        unpack(__ldg(P.pitems + ph.begin + i), q_, write_, w_, tw_);
+      if (ph.list) {
+        const int item = __ldg(P.items + ph.begin + i);
+        q_ = item & (kWriteBit - 1);
+        write_ = (item & kWriteBit) ? 1 : 0;
       } else {
         q_ = ph.begin + i;
         write_ = -1;
-        w_ = __ldg(P.vslot + q_);
-        tw_ = __ldg(P.ftov_twin + q_);
       }
+      w_ = __ldg(P.vslot + q_);
+      tw_ = __ldg(P.ftov_twin + q_);
     };
-    if (start < n) {
-      if (pre && ph.list) unpack(*pre, q, write, w, tw);
-      else fetch(start, q, write, w, tw);
-    }
+    if (start < n) fetch(start, q, write, w, tw);
     for (int i = start; i < n; i += stride) {
       int qn = 0, writen = 0;
       int2 wn = make_int2(0, 0);
@@ -640,24 +629,12 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
   } else {
     int p = 0, tw = 0;
     int2 w = make_int2(0, 0);
-    auto unpack = [&](int4 r, int &p_, int2 &w_, int &tw_) {
-      p_ = r.x;
-      w_ = make_int2(r.y, r.z);
-      tw_ = r.w;
-    };
     auto fetch = [&](int i, int &p_, int2 &w_, int &tw_) {
-      if (ph.list) {
-        unpack(__ldg(P.pitems + ph.begin + i), p_, w_, tw_);
-      } else {
-        p_ = ph.begin + i;
-        w_ = __ldg(P.fslot + p_);
-        tw_ = __ldg(P.vtof_twin + p_);
-      }
+      p_ = ph.list ? __ldg(P.items + ph.begin + i) : ph.begin + i;
+      w_ = __ldg(P.fslot + p_);
+      tw_ = __ldg(P.vtof_twin + p_);
     };
-    if (start < n) {
-      if (pre && ph.list) unpack(*pre, p, w, tw);
-      else fetch(start, p, w, tw);
-    }
+    if (start < n) fetch(start, p, w, tw);
     for (int i = start; i < n; i += stride) {
       int pn = 0, twn = 0;
       int2 wn = make_int2(0, 0);
@@ -725,32 +702,9 @@ __device__ __forceinline__ void write_marginals(const KParams &P) {
   }
 }
 
-// first list-mode item of phase ph for this thread (levelled schedules): the
-// record is static, so it is loaded one phase ahead and the phase itself only
-// waits on its message rows
-__device__ __forceinline__ bool prefetch_item(const KParams &P, const Phase &ph, int4 &out) {
-  if (ph.list != 1) return false;
-  int start;
-  if (ph.grid) {
-    start = blockIdx.x * blockDim.x + threadIdx.x;
-  } else {
-    if ((int)blockIdx.x >= P.csize) return false;
-    start = blockIdx.x * blockDim.x + threadIdx.x;
-  }
-  if (start >= ph.end - ph.begin) return false;
-  out = __ldg(P.pitems + ph.begin + start);
-  return true;
-}
-
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
-  extern __shared__ Phase s_phases[];  // the level program, when it fits
   Ctrl *C = P.ctrl;
-  const bool ph_smem = P.smem_phases >= P.nphases;
-  if (ph_smem)
-    for (int i = threadIdx.x; i < P.nphases; i += blockDim.x) s_phases[i] = P.phases[i];
-  __syncthreads();
-  auto phase_at = [&](int i) -> Phase { return ph_smem ? s_phases[i] : P.phases[i]; };
   const bool multi = gridDim.x > 1;
   const unsigned G = gridDim.x;
   Sync sy;  // sync points passed so far (identical on every CTA)
@@ -780,7 +734,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
     trace_mark(P, it, 0, 0);
-    exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
+    exec_phase(P, P.phases[0], 0, it, it > 1, !final_pass, dmax);
     trace_mark(P, it, 0, 1);
     if (it > 1) {
       unsigned long long m = block_max(dmax);
@@ -823,15 +777,11 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         return;
       }
     }
-    // remaining phases of this iteration; each prefetches its successor's first item
-    int4 cur_item = make_int4(0, 0, 0, 0);
-    bool have_cur = P.nphases > 1 && prefetch_item(P, phase_at(1), cur_item);
+    // remaining phases of this iteration
     for (int p = 1; p < P.nphases; ++p) {
-      const Phase ph = phase_at(p);
-      int4 next_item = make_int4(0, 0, 0, 0);
-      const bool have_next = p + 1 < P.nphases && prefetch_item(P, phase_at(p + 1), next_item);
+      const Phase ph = P.phases[p];
       if (p > 1) {  // transition p-1 -> p (phase 0 -> 1 was the full barrier above)
-        const int prev_grid = phase_at(p - 1).grid;
+        const int prev_grid = P.phases[p - 1].grid;
         const bool in0 = (int)blockIdx.x < P.csize;
         if (!multi) {
           __syncthreads();
@@ -847,14 +797,12 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
       }
       unsigned long long unused = 0;
       trace_mark(P, it, p, 0);
-      exec_phase(P, ph, p, it, false, true, unused, have_cur ? &cur_item : nullptr);
+      exec_phase(P, ph, p, it, false, true, unused);
       trace_mark(P, it, p, 1);
-      cur_item = next_item;
-      have_cur = have_next;
     }
     // transition last phase -> phase 0 of the next iteration (a grid phase)
     if (P.nphases > 1) {
-      const int last_grid = phase_at(P.nphases - 1).grid;
+      const int last_grid = P.phases[P.nphases - 1].grid;
       if (!multi) {
         __syncthreads();
       } else if (last_grid) {
@@ -1246,20 +1194,7 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   if (st != HBP_OK) return st;
   HBP_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
-  // list-mode items resolved to {item, slot word, twin}: one load per item on the device
-  std::vector<int4> pitems(p->host.items.size());
-  for (const auto &ph : p->host.phases) {
-    if (ph.list != 1) continue;
-    for (int32_t i = ph.begin; i < ph.end; ++i) {
-      const int32_t item = p->host.items[i];
-      const int32_t q = ph.type == 0 ? (item & (hbp::kWriteBit - 1)) : item;
-      const std::vector<int32_t> &slot = ph.type == 0 ? g->L.vslot : g->L.fslot;
-      const int32_t tw = ph.type == 0 ? (int32_t)g->L.ftov_twin[q] : g->L.vtof_twin[q];
-      pitems[i] = make_int4(item, slot[2 * (size_t)q], slot[2 * (size_t)q + 1], tw);
-    }
-  }
-  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)) ||
-      (st = upload(&p->d_pitems, pitems, s)))
+  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)))
     return st;
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
@@ -1325,9 +1260,6 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.phases = p->d_phases;
   P.nphases = (int)p->host.phases.size();
   P.items = p->d_items;
-  P.pitems = p->d_pitems;
-  P.smem_phases = (int)p->host.phases.size() <= hbp::kSmemPhases ? (int)p->host.phases.size() : 0;
-  const size_t phase_smem = (size_t)P.smem_phases * sizeof(hbp::Phase);
   P.ctrl = c.ctrl;
   P.delta_bits = c.delta_bits;
   P.uf_msg = c.uf_msg;
@@ -1367,14 +1299,13 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
     at[1].val.clusterDim.z = 1;
     cfg.gridDim = dim3(p->grid);
     cfg.blockDim = dim3(g->threads);
-    cfg.dynamicSmemBytes = phase_smem;
     cfg.stream = g->stream;
     cfg.attrs = at;
     cfg.numAttrs = 2;
     HBP_CUDA(cudaLaunchKernelExC(&cfg, g->kernel, args));
   } else {
-    HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args,
-                                         phase_smem, g->stream));
+    HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
+                                         g->stream));
   }
   HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
   g_last_launches = 1;
