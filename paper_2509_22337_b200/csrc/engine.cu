@@ -38,7 +38,7 @@ namespace hbp {
 
 using namespace dev;
 
-constexpr int kThreads = 1024;  // default block size (HBP_THREADS=512 selects the alternative)
+constexpr int kThreads = 768;  // default block size: 80 registers, fewest spills (measured best)
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 
 struct Ctrl {
@@ -702,8 +702,8 @@ __device__ __forceinline__ void write_marginals(const KParams &P) {
   }
 }
 
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
+template <int THREADS, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
   const bool multi = gridDim.x > 1;
   const unsigned G = gridDim.x;
@@ -1091,10 +1091,16 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   HBP_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
   int per_sm = 0;
   {
+    // HBP_THREADS (A/B): 768 (default: one CTA/SM, 80 registers), 1024 (64
+    // registers, spills), 512 (108 registers), 5122 (512 threads, two CTAs/SM).
+    // Measured on B200: 768 is best for PARALL and levelled schedules alike.
     const char *env = getenv("HBP_THREADS");
-    g->threads = (env && atoi(env) == 512) ? 512 : hbp::kThreads;
-    g->kernel = g->threads == 512 ? (const void *)hbp::lbp_persistent<512>
-                                  : (const void *)hbp::lbp_persistent<hbp::kThreads>;
+    const int sel = env ? atoi(env) : hbp::kThreads;
+    g->threads = sel == 1024 ? 1024 : (sel == 512 || sel == 5122 ? 512 : hbp::kThreads);
+    g->kernel = sel == 512    ? (const void *)hbp::lbp_persistent<512>
+                : sel == 1024 ? (const void *)hbp::lbp_persistent<1024>
+                : sel == 5122 ? (const void *)hbp::lbp_persistent<512, 2>
+                              : (const void *)hbp::lbp_persistent<hbp::kThreads>;
   }
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
