@@ -50,6 +50,10 @@ using namespace dev;
 constexpr int kSwWarps = 8;  // warps per CTA (blockDim = 256); lanes = 32 sets
 constexpr int kSwThreads = 32 * kSwWarps;
 constexpr int kSwMinBlocks = 4;  // default register budget: 4 CTAs (32 warps) per SM
+#ifndef HBP_SWEEP_NS
+#define HBP_SWEEP_NS 2
+#endif
+constexpr int kSweepNS = HBP_SWEEP_NS;  // default sets per lane of the staged kernel
 constexpr int kNoVar = 0x7f7f7f7f;  // ufmarg reset value (memset 0x7F)
 
 struct SweepParams {
@@ -476,18 +480,22 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
 // ---- TMA-staged, warp-specialised sweep kernel (default) ------------------------------------
 // The persistent kernel above issues a node's loads and then computes, so a
 // warp has no memory in flight while it multiplies: HBM-latency bound at
-// ~54 % of peak (profiles/r1_sweep_ncu.md). Here each CTA streams its
-// contiguous, row-balanced node range through a 4-chunk shared-memory ring:
-// one producer warp cuts the range into chunks of <= 32 message rows / 16
-// nodes and fetches each chunk with 1-D bulk copies (cp.async.bulk -> UBLKCP,
-// completion counted on an mbarrier): the chunk's message rows (contiguous in
-// the [S/32][E][32] tiles), its row pointers and twins (16-byte aligned
-// windows), and per node the P0 / evidence rows (variable side) or the factor
-// parameters (factor side). Eight consumer warps take the chunk's nodes
-// round-robin, compute from shared memory exactly as before (same operation
-// order -> same bits) and release the slot through an "empty" mbarrier. The
-// producer runs up to four chunks ahead, so every SM keeps ~60 KB of loads in
-// flight regardless of how long the fp64 chains take.
+// ~54 % of peak (profiles/r1_sweep_ncu.md). Here each CTA streams host-built
+// node chunks (<= 32 message rows / 16 nodes, interleaved over the CTAs)
+// through a shared-memory ring: one producer warp fetches each chunk with 1-D
+// bulk copies (cp.async.bulk -> UBLKCP, completion counted on an mbarrier):
+// the chunk's message rows (contiguous in the [S/32][E][32] tiles), its row
+// pointers and twins (16-byte aligned windows), and per node the P0 /
+// evidence rows (variable side) or the factor parameters (factor side).
+// Consumer warps take the chunk's nodes round-robin, compute from shared
+// memory in the reference's operation order (same bits) and release the
+// slot through an "empty" mbarrier.
+//
+// NS = sets per lane (1 or 2): with NS = 2 a CTA serves two 32-set groups and
+// every lane computes the same node for two sets -- two independent fp64
+// chains per lane (the kernel is bound by dependency latency, not issue) and
+// the node's index work (row pointers, twins, degree dispatch, loop) paid
+// once for both.
 
 #ifndef HBP_WS_DMAX
 #define HBP_WS_DMAX 6  // largest node degree computed from registers (larger: loop path)
@@ -495,33 +503,41 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
 #ifndef HBP_WS_CONSUMERS
 #define HBP_WS_CONSUMERS 8
 #endif
-constexpr int kWsConsumers = HBP_WS_CONSUMERS;
-constexpr int kWsThreads = 32 * (kWsConsumers + 1);
-constexpr int kChR = 32;   // message rows per chunk
-constexpr int kChN = 16;   // nodes per chunk
 #ifndef HBP_WS_RING
 #define HBP_WS_RING 4
 #endif
 #ifndef HBP_WS_MINB
 #define HBP_WS_MINB 2
 #endif
+// consumer warps per CTA: NS = 2 CTAs hold twice the staging, so one CTA per
+// SM with twice the consumers keeps the same number of warps per SM
+template <int NS>
+struct WsCfg {
+  static constexpr int consumers = NS == 1 ? HBP_WS_CONSUMERS : 2 * HBP_WS_CONSUMERS;
+  static constexpr int threads = 32 * (consumers + 1);
+  static constexpr int min_blocks = NS == 1 ? HBP_WS_MINB : 1;
+};
+constexpr int kChR = 32;   // message rows per chunk
+constexpr int kChN = 16;   // nodes per chunk
 constexpr int kRing = HBP_WS_RING;  // chunks in flight per CTA
 constexpr int kPad = 8;    // index arrays are padded so aligned windows stay in bounds
 
+template <int NS>
 struct __align__(16) WsChunk {
-  double2 msg[kChR][32];        // message rows of the chunk, one 512-byte row per slot
-  double p0[kChN][32];          // variable side: P0 of the previous iteration per node
-  unsigned char ev[kChN][32];   // variable side: evidence codes per node
-  double2 fpar[kChN];           // factor side: (p1, p2) per node
-  int rp[kChN + 8];             // row pointers, aligned window from (n0 & ~3)
-  int tw[kChR + 8];             // twins, aligned window from (r0 & ~3)
-  int n0, n1, r0, heavy;        // header written by the producer before arming
+  double2 msg[NS][kChR][32];      // message rows of the chunk, one 512-byte row per slot and group
+  double p0[NS][kChN][32];        // variable side: P0 of the previous iteration per node
+  unsigned char ev[NS][kChN][32]; // variable side: evidence codes per node
+  double2 fpar[kChN];             // factor side: (p1, p2) per node
+  int rp[kChN + 8];               // row pointers, aligned window from (n0 & ~3)
+  int tw[kChR + 8];               // twins, aligned window from (r0 & ~3)
+  int n0, n1, r0, heavy;          // header written by the producer before arming
 };
 
+template <int NS>
 struct WsShared {
-  WsChunk ring[kRing];
+  WsChunk<NS> ring[kRing];
   unsigned long long full[kRing], empty[kRing];
-  unsigned long long red[kWsConsumers][32];
+  unsigned long long red[WsCfg<NS>::consumers][NS][32];
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -554,46 +570,63 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       : "memory");
 }
 
-// variable node of degree D from shared memory (rows x[k*32], twins tw[k])
-template <int D, bool NORM>
-__device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane &L, int v,
-                                      const double2 *x, const int *tw, unsigned code,
-                                      double prev_p0, int it, bool write_vtof,
-                                      unsigned long long &dmax, unsigned &uf) {
-  double x0[D], x1[D];
+// Variable node of degree D for NS sets (set u: rows x[u][k*32], lane view
+// L[u]); twins tw[k] are shared. Per set exactly the single-set operation
+// order; the NS chains are independent and interleave.
+template <int D, int NS, bool NORM>
+__device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane *L, int v,
+                                      const double2 *const *x, const int *tw,
+                                      const unsigned *code, const double *prev_p0, int it,
+                                      bool write_vtof, const bool *alive,
+                                      unsigned long long *dmax, unsigned *uf) {
+  double x0[NS][D], x1[NS][D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double2 m = x[k * 32];
-    x0[k] = m.x;
-    x1[k] = m.y;
-  }
-  double a0 = 1.0, a1 = 1.0;
+  for (int u = 0; u < NS; ++u)
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double2 m = x[u][k * 32];
+      x0[u][k] = m.x;
+      x1[u][k] = m.y;
+    }
+  double a0[NS], a1[NS];
+#pragma unroll
+  for (int u = 0; u < NS; ++u) a0[u] = a1[u] = 1.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     const unsigned t = (unsigned)tw[j];
     if (write_vtof && !(t & kUnaryBit)) {
-      double b0 = a0, b1 = a1;
 #pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b0 = mul(b0, x0[k]);
-        b1 = mul(b1, x1[k]);
+      for (int u = 0; u < NS; ++u) {
+        double b0 = a0[u], b1 = a1[u];
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+          b0 = mul(b0, x0[u][k]);
+          b1 = mul(b1, x1[u][k]);
+        }
+        if (code[u]) sw_clamp(code[u], b0, b1);
+        if (NORM) {
+          const double tt = add(b0, b1);
+          uf[u] = tt < kMinMessageSum ? t + 1 : uf[u];  // last underflowing slot + 1 (rare)
+          div2_rn(b0, b1, tt, b0, b1);
+        }
+        if (NS == 1 || alive[u]) L[u].vtof[t * 32] = make_double2(b0, b1);
       }
-      if (code) sw_clamp(code, b0, b1);
-      if (NORM) {
-        const double tt = add(b0, b1);
-        uf = tt < kMinMessageSum ? t + 1 : uf;  // last underflowing slot + 1 (rare)
-        div2_rn(b0, b1, tt, b0, b1);
-      }
-      L.vtof[t * 32] = make_double2(b0, b1);
     }
-    a0 = mul(a0, x0[j]);
-    a1 = mul(a1, x1[j]);
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+      a0[u] = mul(a0[u], x0[u][j]);
+      a1[u] = mul(a1[u], x1[u][j]);
+    }
   }
-  if (code) sw_clamp(code, a0, a1);
-  sw_marginal(P, L, v, it, a0, a1, prev_p0, dmax);
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
+    if (NS > 1 && !alive[u]) continue;
+    if (code[u]) sw_clamp(code[u], a0[u], a1[u]);
+    sw_marginal(P, L[u], v, it, a0[u], a1[u], prev_p0[u], dmax[u]);
+  }
 }
 
-// any degree, rows re-read per target (heavy nodes: global memory)
+// any degree, one set, rows re-read per target (heavy nodes: global memory)
 template <bool NORM>
 __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, int v,
                                         const double2 *x, int d, const int *tw, unsigned code,
@@ -613,7 +646,7 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, i
       if (code) sw_clamp(code, b0, b1);
       if (NORM) {
         const double tt = add(b0, b1);
-        uf = tt < kMinMessageSum ? t + 1 : uf;  // last underflowing slot + 1 (rare)
+        uf = tt < kMinMessageSum ? t + 1 : uf;
         div2_rn(b0, b1, tt, b0, b1);
       }
       L.vtof[t * 32] = make_double2(b0, b1);
@@ -630,63 +663,73 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, i
 }
 
 template <bool NORM>
-__device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double o1,
-                                      unsigned &uf) {
+__device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double o1, unsigned &uf,
+                                      bool store) {
   if (NORM) {
     const double tt = add(o0, o1);
     uf = tt < kMinMessageSum ? (unsigned)t + 1 : uf;
     div2_rn(o0, o1, tt, o0, o1);
   }
-  L.ftov[t * 32] = make_double2(o0, o1);
+  if (store) L.ftov[t * 32] = make_double2(o0, o1);
 }
 
-// factor node of degree D; FIRST: iteration 1 (every vtof message is uniform)
-template <int D, int KIND, bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_fac(const SwLane &L, const double2 *x, const int *tw,
-                                      double2 pp, unsigned &uf) {
-  double m0[D], m1[D];
+// Factor node of degree D for NS sets; FIRST: iteration 1 (every vtof message
+// is the uniform one, so nothing is read).
+template <int D, int KIND, int NS, bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_fac(const SwLane *L, const double2 *const *x, const int *tw,
+                                      double2 pp, const bool *alive, unsigned *uf) {
+  double m0[NS][D], m1[NS][D];
   const double c = NORM ? 0.5 : 1.0;
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    if (FIRST) {
-      m0[k] = c;
-      m1[k] = c;
-    } else {
-      const double2 m = x[k * 32];
-      m0[k] = m.x;
-      m1[k] = m.y;
-    }
-  }
-  double sm[D];
+  for (int u = 0; u < NS; ++u)
 #pragma unroll
-  for (int k = 1; k < D; ++k) sm[k] = add(m0[k], m1[k]);
-  {
+    for (int k = 0; k < D; ++k) {
+      if (FIRST) {
+        m0[u][k] = c;
+        m1[u][k] = c;
+      } else {
+        const double2 m = x[u][k * 32];
+        m0[u][k] = m.x;
+        m1[u][k] = m.y;
+      }
+    }
+  double sm[NS][D];
+#pragma unroll
+  for (int u = 0; u < NS; ++u)
+#pragma unroll
+    for (int k = 1; k < D; ++k) sm[u][k] = add(m0[u][k], m1[u][k]);
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
     double h1 = 1.0, h2 = 1.0;
 #pragma unroll
     for (int k = 1; k < D; ++k) {
-      h1 = mul(h1, sm[k]);
-      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
+      h1 = mul(h1, sm[u][k]);
+      h2 = mul(h2, KIND == 0 ? m1[u][k] : m0[u][k]);
     }
     double o0, o1;
     head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    ws_put<NORM>(L, tw[0], o0, o1, uf);
+    ws_put<NORM>(L[u], tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
   }
   if (D > 1) {
-    double a1, a2;
-    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
+    double a1[NS], a2[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) head_slot_terms<KIND>(pp.x, pp.y, m0[u][0], m1[u][0], a1[u], a2[u]);
 #pragma unroll
     for (int j = 1; j < D; ++j) {
-      double b1 = a1, b2 = a2;
 #pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b1 = mul(b1, sm[k]);
-        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
+      for (int u = 0; u < NS; ++u) {
+        double b1 = a1[u], b2 = a2[u];
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+          b1 = mul(b1, sm[u][k]);
+          b2 = mul(b2, KIND == 0 ? m1[u][k] : m0[u][k]);
+        }
+        double o0, o1;
+        body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+        ws_put<NORM>(L[u], tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
+        a1[u] = mul(a1[u], sm[u][j]);
+        a2[u] = mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
       }
-      double o0, o1;
-      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-      ws_put<NORM>(L, tw[j], o0, o1, uf);
-      a1 = mul(a1, sm[j]);
-      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
     }
   }
 }
@@ -715,22 +758,65 @@ __device__ __noinline__ void ws_fac_any(const SwLane &L, const double2 *x, int d
       head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
     else
       body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-    ws_put<NORM>(L, tw[j], o0, o1, uf);
+    ws_put<NORM>(L, tw[j], o0, o1, uf, true);
   }
 }
 
-template <int KIND, bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int d, const int *tw,
-                                        double2 pp, unsigned &uf) {
+// degree dispatch; NS = 2 keeps the register path to degree 4 (two sets of rows)
+template <int KIND, int NS, bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_fac_k(const SwLane *L, const double2 *const *x, int d,
+                                        const int *tw, double2 pp, const bool *alive,
+                                        unsigned *uf) {
   switch (d) {
-    case 1: ws_fac<1, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
-    case 2: ws_fac<2, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
-    case 3: ws_fac<3, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
-    case 4: ws_fac<4, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 1: ws_fac<1, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
+    case 2: ws_fac<2, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
+    case 3: ws_fac<3, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
+    case 4: ws_fac<4, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
 #if HBP_WS_DMAX > 4
-    case 5: ws_fac<5, KIND, NORM, FIRST>(L, x, tw, pp, uf); break;
+    case 5:
+      if (NS == 1) {
+        ws_fac<5, KIND, 1, NORM, FIRST>(L, x, tw, pp, alive, uf);
+        break;
+      }
 #endif
-    default: ws_fac_any<KIND, NORM, FIRST>(L, x, d, tw, pp, uf); break;
+    default:
+#pragma unroll
+      for (int u = 0; u < NS; ++u)
+        if (NS == 1 || alive[u]) ws_fac_any<KIND, NORM, FIRST>(L[u], x[u], d, tw, pp, uf[u]);
+      break;
+  }
+}
+
+template <int NS, bool NORM>
+__device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, int v,
+                                        const double2 *const *x, int d, const int *tw,
+                                        const unsigned *code, const double *prev_p0, int it,
+                                        bool write_vtof, const bool *alive,
+                                        unsigned long long *dmax, unsigned *uf) {
+  switch (d) {
+    case 1: ws_var<1, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 2: ws_var<2, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 3: ws_var<3, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 4: ws_var<4, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+#if HBP_WS_DMAX > 4
+    case 5:
+      if (NS == 1) {
+        ws_var<5, 1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
+        break;
+      }
+    case 6:
+      if (NS == 1) {
+        ws_var<6, 1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
+        break;
+      }
+#endif
+    default:
+#pragma unroll
+      for (int u = 0; u < NS; ++u)
+        if (NS == 1 || alive[u])
+          ws_var_any<NORM>(P, L[u], v, x[u], d, tw, code[u], prev_p0[u], it, write_vtof, dmax[u],
+                           uf[u]);
+      break;
   }
 }
 
@@ -742,13 +828,14 @@ __device__ __forceinline__ void ws_fac_k(const SwLane &L, const double2 *x, int 
 // degrees, so the phases stay balanced without atomics.
 // side 0 = variables (ftov rows + P0 rows if want_p0 + evidence rows),
 // side 1 = factors (vtof rows unless iteration 1, + factor parameters).
-__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, int side,
+template <int NS>
+__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &sh, int side,
                                            const int4 *chunks, int first, int count, int stride,
-                                           bool want_msg, bool want_p0, int g, unsigned &seq) {
+                                           bool want_msg, bool want_p0, int g0, unsigned &seq) {
   const int lane = threadIdx.x & 31;
   const int *rowptr = side == 0 ? P.vrow : P.frow;
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
-  const double2 *msg = (side == 0 ? P.ftov : P.vtof) + (size_t)g * P.E * 32;
+  const double2 *msg = side == 0 ? P.ftov : P.vtof;
   // descriptors of the next 32 chunks of this CTA, one per lane
   int k = 0;
   int4 desc = first + lane * stride < count ? __ldg(chunks + first + lane * stride)
@@ -763,7 +850,7 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, i
     const unsigned slot = seq % kRing;
     if (lane == 0) {
       mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
-      WsChunk &ch = sh.ring[slot];
+      WsChunk<NS> &ch = sh.ring[slot];
       const int m = n1 - n0;
       const int heavy = r1 - r0 > kChR;
       ch.n0 = n0;
@@ -778,51 +865,65 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared &sh, i
       const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 256 : 0u;
       const unsigned b_ev = side == 0 ? (unsigned)m * 32 : 0u;
       const unsigned b_fp = side == 1 ? (unsigned)m * 16 : 0u;
-      mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_msg + b_p0 + b_ev + b_fp);
+      mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_fp + NS * (b_msg + b_p0 + b_ev));
       bulk_g2s(ch.rp, rowptr + rp_lo, b_rp, &sh.full[slot]);
       if (b_tw) bulk_g2s(ch.tw, twin + tw_lo, b_tw, &sh.full[slot]);
-      if (b_msg) bulk_g2s(ch.msg, msg + (size_t)r0 * 32, b_msg, &sh.full[slot]);
-      if (b_p0) bulk_g2s(ch.p0, P.p0 + ((size_t)g * P.V + n0) * 32, b_p0, &sh.full[slot]);
-      if (b_ev) bulk_g2s(ch.ev, P.ev + ((size_t)g * P.V + n0) * 32, b_ev, &sh.full[slot]);
       if (b_fp) bulk_g2s(ch.fpar, P.fpar + n0, b_fp, &sh.full[slot]);
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        const size_t g = (size_t)(g0 + u);
+        if (b_msg) bulk_g2s(ch.msg[u], msg + (g * P.E + r0) * 32, b_msg, &sh.full[slot]);
+        if (b_p0) bulk_g2s(ch.p0[u], P.p0 + (g * P.V + n0) * 32, b_p0, &sh.full[slot]);
+        if (b_ev) bulk_g2s(ch.ev[u], P.ev + (g * P.V + n0) * 32, b_ev, &sh.full[slot]);
+      }
     }
     ++seq;
   }
 }
 
-// Consumers: node i of the phase's node stream goes to warp (i mod 8), so the
-// warps stay balanced across chunks of any size.
-template <bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &sh, const SwLane &L,
-                                               int cw, int first, int count, int stride,
-                                               bool alive, unsigned &seq,
-                                               unsigned &uf) {
+// Consumers: node i of the phase's node stream goes to warp (i mod consumers),
+// so the warps stay balanced across chunks of any size.
+template <int NS, bool NORM, bool FIRST>
+__device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS> &sh,
+                                               const SwLane *L, int cw, int first, int count,
+                                               int stride, const bool *alive, unsigned &seq,
+                                               unsigned *uf) {
   const int lane = threadIdx.x & 31;
+  bool any = false;
+#pragma unroll
+  for (int u = 0; u < NS; ++u) any |= alive[u];
   int base = 0;
   for (int c = first; c < count; c += stride) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk &ch = sh.ring[slot];
+    const WsChunk<NS> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    const int start = (cw + kWsConsumers - base % kWsConsumers) % kWsConsumers;
-    if (alive) {
-      for (int f = n0 + start; f < n1; f += kWsConsumers) {
+    const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
+    if (any) {
+      for (int f = n0 + start; f < n1; f += WsCfg<NS>::consumers) {
         const int r = ch.rp[f - rp_lo];
         const int d = ch.rp[f + 1 - rp_lo] - r;
         if (!FIRST && d == 1) continue;  // unary: constant message, written in iteration 1
         const double2 pp = ch.fpar[f - n0];
         const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
         if (ch.heavy) {
+          // rows not staged: twins and messages from global memory
           const int *tw = P.vtof_twin + r;
-          const double2 *x = L.vtof + (size_t)r * 32;
-          if (!is_or) ws_fac_any<0, NORM, FIRST>(L, x, d, tw, pp, uf);
-          else ws_fac_any<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+#pragma unroll
+          for (int u = 0; u < NS; ++u) {
+            if (!alive[u]) continue;
+            const double2 *x = L[u].vtof + (size_t)r * 32;
+            if (!is_or) ws_fac_any<0, NORM, FIRST>(L[u], x, d, tw, pp, uf[u]);
+            else ws_fac_any<1, NORM, FIRST>(L[u], x, d, tw, pp, uf[u]);
+          }
         } else {
           const int *tw = ch.tw + (r - tw_lo);
-          const double2 *x = &ch.msg[r - r0][lane];
-          if (!is_or) ws_fac_k<0, NORM, FIRST>(L, x, d, tw, pp, uf);
-          else ws_fac_k<1, NORM, FIRST>(L, x, d, tw, pp, uf);
+          const double2 *x[NS];
+#pragma unroll
+          for (int u = 0; u < NS; ++u) x[u] = &ch.msg[u][r - r0][lane];
+          if (!is_or) ws_fac_k<0, NS, NORM, FIRST>(L, x, d, tw, pp, alive, uf);
+          else ws_fac_k<1, NS, NORM, FIRST>(L, x, d, tw, pp, alive, uf);
         }
       }
     }
@@ -833,46 +934,49 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared &s
   }
 }
 
-template <bool NORM>
-__device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &sh, const SwLane &L,
-                                               int cw, int first, int count, int stride, int it,
-                                               bool write_vtof, bool alive, unsigned &seq,
-                                               unsigned long long &dmax, unsigned &uf) {
+template <int NS, bool NORM>
+__device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS> &sh,
+                                               const SwLane *L, int cw, int first, int count,
+                                               int stride, int it, bool write_vtof,
+                                               const bool *alive, unsigned &seq,
+                                               unsigned long long *dmax, unsigned *uf) {
   const int lane = threadIdx.x & 31;
+  bool any = false;
+#pragma unroll
+  for (int u = 0; u < NS; ++u) any |= alive[u];
   int base = 0;
   for (int c = first; c < count; c += stride) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk &ch = sh.ring[slot];
+    const WsChunk<NS> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
-    const int start = (cw + kWsConsumers - base % kWsConsumers) % kWsConsumers;
-    if (alive) {
-      for (int v = n0 + start; v < n1; v += kWsConsumers) {
+    const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
+    if (any) {
+      for (int v = n0 + start; v < n1; v += WsCfg<NS>::consumers) {
         const int r = ch.rp[v - rp_lo];
         const int d = ch.rp[v + 1 - rp_lo] - r;
-        const unsigned code = ch.ev[v - n0][lane];
-        const double prev_p0 = it > 2 ? ch.p0[v - n0][lane] : 0.5;
+        unsigned code[NS];
+        double prev_p0[NS];
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+          code[u] = ch.ev[u][v - n0][lane];
+          prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : 0.5;
+        }
         if (ch.heavy) {
-          ws_var_any<NORM>(P, L, v, L.ftov + (size_t)r * 32, d, (const int *)P.ftov_twin + r, code,
-                           prev_p0, it, write_vtof, dmax, uf);
+#pragma unroll
+          for (int u = 0; u < NS; ++u)
+            if (alive[u])
+              ws_var_any<NORM>(P, L[u], v, L[u].ftov + (size_t)r * 32, d,
+                               (const int *)P.ftov_twin + r, code[u], prev_p0[u], it, write_vtof,
+                               dmax[u], uf[u]);
           continue;
         }
         const int *tw = ch.tw + (r - tw_lo);
-        const double2 *x = &ch.msg[r - r0][lane];
-        switch (d) {
-          case 1: ws_var<1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-          case 2: ws_var<2, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-          case 3: ws_var<3, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-          case 4: ws_var<4, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-#if HBP_WS_DMAX > 4
-          case 5: ws_var<5, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-          case 6: ws_var<6, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, dmax, uf); break;
-#endif
-          default:
-            ws_var_any<NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, dmax, uf);
-            break;
-        }
+        const double2 *x[NS];
+#pragma unroll
+        for (int u = 0; u < NS; ++u) x[u] = &ch.msg[u][r - r0][lane];
+        ws_var_k<NS, NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
       }
     }
     base += n1 - n0;
@@ -882,17 +986,32 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared &s
   }
 }
 
-template <bool NORM>
-__global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid_constant__ SweepParams P) {
+// grid (chunk stride, S/32/NS); CTA y serves set groups NS*y .. NS*y+NS-1
+template <bool NORM, int NS>
+__global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
+    sweep_ws(const __grid_constant__ SweepParams P) {
+  constexpr int kWsConsumers = WsCfg<NS>::consumers;
   extern __shared__ __align__(128) unsigned char ws_smem[];
-  WsShared &sh = *reinterpret_cast<WsShared *>(ws_smem);
+  WsShared<NS> &sh = *reinterpret_cast<WsShared<NS> *>(ws_smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool producer = warp == kWsConsumers;
-  const int g = blockIdx.y;
-  const int s = g * 32 + lane;
+  const int g0 = blockIdx.y * NS;
   const unsigned nblocks = gridDim.x * gridDim.y;
-  const SwLane L = sw_lane(P, s, P.E);
-  bool alive = s < P.nsets;
+  SwLane L[NS];
+  bool alive[NS];
+  int sidx[NS];
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
+    sidx[u] = (g0 + u) * 32 + lane;
+    L[u] = sw_lane(P, sidx[u], P.E);
+    alive[u] = sidx[u] < P.nsets;
+  }
+  auto any_alive = [&]() {
+    bool a = false;
+#pragma unroll
+    for (int u = 0; u < NS; ++u) a |= alive[u];
+    return a;
+  };
   unsigned expected = 0, seq = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
@@ -908,68 +1027,93 @@ __global__ void __launch_bounds__(kWsThreads, HBP_WS_MINB) sweep_ws(const __grid
   for (int it = 1;; ++it) {
     if (it >= 2) {
       const bool final_pass = it == P.max_it + 1;
-      unsigned long long dmax = 0;
-      unsigned uf = 0;  // last underflowing vtof slot + 1 of this thread's set
-      if (__syncthreads_or(alive)) {
+      unsigned long long dmax[NS];
+      unsigned uf[NS];  // last underflowing vtof slot + 1 per set
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        dmax[u] = 0;
+        uf[u] = 0;
+      }
+      if (__syncthreads_or(any_alive())) {
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce(P, sh, 0, P.vchunks, x, P.n_vchunks, nx, true, it > 2, g, seq);
+          ws_produce<NS>(P, sh, 0, P.vchunks, x, P.n_vchunks, nx, true, it > 2, g0, seq);
         } else {
-          ws_consume_var<NORM>(P, sh, L, warp, x, P.n_vchunks, nx, it, !final_pass, alive, seq,
-                               dmax, uf);
+          ws_consume_var<NS, NORM>(P, sh, L, warp, x, P.n_vchunks, nx, it, !final_pass, alive, seq,
+                                   dmax, uf);
         }
       }
-      if (!producer) sh.red[warp][lane] = dmax;
+      if (!producer)
+#pragma unroll
+        for (int u = 0; u < NS; ++u) sh.red[warp][u][lane] = dmax[u];
       __syncthreads();
       if (warp == 0) {
-        unsigned long long m = 0;
 #pragma unroll
-        for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][lane] > m ? sh.red[w][lane] : m;
-        if (alive) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + s], m);
+        for (int u = 0; u < NS; ++u) {
+          unsigned long long m = 0;
+#pragma unroll
+          for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][u][lane] > m ? sh.red[w][u][lane] : m;
+          if (alive[u]) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + sidx[u]], m);
+        }
       }
-      if (alive && !producer && uf) atomicMin(&P.ufkey[(size_t)it * P.S + s], (unsigned long long)(uf - 1));
+      if (!producer)
+#pragma unroll
+        for (int u = 0; u < NS; ++u)
+          if (alive[u] && uf[u])
+            atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]], (unsigned long long)(uf[u] - 1));
       if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
         P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
       sw_grid_sync(P.bar, expected, nblocks);
+      // stop decision for iteration done = it - 1: every thread of a set reads
+      // the same final values, so the decision is identical across CTAs
       const int done = it - 1;
-      int stop = 0;
-      if (alive) {
-        const size_t i = (size_t)done * P.S + s;
-        const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
-        const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
-        const int um = ((const volatile int *)P.ufmarg)[i];
-        const int tf = ((const volatile int *)P.tflag)[done];
-        if (uk != ~0ull || um != kNoVar) stop = 4;
-        else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
-        else if (done == P.max_it) stop = 2;
-        else if (tf) stop = 3;
-      }
-      if (stop) {
-        alive = false;
-        if (blockIdx.x == 0 && warp == 0) {
-          P.res_it[s] = done;
-          P.res_stop[s] = stop;
-          atomicAdd(P.nstop, 1u);
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        int stop = 0;
+        if (alive[u]) {
+          const size_t i = (size_t)done * P.S + sidx[u];
+          const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
+          const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
+          const int um = ((const volatile int *)P.ufmarg)[i];
+          const int tf = ((const volatile int *)P.tflag)[done];
+          if (uk != ~0ull || um != kNoVar) stop = 4;
+          else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
+          else if (done == P.max_it) stop = 2;
+          else if (tf) stop = 3;
+        }
+        if (stop) {
+          alive[u] = false;
+          if (blockIdx.x == 0 && warp == 0) {
+            P.res_it[sidx[u]] = done;
+            P.res_stop[sidx[u]] = stop;
+            atomicAdd(P.nstop, 1u);
+          }
         }
       }
     }
     {
-      unsigned uf = 0;  // last underflowing ftov slot + 1
-      if (__syncthreads_or(alive)) {
+      unsigned uf[NS];  // last underflowing ftov slot + 1 per set
+#pragma unroll
+      for (int u = 0; u < NS; ++u) uf[u] = 0;
+      if (__syncthreads_or(any_alive())) {
         const bool first = it == 1;
         // after iteration 1 the unary factors' chunks are skipped (constant messages)
         const int c0 = (first ? 0 : P.fchunk_nonunary) + x;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce(P, sh, 1, P.fchunks, c0, P.n_fchunks, nx, !first, false, g, seq);
+          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks, nx, !first, false, g0, seq);
         } else if (first) {
-          ws_consume_fac<NORM, true>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
+          ws_consume_fac<NS, NORM, true>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
         } else {
-          ws_consume_fac<NORM, false>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
+          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
         }
       }
-      if (alive && !producer && uf)
-        atomicMin(&P.ufkey[(size_t)it * P.S + s], (1ull << 32) | (unsigned long long)(uf - 1));
+      if (!producer)
+#pragma unroll
+        for (int u = 0; u < NS; ++u)
+          if (alive[u] && uf[u])
+            atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]],
+                      (1ull << 32) | (unsigned long long)(uf[u] - 1));
     }
     sw_grid_sync(P.bar, expected, nblocks);
     if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
@@ -1083,6 +1227,8 @@ struct hbp_sweep {
   int cap = 0;           // sets per pass (multiple of 32)
   int grid_x_max = 0;    // co-resident CTAs for the cooperative launch
   const void *kernel = nullptr, *kernel_nonorm = nullptr;
+  int ns = 1;           // sets per lane of the staged kernel (pass sizes are multiples of 32 * ns)
+  int threads = 0;
   int *d_vinv = nullptr;
   int *d_vrow = nullptr, *d_frow = nullptr, *d_vtof_twin = nullptr;  // padded copies (kPad)
   unsigned *d_ftov_twin = nullptr;
@@ -1148,12 +1294,23 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
     const char *kenv = getenv("HBP_SWEEP_KERNEL");
     sw->ws = !(kenv && std::string(kenv) == "plain");
     if (sw->ws) {
-      sw->smem = sizeof(hbp::WsShared);
-      sw->kernel = (const void *)hbp::sweep_ws<true>;
-      sw->kernel_nonorm = (const void *)hbp::sweep_ws<false>;
+      // HBP_SWEEP_NS: sets per lane (1 or 2)
+      const char *nenv = getenv("HBP_SWEEP_NS");
+      sw->ns = (nenv && atoi(nenv) == 1) ? 1 : hbp::kSweepNS;
+      if (sw->ns == 2) {
+        sw->smem = sizeof(hbp::WsShared<2>);
+        sw->threads = hbp::WsCfg<2>::threads;
+        sw->kernel = (const void *)hbp::sweep_ws<true, 2>;
+        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 2>;
+      } else {
+        sw->smem = sizeof(hbp::WsShared<1>);
+        sw->threads = hbp::WsCfg<1>::threads;
+        sw->kernel = (const void *)hbp::sweep_ws<true, 1>;
+        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 1>;
+      }
       for (const void *k : {sw->kernel, sw->kernel_nonorm})
         HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem));
-      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kWsThreads,
+      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, sw->threads,
                                                              sw->smem));
     } else {
       const char *env = getenv("HBP_SWEEP_MINB");
@@ -1171,8 +1328,9 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   size_t free_b = 0, total_b = 0;
   HBP_CUDA(cudaMemGetInfo(&free_b, &total_b));
   int cap = max_sets_per_pass > 0 ? max_sets_per_pass : (int)std::min<size_t>(4096, free_b / 2 / per_set);
-  cap = std::max(32, (cap + 31) / 32 * 32);
-  cap = std::min(cap, 32 * sw->grid_x_max);
+  const int unit = 32 * sw->ns;
+  cap = std::max(unit, (cap + unit - 1) / unit * unit);
+  cap = std::min(cap, unit * sw->grid_x_max);
   sw->cap = cap;
   hbp_status st;
   if ((st = upload(&sw->d_vinv, L.vinv, g->stream))) return st;
@@ -1387,7 +1545,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   double dev_ms = 0, ker_ms = 0;
   for (int base = 0; base < n; base += cap) {
     const int ns = std::min(cap, n - base);
-    const int S = (ns + 31) / 32 * 32;
+    const int unit = 32 * sw->ns;
+    const int S = (ns + unit - 1) / unit * unit;
     const int groups = S / 32;
     const int nx = std::max(1, std::min(sw->grid_x_max / groups, (L.F + hbp::kSwWarps - 1) / hbp::kSwWarps));
     P.S = S;
@@ -1422,9 +1581,10 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
     if (sw->ws) {
-      const int nxw = std::max(1, std::min(sw->grid_x_max / groups, sw->n_vchunks));
+      const int gy = groups / sw->ns;
+      const int nxw = std::max(1, std::min(sw->grid_x_max / gy, sw->n_vchunks));
       HBP_CUDA(cudaLaunchCooperativeKernel(P.normalize ? sw->kernel : sw->kernel_nonorm,
-                                           dim3(nxw, groups), dim3(hbp::kWsThreads), args, sw->smem,
+                                           dim3(nxw, gy), dim3(sw->threads), args, sw->smem,
                                            st));
     } else {
       HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups), dim3(hbp::kSwThreads), args,
