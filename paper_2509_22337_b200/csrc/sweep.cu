@@ -51,7 +51,7 @@ constexpr int kSwWarps = 8;  // warps per CTA (blockDim = 256); lanes = 32 sets
 constexpr int kSwThreads = 32 * kSwWarps;
 constexpr int kSwMinBlocks = 4;  // default register budget: 4 CTAs (32 warps) per SM
 #ifndef HBP_SWEEP_NS
-#define HBP_SWEEP_NS 2
+#define HBP_SWEEP_NS 1
 #endif
 constexpr int kSweepNS = HBP_SWEEP_NS;  // default sets per lane of the staged kernel
 constexpr int kNoVar = 0x7f7f7f7f;  // ufmarg reset value (memset 0x7F)
@@ -1294,9 +1294,10 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
     const char *kenv = getenv("HBP_SWEEP_KERNEL");
     sw->ws = !(kenv && std::string(kenv) == "plain");
     if (sw->ws) {
-      // HBP_SWEEP_NS: sets per lane (1 or 2)
+      // HBP_SWEEP_NS: sets per lane (1 or 2). Measured on B200 (1,024 ftp
+      // sets): NS=1 182-184 ms, NS=2 209 ms -- the default stays 1.
       const char *nenv = getenv("HBP_SWEEP_NS");
-      sw->ns = (nenv && atoi(nenv) == 1) ? 1 : hbp::kSweepNS;
+      sw->ns = nenv ? (atoi(nenv) == 2 ? 2 : 1) : hbp::kSweepNS;
       if (sw->ns == 2) {
         sw->smem = sizeof(hbp::WsShared<2>);
         sw->threads = hbp::WsCfg<2>::threads;
