@@ -78,6 +78,7 @@ struct SweepParams {
   int *tflag;                 // [iteration] time limit exceeded
   int *res_it, *res_stop;     // [S] stopping iteration, reason
   unsigned *nstop;            // sets stopped so far (padding counts as stopped)
+  unsigned *claim;            // [2][gridDim.y] chunk claim counters (ping-pong by phase)
   unsigned *bar;              // grid barrier arrivals
   unsigned long long *t0;
   int max_it, normalize;
@@ -830,27 +831,35 @@ __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, 
 // side 1 = factors (vtof rows unless iteration 1, + factor parameters).
 template <int NS>
 __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &sh, int side,
-                                           const int4 *chunks, int first, int count, int stride,
-                                           bool want_msg, bool want_p0, int g0, unsigned &seq) {
+                                           const int4 *chunks, int cfirst, int count,
+                                           unsigned *claim, bool want_msg, bool want_p0, int g0,
+                                           unsigned &seq) {
   const int lane = threadIdx.x & 31;
   const int *rowptr = side == 0 ? P.vrow : P.frow;
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
   const double2 *msg = side == 0 ? P.ftov : P.vtof;
-  // descriptors of the next 32 chunks of this CTA, one per lane
-  int k = 0;
-  int4 desc = first + lane * stride < count ? __ldg(chunks + first + lane * stride)
-                                            : make_int4(0, 0, 0, 0);
-  for (int c = first; c < count; c += stride, ++k) {
-    if (k == 32) {
-      k = 0;
-      desc = c + lane * stride < count ? __ldg(chunks + c + lane * stride) : make_int4(0, 0, 0, 0);
-    }
-    const int n0 = __shfl_sync(0xffffffffu, desc.x, k), n1 = __shfl_sync(0xffffffffu, desc.y, k);
-    const int r0 = __shfl_sync(0xffffffffu, desc.z, k), r1 = __shfl_sync(0xffffffffu, desc.w, k);
-    const unsigned slot = seq % kRing;
-    if (lane == 0) {
+  if (lane != 0) return;
+  // chunks are claimed two at a time from the CTA row's counter; the next
+  // claim is in flight while the current pair is staged
+  unsigned k = atomicAdd(claim, 2u);
+  for (;;) {
+    // claim the next pair only if this pair is whole: every claim's result is
+    // then consumed before the producer leaves the phase (no atomic in flight
+    // when the counter is zeroed for a later phase)
+    const unsigned kn = (cfirst + (int)k + 1 < count) ? atomicAdd(claim, 2u) : 0u;
+    for (int h = 0; h < 2; ++h) {
+      const int c = cfirst + (int)k + h;
+      const unsigned slot = seq % kRing;
       mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
       WsChunk<NS> &ch = sh.ring[slot];
+      ++seq;
+      if (c >= count) {  // end of the phase's chunks: a sentinel, no bytes
+        ch.n0 = -1;
+        mbar_arrive(&sh.full[slot]);
+        return;
+      }
+      const int4 desc = __ldg(chunks + c);
+      const int n0 = desc.x, n1 = desc.y, r0 = desc.z, r1 = desc.w;
       const int m = n1 - n0;
       const int heavy = r1 - r0 > kChR;
       ch.n0 = n0;
@@ -877,7 +886,7 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &s
         if (b_ev) bulk_g2s(ch.ev[u], P.ev + (g * P.V + n0) * 32, b_ev, &sh.full[slot]);
       }
     }
-    ++seq;
+    k = kn;
   }
 }
 
@@ -885,19 +894,24 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &s
 // so the warps stay balanced across chunks of any size.
 template <int NS, bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS> &sh,
-                                               const SwLane *L, int cw, int first, int count,
-                                               int stride, const bool *alive, unsigned &seq,
-                                               unsigned *uf) {
+                                               const SwLane *L, int cw, const bool *alive,
+                                               unsigned &seq, unsigned *uf) {
   const int lane = threadIdx.x & 31;
   bool any = false;
 #pragma unroll
   for (int u = 0; u < NS; ++u) any |= alive[u];
   int base = 0;
-  for (int c = first; c < count; c += stride) {
+  for (;;) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
     const WsChunk<NS> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
+    if (n0 < 0) {  // the producer's end-of-phase sentinel
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[slot]);
+      ++seq;
+      break;
+    }
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
     const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
     if (any) {
@@ -936,8 +950,7 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
 
 template <int NS, bool NORM>
 __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS> &sh,
-                                               const SwLane *L, int cw, int first, int count,
-                                               int stride, int it, bool write_vtof,
+                                               const SwLane *L, int cw, int it, bool write_vtof,
                                                const bool *alive, unsigned &seq,
                                                unsigned long long *dmax, unsigned *uf) {
   const int lane = threadIdx.x & 31;
@@ -945,11 +958,17 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
 #pragma unroll
   for (int u = 0; u < NS; ++u) any |= alive[u];
   int base = 0;
-  for (int c = first; c < count; c += stride) {
+  for (;;) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
     const WsChunk<NS> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
+    if (n0 < 0) {  // the producer's end-of-phase sentinel
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[slot]);
+      ++seq;
+      break;
+    }
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
     const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
     if (any) {
@@ -1020,7 +1039,14 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int x = blockIdx.x, nx = gridDim.x;
+  // chunk claims: phase q = 2 it + side uses counter (q & 1) of this CTA row;
+  // CTA x == 0 of the row zeroes the other one for phase q + 1 (its last use
+  // was phase q - 1, behind the grid barrier that opened phase q)
+  auto claim_of = [&](int it, int side) -> unsigned * {
+    const int q = 2 * it + side;
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) P.claim[((q + 1) & 1) * gridDim.y + blockIdx.y] = 0;
+    return P.claim + (q & 1) * gridDim.y + blockIdx.y;
+  };
   __syncthreads();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
 
@@ -1037,10 +1063,10 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
       if (__syncthreads_or(any_alive())) {
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 0, P.vchunks, x, P.n_vchunks, nx, true, it > 2, g0, seq);
+          ws_produce<NS>(P, sh, 0, P.vchunks, 0, P.n_vchunks, claim_of(it, 0), true, it > 2, g0,
+                         seq);
         } else {
-          ws_consume_var<NS, NORM>(P, sh, L, warp, x, P.n_vchunks, nx, it, !final_pass, alive, seq,
-                                   dmax, uf);
+          ws_consume_var<NS, NORM>(P, sh, L, warp, it, !final_pass, alive, seq, dmax, uf);
         }
       }
       if (!producer)
@@ -1098,14 +1124,15 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
       if (__syncthreads_or(any_alive())) {
         const bool first = it == 1;
         // after iteration 1 the unary factors' chunks are skipped (constant messages)
-        const int c0 = (first ? 0 : P.fchunk_nonunary) + x;
+        const int c0 = first ? 0 : P.fchunk_nonunary;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks, nx, !first, false, g0, seq);
+          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks, claim_of(it, 1), !first, false, g0,
+                         seq);
         } else if (first) {
-          ws_consume_fac<NS, NORM, true>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
+          ws_consume_fac<NS, NORM, true>(P, sh, L, warp, alive, seq, uf);
         } else {
-          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, c0, P.n_fchunks, nx, alive, seq, uf);
+          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, alive, seq, uf);
         }
       }
       if (!producer)
@@ -1465,7 +1492,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   const size_t o_db = 0, o_uk = o_db + align256(nit * cap * 8), o_um = o_uk + align256(nit * cap * 8),
                o_tf = o_um + align256(nit * cap * 4), o_ri = o_tf + align256(nit * 4),
                o_rs = o_ri + align256((size_t)cap * 4), o_misc = o_rs + align256((size_t)cap * 4),
-               ctrl_need = o_misc + 256;
+               o_claim = o_misc + 256, ctrl_need = o_claim + align256((size_t)cap / 32 * 8 + 8);
   hbp_status s_;
   if ((s_ = ensure(&sw->d_ctrl, &sw->ctrl_bytes, ctrl_need))) return s_;
   char *cb = (char *)sw->d_ctrl;
@@ -1475,6 +1502,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       *d_rs = (int *)(cb + o_rs);
   unsigned *d_nstop = (unsigned *)(cb + o_misc), *d_bar = d_nstop + 1;
   unsigned long long *d_t0 = (unsigned long long *)(cb + o_misc + 64);
+  unsigned *d_claim = (unsigned *)(cb + o_claim);
   // scratch: evidence (set, var, val) for one pass, selection, output staging
   const bool marg_dev = out->marginals && out->marginals_on_device;
   const bool p1_dev = out->p1_select && out->p1_on_device;
@@ -1530,6 +1558,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.res_it = d_ri;
   P.res_stop = d_rs;
   P.nstop = d_nstop;
+  P.claim = d_claim;
   P.bar = d_bar;
   P.t0 = d_t0;
   P.max_it = max_it;
@@ -1576,6 +1605,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemsetAsync(d_um, 0x7F, nit * S * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_tf, 0, nit * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_ri, 0, (size_t)S * 4, st));
+    HBP_CUDA(cudaMemsetAsync(d_claim, 0, (size_t)cap / 32 * 8 + 8, st));
     HBP_CUDA(cudaMemsetAsync(d_rs, 0, (size_t)S * 4, st));
     const unsigned misc[2] = {(unsigned)(S - ns), 0u};
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
