@@ -29,3 +29,28 @@ def test_bad_arguments_raise_before_the_device():
         P.run_many(g, [[]], options=P.EngineOptions(record_history=True))
     with pytest.raises(ValueError):
         P.run_many(g, [[]], options=P.EngineOptions(max_iterations=0))
+
+
+def test_sweep_algorithmic_bytes_formula():
+    """bench.sweep_set_bytes restates DESIGN.md's per-set byte count; check it
+    against a direct count of what the staged kernel moves for tiny graphs."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    g, _ = W.graph("weblech")
+    V, F, E = g.num_variables, g.num_factors, g.num_edges
+    deg = np.diff(np.asarray(g.rowptr))
+    T = int(deg[deg > 1].sum())
+    for n, max_it in ((1, 1000), (5, 1000), (7, 7)):
+        # factor side: iteration 1 writes all E, later ones read + write T;
+        # variable side n times: read E ftov + V evidence bytes, write V P0,
+        # read V P0 after the first, write T vtof unless the run hit max_iterations
+        fac = 16 * E + (n - 1) * 32 * T
+        var = n * (16 * E + V) + n * 8 * V + (n - 1) * 8 * V + (n - (n == max_it)) * 16 * T
+        idx = n * (4 * (V + 1) + 4 * E + 4 * (F + 1) + 4 * E + 16 * F) / 32.0
+        got = float(bench.sweep_set_bytes(g, np.array([n]), max_it)[0])
+        assert got == fac + var + idx
