@@ -47,7 +47,6 @@ struct Ctrl {
   int converged;
   int stop;          // 1 converged, 2 max_iterations, 3 time limit, 4 underflow
   unsigned long long t0;
-  unsigned claim[4];  // PARALL chunk claims: [phase + 2 * (iteration & 1)]
 };
 
 struct KParams {
@@ -89,7 +88,6 @@ struct KParams {
   double2 *hist;                   // [max_it][V] or null
   unsigned long long *trace;       // debug: [kTraceIters][nphases][grid][2] or null
   int csize;                       // CTAs of cluster 0, which runs the small levels
-  unsigned *claim;                 // [4] chunk claim counters of the PARALL phases (or null)
   int max_it;
   int normalize;
   double tol;
@@ -567,43 +565,30 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
       c0 = (threadIdx.x >> 5) * P.csize + blockIdx.x;
       cstride = P.csize * (blockDim.x >> 5);
     }
-    // Every warp takes one chunk statically; the rest are claimed from the
-    // phase's counter (dynamic load balance: the slowest warp no longer sets
-    // the phase time). The next claim is issued before the current chunk is
-    // computed, so it costs no latency. Without a counter: static striding.
-    unsigned *ctr = P.claim ? P.claim + (pidx + (it & 1) * 2) % 4 : nullptr;
-    auto next_chunk = [&](int c) -> int {
-      if (!ctr || !ph.grid) return c + cstride;
-      unsigned k = 0;
-      if (lane == 0) k = atomicAdd(ctr, 1u);
-      return cstride + (int)__shfl_sync(0xffffffffu, k, 0);
-    };
     if (ph.type == 0) {
       const bool marg = do_marg && ph.marg;
       if (marg || do_vtof)
-        for (int c = c0; c * 32 < total;) {
-          const int cn = next_chunk(c);
+        for (int c = c0; c * 32 < total; c += cstride) {
           const int i = c * 32 + lane;
+          if (i >= total) break;
           if (i < nn) {
             vnode(P, ph.begin + i, marg, do_vtof, it, pidx, dmax, ufkey, it == 1 && pidx == 0);
-          } else if (i < total) {
+          } else {
             const int q = ph.sbegin + (i - nn);
             v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
                    pidx, dmax, ufkey, it == 1 && pidx == 0);
           }
-          c = cn;
         }
     } else {
-      for (int c = c0; c * 32 < total;) {
-        const int cn = next_chunk(c);
+      for (int c = c0; c * 32 < total; c += cstride) {
         const int i = c * 32 + lane;
+        if (i >= total) break;
         if (i < nn) {
           fnode(P, ph.begin + i, pidx, it == 1, ufkey);
-        } else if (i < total) {
+        } else {
           const int p = ph.sbegin + (i - nn);
           f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
         }
-        c = cn;
       }
     }
     flush_underflow(P, it, ufkey);
@@ -748,9 +733,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
   for (int it = 1;; ++it) {
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
-    // zero the claim counter this phase will use next iteration (its last use
-    // was the previous iteration, behind the barrier that opened this phase)
-    if (P.claim && blockIdx.x == 0 && threadIdx.x == 0) P.claim[0 + 2 * ((it + 1) & 1)] = 0;
     trace_mark(P, it, 0, 0);
     exec_phase(P, P.phases[0], 0, it, it > 1, !final_pass, dmax);
     trace_mark(P, it, 0, 1);
@@ -814,7 +796,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
         }
       }
       unsigned long long unused = 0;
-      if (P.claim && p == 1 && blockIdx.x == 0 && threadIdx.x == 0) P.claim[1 + 2 * ((it + 1) & 1)] = 0;
       trace_mark(P, it, p, 0);
       exec_phase(P, ph, p, it, false, true, unused);
       trace_mark(P, it, p, 1);
@@ -1286,11 +1267,6 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.nphases = (int)p->host.phases.size();
   P.items = p->d_items;
   P.ctrl = c.ctrl;
-  // dynamic chunk claims for PARALL's two whole-graph phases
-  P.claim = (p->host.phases.size() == 2 && p->host.phases[0].list == 2 &&
-             p->host.phases[1].list == 2 && !getenv("HBP_STATIC_CHUNKS"))
-                ? c.ctrl->claim
-                : nullptr;
   P.delta_bits = c.delta_bits;
   P.uf_msg = c.uf_msg;
   P.uf_marg = c.uf_marg;
