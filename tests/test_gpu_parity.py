@@ -366,3 +366,19 @@ def test_shared_reciprocal_division_is_ddiv_rn():
                                              _native.ptr(fast, C.c_double), _native.ptr(ref, C.c_double))
     assert st == 0, _native.last_error()
     assert fast.tobytes() == ref.tobytes()
+
+
+def test_long_rows_bitwise_vs_oracle():
+    """Variable rows of 40+ slots and a 41-slot clause: the slot-per-thread
+    heavy paths of the single-graph executor, all strategies."""
+    from builders import hub_graph
+    rng = np.random.default_rng(123)
+    for trial in range(4):
+        g = hub_graph(rng)
+        for strat in (Strategy.parall(), Strategy.seqfix()):
+            sched = strat.compile(g)
+            opts = EngineOptions(max_iterations=60, tolerance=1e-12)
+            res, o = device_vs_oracle(g, sched, opts)
+            assert res.iterations == o["iterations"]
+            assert res.marginals.tobytes() == o["marginals"].tobytes(), (trial, strat.kind)
+            assert np.asarray(res.deltas).tobytes() == o["deltas"].tobytes()

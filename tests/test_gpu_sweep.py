@@ -150,3 +150,16 @@ def test_sweep_non_parall_strategy_materialises():
         cur = clamp_all(g, pairs)
         r = P.run(cur, Strategy.seqfix().compile(cur), EngineOptions(1000, 1e-9))
         assert res.marginals[j].tobytes() == r.marginals.tobytes()
+
+
+def test_sweep_long_rows_heavy_chunks():
+    """Rows longer than a staged chunk (32 rows) take the heavy path (rows read
+    from global memory); bitwise against the oracle, evidence on the hub."""
+    from builders import hub_graph
+    rng = np.random.default_rng(321)
+    g = hub_graph(rng, hub_degree=45, wide_body=44)
+    sets = [[], [(0, True)], [(0, False), (3, True)], [(g.num_variables - 2, True)]] + \
+        random_sets(rng, g.num_variables, 40, max_size=3)
+    opts = EngineOptions(max_iterations=80, tolerance=1e-12)
+    res = P.run_many(g, sets, None, opts)
+    check_against_oracle(g, sets, opts, res)
