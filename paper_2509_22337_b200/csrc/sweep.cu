@@ -1006,31 +1006,46 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
 }
 
 // grid (chunk stride, S/32/NS); CTA y serves set groups NS*y .. NS*y+NS-1
+// stop decision for set s after iteration done (delta < tol, max_iterations,
+// time limit, underflow): a pure function of final per-set values, so every
+// CTA that evaluates it gets the same answer
+__device__ __forceinline__ int sw_decide(const SweepParams &P, int s, int done) {
+  const size_t i = (size_t)done * P.S + s;
+  const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
+  const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
+  const int um = ((const volatile int *)P.ufmarg)[i];
+  const int tf = ((const volatile int *)P.tflag)[done];
+  if (uk != ~0ull || um != kNoVar) return 4;
+  if (__longlong_as_double((long long)db) < P.tol) return 1;
+  if (done == P.max_it) return 2;
+  if (tf) return 3;
+  return 0;
+}
+
+constexpr int kMaxUnits = 512;  // CTA rows (units of NS x 32 sets) a pass may have
+
+// grid (CTAs per unit, S/32/NS); unit y = set groups NS*y .. NS*y+NS-1.
+// Row adoption: a CTA whose own unit has no running set works, phase by
+// phase, for a unit that still has one (round-robin over the running units,
+// sharing its chunk claims) -- so the tail of the sweep, when a few straggler
+// sets keep iterating, runs on the whole GPU instead of on their own CTAs.
 template <bool NORM, int NS>
 __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     sweep_ws(const __grid_constant__ SweepParams P) {
   constexpr int kWsConsumers = WsCfg<NS>::consumers;
+  constexpr int kWarps = kWsConsumers + 1;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   WsShared<NS> &sh = *reinterpret_cast<WsShared<NS> *>(ws_smem);
+  __shared__ unsigned umask[kMaxUnits][NS];  // running sets per unit, one bit per lane
+  __shared__ int ulist[kMaxUnits];            // running units, ascending
+  __shared__ int s_nunits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool producer = warp == kWsConsumers;
-  const int g0 = blockIdx.y * NS;
+  const int units = gridDim.y;
   const unsigned nblocks = gridDim.x * gridDim.y;
   SwLane L[NS];
   bool alive[NS];
   int sidx[NS];
-#pragma unroll
-  for (int u = 0; u < NS; ++u) {
-    sidx[u] = (g0 + u) * 32 + lane;
-    L[u] = sw_lane(P, sidx[u], P.E);
-    alive[u] = sidx[u] < P.nsets;
-  }
-  auto any_alive = [&]() {
-    bool a = false;
-#pragma unroll
-    for (int u = 0; u < NS; ++u) a |= alive[u];
-    return a;
-  };
   unsigned expected = 0, seq = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
@@ -1039,16 +1054,62 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // chunk claims: phase q = 2 it + side uses counter (q & 1) of this CTA row;
-  // CTA x == 0 of the row zeroes the other one for phase q + 1 (its last use
-  // was phase q - 1, behind the grid barrier that opened phase q)
-  auto claim_of = [&](int it, int side) -> unsigned * {
-    const int q = 2 * it + side;
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) P.claim[((q + 1) & 1) * gridDim.y + blockIdx.y] = 0;
-    return P.claim + (q & 1) * gridDim.y + blockIdx.y;
-  };
   __syncthreads();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
+
+  // Running sets of every unit (phase B: minus the decision taken at `done`),
+  // then this CTA's unit for the phase: its own while it has running sets,
+  // otherwise an adopted one. Returns the unit or -1 (nothing to do).
+  auto pick_unit = [&](bool after_decision, int done) -> int {
+    for (int r = warp; r < units; r += kWarps) {
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        const int s = (r * NS + u) * 32 + lane;
+        bool run = s < P.nsets && ((const volatile int *)P.res_stop)[s] == 0;
+        if (run && after_decision) run = sw_decide(P, s, done) == 0;
+        const unsigned m = __ballot_sync(0xffffffffu, run);
+        if (lane == 0) umask[r][u] = m;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int base = 0;
+      for (int r0 = 0; r0 < units; r0 += 32) {
+        const int r = r0 + lane;
+        bool any = false;
+        if (r < units)
+#pragma unroll
+          for (int u = 0; u < NS; ++u) any |= umask[r][u] != 0;
+        const unsigned b = __ballot_sync(0xffffffffu, any);
+        if (any) ulist[base + __popc(b & ((1u << lane) - 1))] = r;
+        base += __popc(b);
+      }
+      if (lane == 0) s_nunits = base;
+    }
+    __syncthreads();
+    const int n = s_nunits;
+    if (n == 0) return -1;
+    const int own = blockIdx.y;
+    bool own_runs = false;
+#pragma unroll
+    for (int u = 0; u < NS; ++u) own_runs |= umask[own][u] != 0;
+    if (own_runs) return own;
+    return ulist[(int)((blockIdx.y * gridDim.x + blockIdx.x) % (unsigned)n)];
+  };
+  auto bind_unit = [&](int t) {
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+      sidx[u] = (t * NS + u) * 32 + lane;
+      L[u] = sw_lane(P, sidx[u], P.E);
+      alive[u] = (umask[t][u] >> lane) & 1u;
+    }
+  };
+  // chunk claims: phase q = 2 it + side uses counter (q & 1) of the unit;
+  // CTA x == 0 of each unit zeroes the unit's other counter for phase q + 1
+  // (its last use was phase q - 1, behind the barrier that opened phase q)
+  auto reset_claims = [&](int q) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.claim[((q + 1) & 1) * units + blockIdx.y] = 0;
+  };
 
   for (int it = 1;; ++it) {
     if (it >= 2) {
@@ -1060,59 +1121,53 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         dmax[u] = 0;
         uf[u] = 0;
       }
-      if (__syncthreads_or(any_alive())) {
+      reset_claims(2 * it);
+      const int t = pick_unit(false, 0);
+      if (t >= 0) {
+        bind_unit(t);
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 0, P.vchunks, 0, P.n_vchunks, claim_of(it, 0), true, it > 2, g0,
-                         seq);
+          ws_produce<NS>(P, sh, 0, P.vchunks, 0, P.n_vchunks, P.claim + (size_t)((2 * it) & 1) * units + t,
+                         true, it > 2, t * NS, seq);
         } else {
           ws_consume_var<NS, NORM>(P, sh, L, warp, it, !final_pass, alive, seq, dmax, uf);
         }
-      }
-      if (!producer)
+        if (!producer)
 #pragma unroll
-        for (int u = 0; u < NS; ++u) sh.red[warp][u][lane] = dmax[u];
-      __syncthreads();
-      if (warp == 0) {
+          for (int u = 0; u < NS; ++u) sh.red[warp][u][lane] = dmax[u];
+        __syncthreads();
+        if (warp == 0) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) {
-          unsigned long long m = 0;
+          for (int u = 0; u < NS; ++u) {
+            unsigned long long m = 0;
 #pragma unroll
-          for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][u][lane] > m ? sh.red[w][u][lane] : m;
-          if (alive[u]) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + sidx[u]], m);
+            for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][u][lane] > m ? sh.red[w][u][lane] : m;
+            if (alive[u]) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + sidx[u]], m);
+          }
         }
-      }
-      if (!producer)
+        if (!producer)
 #pragma unroll
-        for (int u = 0; u < NS; ++u)
-          if (alive[u] && uf[u])
-            atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]], (unsigned long long)(uf[u] - 1));
+          for (int u = 0; u < NS; ++u)
+            if (alive[u] && uf[u])
+              atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]], (unsigned long long)(uf[u] - 1));
+      }
       if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
         P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
       sw_grid_sync(P.bar, expected, nblocks);
-      // stop decision for iteration done = it - 1: every thread of a set reads
-      // the same final values, so the decision is identical across CTAs
+      // stop decisions for iteration done = it - 1, recorded once per set by
+      // CTA x == 0 of the set's own unit
       const int done = it - 1;
+      if (blockIdx.x == 0 && warp == 0) {
 #pragma unroll
-      for (int u = 0; u < NS; ++u) {
-        int stop = 0;
-        if (alive[u]) {
-          const size_t i = (size_t)done * P.S + sidx[u];
-          const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
-          const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
-          const int um = ((const volatile int *)P.ufmarg)[i];
-          const int tf = ((const volatile int *)P.tflag)[done];
-          if (uk != ~0ull || um != kNoVar) stop = 4;
-          else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
-          else if (done == P.max_it) stop = 2;
-          else if (tf) stop = 3;
-        }
-        if (stop) {
-          alive[u] = false;
-          if (blockIdx.x == 0 && warp == 0) {
-            P.res_it[sidx[u]] = done;
-            P.res_stop[sidx[u]] = stop;
-            atomicAdd(P.nstop, 1u);
+        for (int u = 0; u < NS; ++u) {
+          const int sh_s = (blockIdx.y * NS + u) * 32 + lane;
+          if (sh_s < P.nsets && ((const volatile int *)P.res_stop)[sh_s] == 0) {
+            const int stop = sw_decide(P, sh_s, done);
+            if (stop) {
+              P.res_it[sh_s] = done;
+              P.res_stop[sh_s] = stop;
+              atomicAdd(P.nstop, 1u);
+            }
           }
         }
       }
@@ -1121,26 +1176,32 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
       unsigned uf[NS];  // last underflowing ftov slot + 1 per set
 #pragma unroll
       for (int u = 0; u < NS; ++u) uf[u] = 0;
-      if (__syncthreads_or(any_alive())) {
+      reset_claims(2 * it + 1);
+      // the decision just taken is not visible through res_stop yet for other
+      // CTAs: pick_unit re-evaluates it (same inputs, same answer)
+      const int t = pick_unit(it >= 2, it - 1);
+      if (t >= 0) {
+        bind_unit(t);
         const bool first = it == 1;
         // after iteration 1 the unary factors' chunks are skipped (constant messages)
         const int c0 = first ? 0 : P.fchunk_nonunary;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks, claim_of(it, 1), !first, false, g0,
+          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks,
+                         P.claim + (size_t)((2 * it + 1) & 1) * units + t, !first, false, t * NS,
                          seq);
         } else if (first) {
           ws_consume_fac<NS, NORM, true>(P, sh, L, warp, alive, seq, uf);
         } else {
           ws_consume_fac<NS, NORM, false>(P, sh, L, warp, alive, seq, uf);
         }
-      }
-      if (!producer)
+        if (!producer)
 #pragma unroll
-        for (int u = 0; u < NS; ++u)
-          if (alive[u] && uf[u])
-            atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]],
-                      (1ull << 32) | (unsigned long long)(uf[u] - 1));
+          for (int u = 0; u < NS; ++u)
+            if (alive[u] && uf[u])
+              atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]],
+                        (1ull << 32) | (unsigned long long)(uf[u] - 1));
+      }
     }
     sw_grid_sync(P.bar, expected, nblocks);
     if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
