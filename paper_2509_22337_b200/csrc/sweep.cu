@@ -79,6 +79,14 @@ struct SweepParams {
   int *res_it, *res_stop;     // [S] stopping iteration, reason
   unsigned *nstop;            // sets stopped so far (padding counts as stopped)
   unsigned *claim;            // [2][gridDim.y] chunk claim counters (ping-pong by phase)
+  // staged kernel: set compaction. Sets live in slots; slot2set[slot] (-1:
+  // empty) changes when the running sets are packed into fewer tiles, and the
+  // state is double buffered (the vtof buffer receives the packed ftov rows)
+  double *p0_alt;
+  unsigned char *ev_alt;
+  int *slot2set;              // [S]
+  int *res_pos;               // [S] per set: slot | buffer parity << 30 of its final P0
+  int compact;                // 1: pack the running sets when that halves the live tiles
   unsigned *bar;              // grid barrier arrivals
   unsigned long long *t0;
   int max_it, normalize;
@@ -122,6 +130,25 @@ struct SwLane {
   const unsigned char *ev;
   int s;                    // set index within the pass
 };
+
+// current state buffers of the staged kernel (swapped by a compaction)
+struct SwBufs {
+  double2 *ftov, *vtof;
+  double *p0;
+  unsigned char *ev;
+  int parity;  // 0: the pass's original p0 / ev buffers, 1: the alternates
+};
+
+__device__ __forceinline__ SwLane sw_lane_b(const SwBufs &B, int slot, int set, int E, int V) {
+  const int g = slot >> 5, lane = slot & 31;
+  SwLane L;
+  L.vtof = B.vtof + (size_t)g * E * 32 + lane;
+  L.ftov = B.ftov + (size_t)g * E * 32 + lane;
+  L.p0 = B.p0 + (size_t)g * V * 32 + lane;
+  L.ev = B.ev + (size_t)g * V * 32 + lane;
+  L.s = set;
+  return L;
+}
 
 __device__ __forceinline__ SwLane sw_lane(const SweepParams &P, int s, int E) {
   const int g = s >> 5, lane = s & 31;
@@ -830,14 +857,14 @@ __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, 
 // side 0 = variables (ftov rows + P0 rows if want_p0 + evidence rows),
 // side 1 = factors (vtof rows unless iteration 1, + factor parameters).
 template <int NS>
-__device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &sh, int side,
-                                           const int4 *chunks, int cfirst, int count,
+__device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B, WsShared<NS> &sh,
+                                           int side, const int4 *chunks, int cfirst, int count,
                                            unsigned *claim, bool want_msg, bool want_p0, int g0,
                                            unsigned &seq) {
   const int lane = threadIdx.x & 31;
   const int *rowptr = side == 0 ? P.vrow : P.frow;
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
-  const double2 *msg = side == 0 ? P.ftov : P.vtof;
+  const double2 *msg = side == 0 ? B.ftov : B.vtof;
   if (lane != 0) return;
   // chunks are claimed two at a time from the CTA row's counter; the next
   // claim is in flight while the current pair is staged
@@ -882,8 +909,8 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, WsShared<NS> &s
       for (int u = 0; u < NS; ++u) {
         const size_t g = (size_t)(g0 + u);
         if (b_msg) bulk_g2s(ch.msg[u], msg + (g * P.E + r0) * 32, b_msg, &sh.full[slot]);
-        if (b_p0) bulk_g2s(ch.p0[u], P.p0 + (g * P.V + n0) * 32, b_p0, &sh.full[slot]);
-        if (b_ev) bulk_g2s(ch.ev[u], P.ev + (g * P.V + n0) * 32, b_ev, &sh.full[slot]);
+        if (b_p0) bulk_g2s(ch.p0[u], B.p0 + (g * P.V + n0) * 32, b_p0, &sh.full[slot]);
+        if (b_ev) bulk_g2s(ch.ev[u], B.ev + (g * P.V + n0) * 32, b_ev, &sh.full[slot]);
       }
     }
     k = kn;
@@ -1022,13 +1049,23 @@ __device__ __forceinline__ int sw_decide(const SweepParams &P, int s, int done) 
   return 0;
 }
 
-constexpr int kMaxUnits = 512;  // CTA rows (units of NS x 32 sets) a pass may have
+constexpr int kMaxUnits = 512;     // CTA rows (units of NS x 32 sets) a pass may have
+constexpr int kMaxCompact = 1024;  // passes up to this many slots may compact
 
-// grid (CTAs per unit, S/32/NS); unit y = set groups NS*y .. NS*y+NS-1.
-// Row adoption: a CTA whose own unit has no running set works, phase by
-// phase, for a unit that still has one (round-robin over the running units,
-// sharing its chunk claims) -- so the tail of the sweep, when a few straggler
-// sets keep iterating, runs on the whole GPU instead of on their own CTAs.
+// grid (CTAs per unit, S/32/NS); unit y = slots of set groups NS*y .. NS*y+NS-1.
+//
+// Straggler handling. Sets converge after different iteration counts (C5:
+// 23..32, most at 23), but a tile streams full 512-byte rows as long as ONE
+// of its 32 sets runs. Two mechanisms keep the tail short:
+//  - row adoption: a CTA whose own unit has no running set works, phase by
+//    phase, for a unit that still has one (round-robin, sharing its chunk
+//    claims), so the tail runs on the whole GPU;
+//  - compaction: when packing the running sets into the lowest slots at least
+//    halves the number of live tiles, every CTA copies its share of their
+//    state (ftov rows into the free vtof buffer, P0 and evidence into the
+//    alternate buffers), slot2set is rewritten and the buffers swap. Per-set
+//    control data is indexed by set, not slot, and res_pos records where each
+//    set's final marginals are.
 template <bool NORM, int NS>
 __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     sweep_ws(const __grid_constant__ SweepParams P) {
@@ -1038,14 +1075,24 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   WsShared<NS> &sh = *reinterpret_cast<WsShared<NS> *>(ws_smem);
   __shared__ unsigned umask[kMaxUnits][NS];  // running sets per unit, one bit per lane
   __shared__ int ulist[kMaxUnits];            // running units, ascending
-  __shared__ int s_nunits;
+  __shared__ int s_nunits, s_nrun;
+  __shared__ short n2o[kMaxCompact];          // compaction: new slot -> old slot
+  __shared__ int s2s_old[kMaxCompact];        // compaction: slot2set before it
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool producer = warp == kWsConsumers;
   const int units = gridDim.y;
+  const int S = P.S;
   const unsigned nblocks = gridDim.x * gridDim.y;
+  SwBufs B;
+  B.ftov = P.ftov;
+  B.vtof = P.vtof;
+  B.p0 = P.p0;
+  B.ev = const_cast<unsigned char *>(P.ev);
+  B.parity = 0;
   SwLane L[NS];
   bool alive[NS];
-  int sidx[NS];
+  int sidx[NS];  // slots
+  int sset[NS];  // their sets
   unsigned expected = 0, seq = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
@@ -1057,34 +1104,46 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   __syncthreads();
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
 
-  // Running sets of every unit (phase B: minus the decision taken at `done`),
-  // then this CTA's unit for the phase: its own while it has running sets,
-  // otherwise an adopted one. Returns the unit or -1 (nothing to do).
+  auto set_of = [&](int slot) -> int { return __ldcg(P.slot2set + slot); };
+  // Running slots of every unit (after_decision: minus the decision taken at
+  // `done`, which other CTAs cannot see through res_stop yet -- re-evaluated,
+  // same inputs, same answer); then this CTA's unit for the phase: its own
+  // while it has running sets, otherwise an adopted one; -1: nothing to do.
   auto pick_unit = [&](bool after_decision, int done) -> int {
     for (int r = warp; r < units; r += kWarps) {
 #pragma unroll
       for (int u = 0; u < NS; ++u) {
-        const int s = (r * NS + u) * 32 + lane;
-        bool run = s < P.nsets && ((const volatile int *)P.res_stop)[s] == 0;
-        if (run && after_decision) run = sw_decide(P, s, done) == 0;
+        const int set = set_of((r * NS + u) * 32 + lane);
+        bool run = set >= 0 && ((const volatile int *)P.res_stop)[set] == 0;
+        if (run && after_decision) run = sw_decide(P, set, done) == 0;
         const unsigned m = __ballot_sync(0xffffffffu, run);
         if (lane == 0) umask[r][u] = m;
       }
     }
     __syncthreads();
     if (warp == 0) {
-      int base = 0;
+      int base = 0, nrun = 0;
       for (int r0 = 0; r0 < units; r0 += 32) {
         const int r = r0 + lane;
         bool any = false;
+        int cnt = 0;
         if (r < units)
 #pragma unroll
-          for (int u = 0; u < NS; ++u) any |= umask[r][u] != 0;
+          for (int u = 0; u < NS; ++u) {
+            any |= umask[r][u] != 0;
+            cnt += __popc(umask[r][u]);
+          }
         const unsigned b = __ballot_sync(0xffffffffu, any);
         if (any) ulist[base + __popc(b & ((1u << lane) - 1))] = r;
         base += __popc(b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        nrun += cnt;
       }
-      if (lane == 0) s_nunits = base;
+      if (lane == 0) {
+        s_nunits = base;
+        s_nrun = nrun;
+      }
     }
     __syncthreads();
     const int n = s_nunits;
@@ -1100,7 +1159,8 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
       sidx[u] = (t * NS + u) * 32 + lane;
-      L[u] = sw_lane(P, sidx[u], P.E);
+      sset[u] = set_of(sidx[u]);
+      L[u] = sw_lane_b(B, sidx[u], sset[u], P.E, P.V);
       alive[u] = (umask[t][u] >> lane) & 1u;
     }
   };
@@ -1127,8 +1187,8 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         bind_unit(t);
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 0, P.vchunks, 0, P.n_vchunks, P.claim + (size_t)((2 * it) & 1) * units + t,
-                         true, it > 2, t * NS, seq);
+          ws_produce<NS>(P, B, sh, 0, P.vchunks, 0, P.n_vchunks,
+                         P.claim + (size_t)((2 * it) & 1) * units + t, true, it > 2, t * NS, seq);
         } else {
           ws_consume_var<NS, NORM>(P, sh, L, warp, it, !final_pass, alive, seq, dmax, uf);
         }
@@ -1142,30 +1202,32 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
             unsigned long long m = 0;
 #pragma unroll
             for (int w = 0; w < kWsConsumers; ++w) m = sh.red[w][u][lane] > m ? sh.red[w][u][lane] : m;
-            if (alive[u]) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + sidx[u]], m);
+            if (alive[u]) atomicMax(&P.dbits[(size_t)(it - 1) * S + sset[u]], m);
           }
         }
         if (!producer)
 #pragma unroll
           for (int u = 0; u < NS; ++u)
             if (alive[u] && uf[u])
-              atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]], (unsigned long long)(uf[u] - 1));
+              atomicMin(&P.ufkey[(size_t)it * S + sset[u]], (unsigned long long)(uf[u] - 1));
       }
       if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
         P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
       sw_grid_sync(P.bar, expected, nblocks);
       // stop decisions for iteration done = it - 1, recorded once per set by
-      // CTA x == 0 of the set's own unit
+      // CTA x == 0 of the unit holding the set's slot
       const int done = it - 1;
       if (blockIdx.x == 0 && warp == 0) {
 #pragma unroll
         for (int u = 0; u < NS; ++u) {
-          const int sh_s = (blockIdx.y * NS + u) * 32 + lane;
-          if (sh_s < P.nsets && ((const volatile int *)P.res_stop)[sh_s] == 0) {
-            const int stop = sw_decide(P, sh_s, done);
+          const int slot = (blockIdx.y * NS + u) * 32 + lane;
+          const int set = set_of(slot);
+          if (set >= 0 && ((const volatile int *)P.res_stop)[set] == 0) {
+            const int stop = sw_decide(P, set, done);
             if (stop) {
-              P.res_it[sh_s] = done;
-              P.res_stop[sh_s] = stop;
+              P.res_it[set] = done;
+              P.res_pos[set] = slot | (B.parity << 30);
+              P.res_stop[set] = stop;
               atomicAdd(P.nstop, 1u);
             }
           }
@@ -1177,8 +1239,6 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
 #pragma unroll
       for (int u = 0; u < NS; ++u) uf[u] = 0;
       reset_claims(2 * it + 1);
-      // the decision just taken is not visible through res_stop yet for other
-      // CTAs: pick_unit re-evaluates it (same inputs, same answer)
       const int t = pick_unit(it >= 2, it - 1);
       if (t >= 0) {
         bind_unit(t);
@@ -1187,7 +1247,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         const int c0 = first ? 0 : P.fchunk_nonunary;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, sh, 1, P.fchunks, c0, P.n_fchunks,
+          ws_produce<NS>(P, B, sh, 1, P.fchunks, c0, P.n_fchunks,
                          P.claim + (size_t)((2 * it + 1) & 1) * units + t, !first, false, t * NS,
                          seq);
         } else if (first) {
@@ -1199,12 +1259,77 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
 #pragma unroll
           for (int u = 0; u < NS; ++u)
             if (alive[u] && uf[u])
-              atomicMin(&P.ufkey[(size_t)it * P.S + sidx[u]],
+              atomicMin(&P.ufkey[(size_t)it * S + sset[u]],
                         (1ull << 32) | (unsigned long long)(uf[u] - 1));
       }
     }
     sw_grid_sync(P.bar, expected, nblocks);
-    if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
+    if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)S) return;
+
+    // ---- compaction (identical decision on every CTA; inputs final after the barrier)
+    if (P.compact && S <= kMaxCompact) {
+      // umask / s_nrun of the running sets at the end of iteration it
+      pick_unit(false, 0);
+      const int nrun = s_nrun, live = s_nunits;
+      const int need = (nrun + 32 * NS - 1) / (32 * NS);
+      if (nrun > 0 && 2 * need <= live) {
+        // n2o: running slots in ascending order; s2s_old: slot2set before
+        for (int i = threadIdx.x; i < S; i += blockDim.x) s2s_old[i] = set_of(i);
+        __syncthreads();
+        if (warp == 0) {
+          int base = 0;
+          for (int s0 = 0; s0 < S; s0 += 32) {
+            const int sl = s0 + lane;
+            const int r = sl / (32 * NS), u = (sl / 32) % NS;
+            const bool run = sl < S && ((umask[r][u] >> (sl & 31)) & 1u);
+            const unsigned b = __ballot_sync(0xffffffffu, run);
+            if (run) n2o[base + __popc(b & ((1u << lane) - 1))] = (short)sl;
+            base += __popc(b);
+          }
+        }
+        __syncthreads();
+        // everybody has read the old slot2set: it may now be rewritten
+        sw_grid_sync(P.bar, expected, nblocks);
+        const int R = nrun;
+        const int R32 = need * 32 * NS;
+        double *p0_new = B.parity ? P.p0 : P.p0_alt;
+        unsigned char *ev_new = B.parity ? const_cast<unsigned char *>(P.ev) : P.ev_alt;
+        // copy: ftov rows (E), P0 rows (V), evidence rows (V); k (new slot) fastest
+        const size_t tot_m = (size_t)P.E * R32, tot_v = (size_t)P.V * R32;
+        const size_t gtid = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+        const size_t gstride = (size_t)nblocks * blockDim.x;
+        for (size_t i = gtid; i < tot_m; i += gstride) {
+          const int k = (int)(i % R32);
+          const size_t row = i / R32;
+          if (k < R) {
+            const int o = n2o[k];
+            B.vtof[((size_t)(k >> 5) * P.E + row) * 32 + (k & 31)] =
+                B.ftov[((size_t)(o >> 5) * P.E + row) * 32 + (o & 31)];
+          }
+        }
+        for (size_t i = gtid; i < tot_v; i += gstride) {
+          const int k = (int)(i % R32);
+          const size_t row = i / R32;
+          if (k < R) {
+            const int o = n2o[k];
+            const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
+            const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
+            p0_new[dst] = B.p0[src];
+            ev_new[dst] = B.ev[src];
+          }
+        }
+        if (blockIdx.x == 0 && blockIdx.y == 0)
+          for (int k = threadIdx.x; k < S; k += blockDim.x)
+            P.slot2set[k] = k < R ? s2s_old[n2o[k]] : -1;
+        sw_grid_sync(P.bar, expected, nblocks);
+        double2 *nf = B.vtof;
+        B.vtof = B.ftov;
+        B.ftov = nf;
+        B.p0 = p0_new;
+        B.ev = ev_new;
+        B.parity ^= 1;
+      }
+    }
   }
 }
 
@@ -1227,7 +1352,16 @@ __global__ void sweep_evidence_kernel(unsigned char *ev, const int *vinv, const 
 
 // out[set][k][2] = (P0, 1 - P0) of original variable sel[k] (sel == null: k itself);
 // 32 x 32 tiles: coalesced reads along sets, coalesced writes along variables
-__global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const int *sel, int nsel,
+// res_pos[s] = slot | parity << 30: where set s's final marginals are (the
+// staged kernel may have moved the set; parity 1 = the alternate buffers)
+__device__ __forceinline__ size_t final_pos(const int *res_pos, int s, int vi, int V, int &parity) {
+  const int rp = res_pos[s];
+  parity = (rp >> 30) & 1;
+  return tile_pos(vi, rp & 0x3fffffff, V);
+}
+
+__global__ void sweep_marginals_kernel(const double *p0, const double *p0_alt, const int *res_pos,
+                                       const int *vinv, const int *sel, int nsel,
                                        int V, int nsets, int set_base, double *out_pair,
                                        double *out_p1) {
   __shared__ double tile[32][33];
@@ -1238,7 +1372,9 @@ __global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const 
     double v = 0.0;
     if (k < nsel && s < nsets) {
       const int var = sel ? sel[k] : k;
-      v = p0[tile_pos(vinv[var], s, V)];
+      int par;
+      const size_t at = final_pos(res_pos, s, vinv[var], V, par);
+      v = par ? p0_alt[at] : p0[at];
     }
     tile[r][tx] = v;
   }
@@ -1261,7 +1397,10 @@ __global__ void sweep_marginals_kernel(const double *p0, const int *vinv, const 
 // ties by ascending id. One CTA per set; bitonic sort of (~bits(P1), position)
 // in shared memory -- P1 >= 0, so its bit pattern orders like its value, and
 // positions index the id-sorted selection. Labeled = clamped in this set.
-__global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, const unsigned char *ev,
+__global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, const double *p0_alt,
+                                                           const unsigned char *ev,
+                                                           const unsigned char *ev_alt,
+                                                           const int *res_pos,
                                                            const int *vinv, const int *sel,
                                                            int nsel, int npow2, int V,
                                                            int set_base, int topk, int *ranked) {
@@ -1272,9 +1411,10 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, cons
   for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
     unsigned long long k = ~0ull;
     if (i < nsel) {
-      const size_t at = tile_pos(vinv[sel[i]], s, V);
-      if (ev[at] == 0) {
-        const double p1 = sub(1.0, p0[at]);
+      int par;
+      const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
+      if ((par ? ev_alt : ev)[at] == 0) {
+        const double p1 = sub(1.0, (par ? p0_alt : p0)[at]);
         k = ~(unsigned long long)__double_as_longlong(p1);
       }
     }
@@ -1326,8 +1466,8 @@ struct hbp_sweep {
   size_t smem = 0;
   bool ws = true;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
-  double *d_p0 = nullptr;
-  unsigned char *d_ev = nullptr;
+  double *d_p0 = nullptr, *d_p0_alt = nullptr;
+  unsigned char *d_ev = nullptr, *d_ev_alt = nullptr;
   void *d_ctrl = nullptr;
   size_t ctrl_bytes = 0;
   void *d_scratch = nullptr;  // evidence lists, selection, staging outputs
@@ -1336,6 +1476,7 @@ struct hbp_sweep {
   ~hbp_sweep() {
     cudaSetDevice(g->device);
     for (void *p : {(void *)d_vinv, (void *)d_vtof, (void *)d_ftov, (void *)d_p0, (void *)d_ev,
+                    (void *)d_p0_alt, (void *)d_ev_alt,
                     d_ctrl, d_scratch, (void *)d_vrow, (void *)d_frow, (void *)d_vtof_twin,
                     (void *)d_ftov_twin, (void *)d_vchunks, (void *)d_fchunks})
       if (p) cudaFree(p);
@@ -1471,6 +1612,10 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_p0, (size_t)std::max(1, L.V) * cap * sizeof(double)));
   HBP_CUDA(cudaMalloc(&sw->d_ev, (size_t)std::max(1, L.V) * cap + 4));
+  if (sw->ws && cap <= hbp::kMaxCompact) {  // compaction's alternate state buffers
+    HBP_CUDA(cudaMalloc(&sw->d_p0_alt, (size_t)std::max(1, L.V) * cap * sizeof(double)));
+    HBP_CUDA(cudaMalloc(&sw->d_ev_alt, (size_t)std::max(1, L.V) * cap + 4));
+  }
   HBP_CUDA(cudaEventCreate(&sw->e0));
   HBP_CUDA(cudaEventCreate(&sw->e1));
   HBP_CUDA(cudaEventCreate(&sw->k0));
@@ -1553,7 +1698,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   const size_t o_db = 0, o_uk = o_db + align256(nit * cap * 8), o_um = o_uk + align256(nit * cap * 8),
                o_tf = o_um + align256(nit * cap * 4), o_ri = o_tf + align256(nit * 4),
                o_rs = o_ri + align256((size_t)cap * 4), o_misc = o_rs + align256((size_t)cap * 4),
-               o_claim = o_misc + 256, ctrl_need = o_claim + align256((size_t)cap / 32 * 8 + 8);
+               o_claim = o_misc + 256, o_s2s = o_claim + align256((size_t)cap / 32 * 8 + 8),
+               o_rpos = o_s2s + align256((size_t)cap * 4), ctrl_need = o_rpos + align256((size_t)cap * 4);
   hbp_status s_;
   if ((s_ = ensure(&sw->d_ctrl, &sw->ctrl_bytes, ctrl_need))) return s_;
   char *cb = (char *)sw->d_ctrl;
@@ -1564,6 +1710,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   unsigned *d_nstop = (unsigned *)(cb + o_misc), *d_bar = d_nstop + 1;
   unsigned long long *d_t0 = (unsigned long long *)(cb + o_misc + 64);
   unsigned *d_claim = (unsigned *)(cb + o_claim);
+  int *d_s2s = (int *)(cb + o_s2s), *d_rpos = (int *)(cb + o_rpos);
   // scratch: evidence (set, var, val) for one pass, selection, output staging
   const bool marg_dev = out->marginals && out->marginals_on_device;
   const bool p1_dev = out->p1_select && out->p1_on_device;
@@ -1620,6 +1767,14 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.res_stop = d_rs;
   P.nstop = d_nstop;
   P.claim = d_claim;
+  P.p0_alt = sw->d_p0_alt;
+  P.ev_alt = sw->d_ev_alt;
+  P.slot2set = d_s2s;
+  P.res_pos = d_rpos;
+  {
+    const char *cenv = getenv("HBP_SWEEP_COMPACT");
+    P.compact = (sw->d_p0_alt && !(cenv && atoi(cenv) == 0)) ? 1 : 0;
+  }
   P.bar = d_bar;
   P.t0 = d_t0;
   P.max_it = max_it;
@@ -1667,6 +1822,14 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemsetAsync(d_tf, 0, nit * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_ri, 0, (size_t)S * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_claim, 0, (size_t)cap / 32 * 8 + 8, st));
+    {  // slot s holds set s (pass-relative); res_pos defaults to the same slot
+      std::vector<int> ident((size_t)S);
+      for (int i = 0; i < S; ++i) ident[i] = i < ns ? i : -1;
+      HBP_CUDA(cudaMemcpyAsync(d_s2s, ident.data(), (size_t)S * 4, cudaMemcpyHostToDevice, st));
+      for (int i = ns; i < S; ++i) ident[i] = i;
+      HBP_CUDA(cudaMemcpyAsync(d_rpos, ident.data(), (size_t)S * 4, cudaMemcpyHostToDevice, st));
+      HBP_CUDA(cudaStreamSynchronize(st));  // ident is a stack buffer
+    }
     HBP_CUDA(cudaMemsetAsync(d_rs, 0, (size_t)S * 4, st));
     const unsigned misc[2] = {(unsigned)(S - ns), 0u};
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
@@ -1689,7 +1852,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       double *dst = marg_dev ? out->marginals : stage_marg;
       const int bbase = marg_dev ? base : 0;
       hbp::sweep_marginals_kernel<<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
+          sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
       ++launches;
       if (!marg_dev)
         HBP_CUDA(cudaMemcpyAsync(out->marginals + (size_t)base * L.V * 2, stage_marg,
@@ -1699,7 +1862,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       double *dst = p1_dev ? out->p1_select : stage_p1;
       const int bbase = p1_dev ? base : 0;
       hbp::sweep_marginals_kernel<<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
+          sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
       ++launches;
       if (!p1_dev)
         HBP_CUDA(cudaMemcpyAsync(out->p1_select + (size_t)base * nsel, stage_p1,
@@ -1712,7 +1875,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       if (smem > 48 * 1024)
         HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      hbp::sweep_rank_kernel<<<ns, 1024, smem, st>>>(sw->d_p0, sw->d_ev, sw->d_vinv, d_sel, nsel,
+      hbp::sweep_rank_kernel<<<ns, 1024, smem, st>>>(sw->d_p0, sw->d_p0_alt, sw->d_ev, sw->d_ev_alt,
+                                                     d_rpos, sw->d_vinv, d_sel, nsel,
                                                      std::max(npow2, 2), L.V, bbase, out->topk, dst);
       ++launches;
       if (!rk_dev)
