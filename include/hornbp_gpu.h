@@ -225,6 +225,7 @@ typedef struct {
   double wall_ms;
   int32_t launches;
   int32_t passes;
+  int32_t compactions;           /* straggler compactions performed (staged kernel)      */
 } hbp_sweep_outputs;
 
 /* max_sets_per_pass: 0 = as many as fit in half of the free device memory. */

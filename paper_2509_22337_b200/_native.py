@@ -106,6 +106,7 @@ class SweepOutputs(C.Structure):
         ("wall_ms", C.c_double),
         ("launches", C.c_int32),
         ("passes", C.c_int32),
+        ("compactions", C.c_int32),
     ]
 
 

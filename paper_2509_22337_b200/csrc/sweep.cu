@@ -87,6 +87,7 @@ struct SweepParams {
   int *slot2set;              // [S]
   int *res_pos;               // [S] per set: slot | buffer parity << 30 of its final P0
   int compact;                // 1: pack the running sets when that halves the live tiles
+  int debug;                  // HBP_SWEEP_DEBUG=1: device printf of tail events
   unsigned *bar;              // grid barrier arrivals
   unsigned long long *t0;
   int max_it, normalize;
@@ -922,7 +923,7 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B
 template <int NS, bool NORM, bool FIRST>
 __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS> &sh,
                                                const SwLane *L, int cw, const bool *alive,
-                                               unsigned &seq, unsigned *uf) {
+                                               unsigned &seq, unsigned *uf, bool unary = false) {
   const int lane = threadIdx.x & 31;
   bool any = false;
 #pragma unroll
@@ -945,7 +946,8 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
       for (int f = n0 + start; f < n1; f += WsCfg<NS>::consumers) {
         const int r = ch.rp[f - rp_lo];
         const int d = ch.rp[f + 1 - rp_lo] - r;
-        if (!FIRST && d == 1) continue;  // unary: constant message, written in iteration 1
+        // unary: a constant message, written in iteration 1 (and again after a compaction)
+        if (!FIRST && !unary && d == 1) continue;
         const double2 pp = ch.fpar[f - n0];
         const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
         if (ch.heavy) {
@@ -1171,7 +1173,78 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     if (blockIdx.x == 0 && threadIdx.x == 0) P.claim[((q + 1) & 1) * units + blockIdx.y] = 0;
   };
 
+  // ---- compaction, at most once per pass, right after a stop decision: the
+  // running sets move to the lowest slots (vtof rows of the current iteration
+  // into the ftov buffer, P0 and evidence into the alternate buffers), the
+  // buffers swap roles, and the following factor phase rewrites the unary
+  // factors' constant messages (the new ftov buffer does not hold them).
+  // Inputs: umask / s_nrun / s_nunits from pick_unit(true, done).
+  bool compacted = false;
+  auto maybe_compact = [&](int it) -> bool {
+    if (!P.compact || compacted || S > kMaxCompact) return false;
+    const int nrun = s_nrun, live = s_nunits;
+    const int need = (nrun + 32 * NS - 1) / (32 * NS);
+    if (P.debug && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+      printf("it %d: running %d sets in %d units (packed: %d)\n", it, nrun, live, need);
+    if (!(nrun > 0 && 2 * need <= live)) return false;
+    // n2o: running slots in ascending order; s2s_old: slot2set before
+    for (int i = threadIdx.x; i < S; i += blockDim.x) s2s_old[i] = set_of(i);
+    __syncthreads();
+    if (warp == 0) {
+      int base = 0;
+      for (int s0 = 0; s0 < S; s0 += 32) {
+        const int sl = s0 + lane;
+        const int r = sl / (32 * NS), u = (sl / 32) % NS;
+        const bool run = sl < S && ((umask[r][u] >> (sl & 31)) & 1u);
+        const unsigned b = __ballot_sync(0xffffffffu, run);
+        if (run) n2o[base + __popc(b & ((1u << lane) - 1))] = (short)sl;
+        base += __popc(b);
+      }
+    }
+    __syncthreads();
+    // every CTA has read the old slot2set: it may now be rewritten
+    sw_grid_sync(P.bar, expected, nblocks);
+    const int R = nrun;
+    const int R32 = need * 32 * NS;
+    const size_t tot_m = (size_t)P.E * R32, tot_v = (size_t)P.V * R32;
+    const size_t gtid = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t gstride = (size_t)nblocks * blockDim.x;
+    for (size_t i = gtid; i < tot_m; i += gstride) {
+      const int k = (int)(i % R32);
+      const size_t row = i / R32;
+      if (k < R) {
+        const int o = n2o[k];
+        B.ftov[((size_t)(k >> 5) * P.E + row) * 32 + (k & 31)] =
+            B.vtof[((size_t)(o >> 5) * P.E + row) * 32 + (o & 31)];
+      }
+    }
+    for (size_t i = gtid; i < tot_v; i += gstride) {
+      const int k = (int)(i % R32);
+      const size_t row = i / R32;
+      if (k < R) {
+        const int o = n2o[k];
+        const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
+        const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
+        P.p0_alt[dst] = B.p0[src];
+        P.ev_alt[dst] = B.ev[src];
+      }
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+      for (int k = threadIdx.x; k < S; k += blockDim.x) P.slot2set[k] = k < R ? s2s_old[n2o[k]] : -1;
+    sw_grid_sync(P.bar, expected, nblocks);
+    double2 *nv = B.ftov;  // holds the packed vtof rows
+    B.ftov = B.vtof;
+    B.vtof = nv;
+    B.p0 = P.p0_alt;
+    B.ev = P.ev_alt;
+    B.parity = 1;
+    compacted = true;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(P.nstop + 2, 1u);
+    return true;
+  };
+
   for (int it = 1;; ++it) {
+    bool rewrite_unary = false;
     if (it >= 2) {
       const bool final_pass = it == P.max_it + 1;
       unsigned long long dmax[NS];
@@ -1233,6 +1306,10 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
           }
         }
       }
+      if (P.compact && !compacted && !final_pass) {
+        pick_unit(true, done);
+        rewrite_unary = maybe_compact(it);
+      }
     }
     {
       unsigned uf[NS];  // last underflowing ftov slot + 1 per set
@@ -1243,8 +1320,9 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
       if (t >= 0) {
         bind_unit(t);
         const bool first = it == 1;
-        // after iteration 1 the unary factors' chunks are skipped (constant messages)
-        const int c0 = first ? 0 : P.fchunk_nonunary;
+        // after iteration 1 the unary factors' chunks are skipped (constant
+        // messages) -- except right after a compaction, which left them behind
+        const int c0 = (first || rewrite_unary) ? 0 : P.fchunk_nonunary;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           ws_produce<NS>(P, B, sh, 1, P.fchunks, c0, P.n_fchunks,
@@ -1253,7 +1331,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         } else if (first) {
           ws_consume_fac<NS, NORM, true>(P, sh, L, warp, alive, seq, uf);
         } else {
-          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, alive, seq, uf);
+          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, alive, seq, uf, rewrite_unary);
         }
         if (!producer)
 #pragma unroll
@@ -1266,70 +1344,6 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     sw_grid_sync(P.bar, expected, nblocks);
     if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)S) return;
 
-    // ---- compaction (identical decision on every CTA; inputs final after the barrier)
-    if (P.compact && S <= kMaxCompact) {
-      // umask / s_nrun of the running sets at the end of iteration it
-      pick_unit(false, 0);
-      const int nrun = s_nrun, live = s_nunits;
-      const int need = (nrun + 32 * NS - 1) / (32 * NS);
-      if (nrun > 0 && 2 * need <= live) {
-        // n2o: running slots in ascending order; s2s_old: slot2set before
-        for (int i = threadIdx.x; i < S; i += blockDim.x) s2s_old[i] = set_of(i);
-        __syncthreads();
-        if (warp == 0) {
-          int base = 0;
-          for (int s0 = 0; s0 < S; s0 += 32) {
-            const int sl = s0 + lane;
-            const int r = sl / (32 * NS), u = (sl / 32) % NS;
-            const bool run = sl < S && ((umask[r][u] >> (sl & 31)) & 1u);
-            const unsigned b = __ballot_sync(0xffffffffu, run);
-            if (run) n2o[base + __popc(b & ((1u << lane) - 1))] = (short)sl;
-            base += __popc(b);
-          }
-        }
-        __syncthreads();
-        // everybody has read the old slot2set: it may now be rewritten
-        sw_grid_sync(P.bar, expected, nblocks);
-        const int R = nrun;
-        const int R32 = need * 32 * NS;
-        double *p0_new = B.parity ? P.p0 : P.p0_alt;
-        unsigned char *ev_new = B.parity ? const_cast<unsigned char *>(P.ev) : P.ev_alt;
-        // copy: ftov rows (E), P0 rows (V), evidence rows (V); k (new slot) fastest
-        const size_t tot_m = (size_t)P.E * R32, tot_v = (size_t)P.V * R32;
-        const size_t gtid = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-        const size_t gstride = (size_t)nblocks * blockDim.x;
-        for (size_t i = gtid; i < tot_m; i += gstride) {
-          const int k = (int)(i % R32);
-          const size_t row = i / R32;
-          if (k < R) {
-            const int o = n2o[k];
-            B.vtof[((size_t)(k >> 5) * P.E + row) * 32 + (k & 31)] =
-                B.ftov[((size_t)(o >> 5) * P.E + row) * 32 + (o & 31)];
-          }
-        }
-        for (size_t i = gtid; i < tot_v; i += gstride) {
-          const int k = (int)(i % R32);
-          const size_t row = i / R32;
-          if (k < R) {
-            const int o = n2o[k];
-            const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
-            const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
-            p0_new[dst] = B.p0[src];
-            ev_new[dst] = B.ev[src];
-          }
-        }
-        if (blockIdx.x == 0 && blockIdx.y == 0)
-          for (int k = threadIdx.x; k < S; k += blockDim.x)
-            P.slot2set[k] = k < R ? s2s_old[n2o[k]] : -1;
-        sw_grid_sync(P.bar, expected, nblocks);
-        double2 *nf = B.vtof;
-        B.vtof = B.ftov;
-        B.ftov = nf;
-        B.p0 = p0_new;
-        B.ev = ev_new;
-        B.parity ^= 1;
-      }
-    }
   }
 }
 
@@ -1467,6 +1481,7 @@ struct hbp_sweep {
   bool ws = true;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
   double *d_p0 = nullptr, *d_p0_alt = nullptr;
+  int compact_cap = 0;  // slots the alternate buffers hold
   unsigned char *d_ev = nullptr, *d_ev_alt = nullptr;
   void *d_ctrl = nullptr;
   size_t ctrl_bytes = 0;
@@ -1612,9 +1627,10 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_p0, (size_t)std::max(1, L.V) * cap * sizeof(double)));
   HBP_CUDA(cudaMalloc(&sw->d_ev, (size_t)std::max(1, L.V) * cap + 4));
-  if (sw->ws && cap <= hbp::kMaxCompact) {  // compaction's alternate state buffers
-    HBP_CUDA(cudaMalloc(&sw->d_p0_alt, (size_t)std::max(1, L.V) * cap * sizeof(double)));
-    HBP_CUDA(cudaMalloc(&sw->d_ev_alt, (size_t)std::max(1, L.V) * cap + 4));
+  if (sw->ws) {  // compaction's alternate state buffers (passes of <= kMaxCompact slots)
+    sw->compact_cap = std::min(cap, hbp::kMaxCompact);
+    HBP_CUDA(cudaMalloc(&sw->d_p0_alt, (size_t)std::max(1, L.V) * sw->compact_cap * sizeof(double)));
+    HBP_CUDA(cudaMalloc(&sw->d_ev_alt, (size_t)std::max(1, L.V) * sw->compact_cap + 4));
   }
   HBP_CUDA(cudaEventCreate(&sw->e0));
   HBP_CUDA(cudaEventCreate(&sw->e1));
@@ -1707,7 +1723,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   unsigned long long *d_uk = (unsigned long long *)(cb + o_uk);
   int *d_um = (int *)(cb + o_um), *d_tf = (int *)(cb + o_tf), *d_ri = (int *)(cb + o_ri),
       *d_rs = (int *)(cb + o_rs);
-  unsigned *d_nstop = (unsigned *)(cb + o_misc), *d_bar = d_nstop + 1;
+  unsigned *d_nstop = (unsigned *)(cb + o_misc), *d_bar = d_nstop + 1;  // d_nstop[2]: compactions
   unsigned long long *d_t0 = (unsigned long long *)(cb + o_misc + 64);
   unsigned *d_claim = (unsigned *)(cb + o_claim);
   int *d_s2s = (int *)(cb + o_s2s), *d_rpos = (int *)(cb + o_rpos);
@@ -1773,8 +1789,10 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.res_pos = d_rpos;
   {
     const char *cenv = getenv("HBP_SWEEP_COMPACT");
-    P.compact = (sw->d_p0_alt && !(cenv && atoi(cenv) == 0)) ? 1 : 0;
+    P.compact = (sw->d_p0_alt && !(cenv && atoi(cenv) == 0)) ? 1 : 0;  // per pass: S <= compact_cap
+    P.debug = getenv("HBP_SWEEP_DEBUG") ? 1 : 0;
   }
+  const int compact_enabled = P.compact;
   P.bar = d_bar;
   P.t0 = d_t0;
   P.max_it = max_it;
@@ -1787,7 +1805,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   std::vector<int> h_ev_set, h_ev_var;
   std::vector<signed char> h_ev_val;
   int64_t launches = 0;
-  int passes = 0;
+  int passes = 0, compactions = 0;
   double dev_ms = 0, ker_ms = 0;
   for (int base = 0; base < n; base += cap) {
     const int ns = std::min(cap, n - base);
@@ -1797,6 +1815,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     const int nx = std::max(1, std::min(sw->grid_x_max / groups, (L.F + hbp::kSwWarps - 1) / hbp::kSwWarps));
     P.S = S;
     P.nsets = ns;
+    P.compact = compact_enabled && S <= sw->compact_cap;
     // evidence table of this pass
     const int64_t e_lo = ev->offsets[base], e_hi = ev->offsets[base + ns];
     const int64_t ne = e_hi - e_lo;
@@ -1831,8 +1850,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       HBP_CUDA(cudaStreamSynchronize(st));  // ident is a stack buffer
     }
     HBP_CUDA(cudaMemsetAsync(d_rs, 0, (size_t)S * 4, st));
-    const unsigned misc[2] = {(unsigned)(S - ns), 0u};
-    HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 8, cudaMemcpyHostToDevice, st));
+    const unsigned misc[3] = {(unsigned)(S - ns), 0u, 0u};
+    HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 12, cudaMemcpyHostToDevice, st));
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
     if (sw->ws) {
@@ -1893,6 +1912,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     h_rs.resize(S);
     HBP_CUDA(cudaMemcpyAsync(h_ri.data(), d_ri, (size_t)S * 4, cudaMemcpyDeviceToHost, st));
     HBP_CUDA(cudaMemcpyAsync(h_rs.data(), d_rs, (size_t)S * 4, cudaMemcpyDeviceToHost, st));
+    unsigned h_misc[3] = {0, 0, 0};
+    HBP_CUDA(cudaMemcpyAsync(h_misc, d_nstop, 12, cudaMemcpyDeviceToHost, st));
     HBP_CUDA(cudaStreamSynchronize(st));
     {
       float a = 0, b = 0;
@@ -1901,6 +1922,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       dev_ms += a;
       ker_ms += b;
     }
+    compactions += (int)h_misc[2];
     int maxit_seen = 0;
     for (int j = 0; j < ns; ++j) maxit_seen = std::max(maxit_seen, h_ri[j]);
     const size_t rows = (size_t)maxit_seen + 2;
@@ -1939,6 +1961,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   out->launches = (int32_t)launches;
   out->passes = passes;
+  out->compactions = compactions;
   hbp::set_last_launches(launches);
   return HBP_OK;
 }

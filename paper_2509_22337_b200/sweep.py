@@ -49,6 +49,7 @@ class SweepResult:
     kernel_ms: Optional[float] = None      # persistent sweep kernel(s) only
     launches: int = 0
     passes: int = 0
+    compactions: int = 0                   # straggler compactions (staged kernel)
 
     def __len__(self) -> int:
         return len(self.iterations)
@@ -199,7 +200,8 @@ def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Str
         marginals=mg, p1_select=p1, ranked=rk, select=sel, errors=errors,
         updates_per_iteration=base_upd + np.diff(off),
         device_ms=float(outs.device_ms), kernel_ms=float(outs.kernel_ms),
-        launches=int(outs.launches), passes=int(outs.passes))
+        launches=int(outs.launches), passes=int(outs.passes),
+        compactions=int(outs.compactions))
 
 
 def _run_materialised(graph, off, var, val, strategy, options, want_marg, want_deltas, sel, topk):

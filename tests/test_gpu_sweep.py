@@ -163,3 +163,40 @@ def test_sweep_long_rows_heavy_chunks():
     opts = EngineOptions(max_iterations=80, tolerance=1e-12)
     res = P.run_many(g, sets, None, opts)
     check_against_oracle(g, sets, opts, res)
+
+
+@pytest.mark.parametrize("name,n", [("weblech", 300), ("hedc", 160)])
+def test_sweep_compaction_every_set_bitwise(name, n):
+    """Many sets with spread-out convergence: the staged kernel packs the
+    stragglers into fewer tiles mid-run (compaction) -- every set, stopped
+    before or after it, must still equal the oracle bit for bit."""
+    g, alarms = W.graph(name)
+    rng = np.random.default_rng(2025)
+    ids = np.asarray(alarms.alarms)
+    labels = np.asarray(alarms.labels)
+    sets = []
+    for j in range(n):
+        k = int(rng.integers(0, min(10, len(ids)) + 1))
+        pick = rng.choice(len(ids), k, replace=False)
+        sets.append(list(zip(ids[pick].tolist(), labels[pick].tolist())))
+    opts = EngineOptions(1000, 1e-9)
+    sel = np.sort(ids)
+    res = P.run_many(g, sets, None, opts, select=sel, topk=min(20, len(sel)))
+    assert res.compactions >= 1, "the test graph must trigger a compaction"
+    check_against_oracle(g, sets, opts, res)
+    for j, pairs in enumerate(sets):
+        assert res.p1_select[j].tobytes() == res.marginals[j][sel, 1].tobytes()
+        want = rank_alarms(res.marginals[j], alarms, [v for v, _ in pairs])[:min(20, len(sel))]
+        assert res.ranked[j][:len(want)].tolist() == want, j
+
+
+def test_sweep_ftp_many_sets_vs_oracle():
+    """48 C5-style ftp sets (PARALL, tol 1e-9), every set against the oracle."""
+    g, alarms = W.graph("ftp")
+    sets = [W.evidence_set(alarms, j) for j in range(100, 148)]
+    opts = EngineOptions(1000, 1e-9)
+    res = P.run_many(g, sets, None, opts)
+    for j, (ids, labels) in enumerate(sets):
+        o, _ = oracle_set(g, list(zip(ids.tolist(), labels.tolist())), opts)
+        assert res.iterations[j] == o["iterations"], j
+        assert res.marginals[j].tobytes() == o["marginals"].tobytes(), j
