@@ -551,8 +551,11 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     // whole light nodes [begin, end), then the slots of the heavy nodes
     // [sbegin, send); grid-strided so a warp's 32 items are neighbouring rows
     // (coalesced row loads, uniform degree).
+    // the heavy nodes' slot items come first (longest work first: the
+    // phase's tail is made of cheap light nodes, which balances the warps)
     const int nn = ph.end - ph.begin;
-    const int total = nn + (ph.send - ph.sbegin);
+    const int hn = ph.send - ph.sbegin;
+    const int total = nn + hn;
     // warp chunks of 32 consecutive items (coalesced rows, uniform degree)
     // dealt round-robin over CTAs, so every SM gets the same degree mix
     // (heavy rows sit at the end of the degree-sorted order)
@@ -571,10 +574,11 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
         for (int c = c0; c * 32 < total; c += cstride) {
           const int i = c * 32 + lane;
           if (i >= total) break;
-          if (i < nn) {
-            vnode(P, ph.begin + i, marg, do_vtof, it, pidx, dmax, ufkey, it == 1 && pidx == 0);
+          if (i >= hn) {
+            vnode(P, ph.begin + (i - hn), marg, do_vtof, it, pidx, dmax, ufkey,
+                  it == 1 && pidx == 0);
           } else {
-            const int q = ph.sbegin + (i - nn);
+            const int q = ph.sbegin + i;
             v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
                    pidx, dmax, ufkey, it == 1 && pidx == 0);
           }
@@ -583,10 +587,10 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
       for (int c = c0; c * 32 < total; c += cstride) {
         const int i = c * 32 + lane;
         if (i >= total) break;
-        if (i < nn) {
-          fnode(P, ph.begin + i, pidx, it == 1, ufkey);
+        if (i >= hn) {
+          fnode(P, ph.begin + (i - hn), pidx, it == 1, ufkey);
         } else {
-          const int p = ph.sbegin + (i - nn);
+          const int p = ph.sbegin + i;
           f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
         }
       }
@@ -751,21 +755,28 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
     // loads overlap phase 1; a stop then only wastes a factor-side phase
     // whose output (ftov) is never observed.
     __shared__ int s_stop;
-    int stop = 0;  // thread 0
     const int done = it - 1;
+    // the decision inputs are loaded now and evaluated where the decision is
+    // applied: in the deferred (PARALL) case warp 0 does not wait on them
+    // before its share of the factor phase
+    int ufm = 0, ufg = 0, tf = 0;
+    unsigned long long db = 0;
     if (it > 1 && threadIdx.x == 0) {
-      const int ufm = ((const volatile int *)P.uf_msg)[done];
-      const int ufg = ((const volatile int *)P.uf_marg)[done];
-      const int tf = ((const volatile int *)P.tflag)[done];
-      const unsigned long long db = ((const volatile unsigned long long *)P.delta_bits)[done];
-      if (ufm || ufg) stop = 4;
-      else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
-      else if (done == P.max_it) stop = 2;
-      else if (tf) stop = 3;
+      ufm = ((const volatile int *)P.uf_msg)[done];
+      ufg = ((const volatile int *)P.uf_marg)[done];
+      tf = ((const volatile int *)P.tflag)[done];
+      db = ((const volatile unsigned long long *)P.delta_bits)[done];
     }
+    auto decide = [&]() -> int {
+      if (ufm || ufg) return 4;
+      if (__longlong_as_double((long long)db) < P.tol) return 1;
+      if (done == P.max_it) return 2;
+      if (tf) return 3;
+      return 0;
+    };
     const bool defer = P.nphases == 2 && !final_pass;
     if (it > 1 && !defer) {
-      if (threadIdx.x == 0) s_stop = stop;
+      if (threadIdx.x == 0) s_stop = decide();
       __syncthreads();
       if (s_stop) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -812,7 +823,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       }
     }
     if (it > 1 && defer) {
-      if (threadIdx.x == 0) s_stop = stop;
+      if (threadIdx.x == 0) s_stop = decide();
       __syncthreads();
       if (s_stop) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
