@@ -162,29 +162,31 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   classes(L.frow, 0, L.f_or_light, L.fa_node, L.fa_row);
   classes(L.frow, L.f_or_light, L.f_heavy, L.fo_node, L.fo_row);
 
+  // the reference's own ftov order: variables by id, rows in canonical order
+  // (a stable counting sort, storage.py:61)
+  L.ref_ftov.resize(E);
+  std::vector<int64_t> vstart((size_t)V + 1, 0);
+  {
+    for (int64_t e = 0; e < E; ++e) vstart[(size_t)L.edge_var[e] + 1]++;
+    for (int32_t v = 0; v < V; ++v) vstart[v + 1] += vstart[v];
+    std::vector<int64_t> fill(vstart.begin(), vstart.end() - 1);
+    for (int64_t e = 0; e < E; ++e) L.ref_ftov[(size_t)fill[L.edge_var[e]]++] = (int32_t)e;
+  }
   // ftov rows: canonical order within each variable == (factor, slot) order,
-  // which is the reference's product order (storage.py:59-61)
+  // which is the reference's product order (storage.py:59-61): variable v's
+  // reference row, placed at its internal row
   L.canon2f.resize(E);
   L.vslot.resize(2 * E);
-  {
-    std::vector<int32_t> fill((size_t)V, 0);
-    for (int64_t e = 0; e < E; ++e) {
-      const int32_t v = L.edge_var[e];
-      const int32_t vi = L.vinv[v];
-      const int32_t j = fill[v]++;
+  for (int32_t v = 0; v < V; ++v) {
+    const int32_t vi = L.vinv[v];
+    const int32_t d = (int32_t)(vstart[v + 1] - vstart[v]);
+    for (int32_t j = 0; j < d; ++j) {
+      const int32_t e = L.ref_ftov[(size_t)vstart[v] + j];
       const int32_t q = L.vrow[vi] + j;
       L.canon2f[e] = q;
       L.vslot[2 * (size_t)q] = vi;
-      L.vslot[2 * (size_t)q + 1] = (vdeg[v] << 16) | j;
+      L.vslot[2 * (size_t)q + 1] = (d << 16) | j;
     }
-  }
-  // the reference's own ftov order: variables by id, rows in canonical order
-  L.ref_ftov.resize(E);
-  {
-    std::vector<int64_t> start((size_t)V + 1, 0);
-    for (int64_t e = 0; e < E; ++e) start[(size_t)L.edge_var[e] + 1]++;
-    for (int32_t v = 0; v < V; ++v) start[v + 1] += start[v];
-    for (int64_t e = 0; e < E; ++e) L.ref_ftov[(size_t)start[L.edge_var[e]]++] = (int32_t)e;
   }
   L.vtof2canon.resize(E);
   L.ftov2canon.resize(E);
@@ -194,8 +196,8 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     L.vtof2canon[L.canon2v[e]] = (int32_t)e;
     L.ftov2canon[L.canon2f[e]] = (int32_t)e;
     L.vtof_twin[L.canon2v[e]] = L.canon2f[e];
-    int32_t f = L.edge_factor[e];
-    bool unary = L.rowptr[f + 1] - L.rowptr[f] == 1;
+    const int32_t f = L.edge_factor[e];
+    const bool unary = L.rowptr[f + 1] - L.rowptr[f] == 1;
     L.ftov_twin[L.canon2f[e]] = (uint32_t)L.canon2v[e] | (unary ? kUnaryBit : 0u);
   }
   return HBP_OK;
@@ -244,6 +246,46 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
     P.max_items = std::max(P.max_items, n);
     P.phases.push_back(ph);
   };
+
+  // PARALL fast path: one batch holding every edge once and every slot of a
+  // non-unary factor once compiles to the two whole-graph phases directly
+  if (k == 1 && ns == E && nt == nonunary_total) {
+    std::vector<uint8_t> seen((size_t)E, 0);
+    bool ok = true;
+    for (int64_t i = 0; i < ns && ok; ++i) {
+      uint8_t &m = seen[s_edges[i]];
+      ok = !(m & 1);
+      m |= 1;
+    }
+    for (int64_t i = 0; i < nt && ok; ++i) {
+      const int32_t e = t_edges[i];
+      const int32_t f = L.edge_factor[e];
+      uint8_t &m = seen[e];
+      ok = !(m & 2) && L.rowptr[f + 1] - L.rowptr[f] > 1;
+      m |= 2;
+    }
+    if (ok) {
+      Phase v{};
+      v.type = 0;
+      v.list = 2;
+      v.marg = 1;
+      v.begin = 0;
+      v.end = L.v_heavy;
+      v.sbegin = L.vrow[L.v_heavy];
+      v.send = (int32_t)E;
+      push_phase(v, L.v_heavy + (v.send - v.sbegin));
+      P.phases.back().grid = 1;  // phase 0 carries the convergence test
+      Phase f{};
+      f.type = 1;
+      f.list = 2;
+      f.begin = 0;
+      f.end = L.f_heavy;
+      f.sbegin = L.frow[L.f_heavy];
+      f.send = (int32_t)E;
+      push_phase(f, L.f_heavy + (f.send - f.sbegin));
+      return HBP_OK;
+    }
+  }
 
   const int64_t levels = std::max<int64_t>(k, 1);
   for (int64_t b = 0; b < levels; ++b) {
