@@ -121,6 +121,8 @@ typedef struct {
   int32_t evidence_count;     /* clamp factors appended to the graph (info) */
   double tolerance;           /* >= 0; converged iff delta < tolerance     */
   double time_limit;          /* seconds; <= 0 means none                  */
+  int32_t precision;          /* 0: fp64, bitwise with the reference (default); 1: fp32
+                                 messages (hbp_sweep_run only; marginals within 1e-5)   */
 } hbp_options;
 
 typedef struct {

@@ -52,6 +52,7 @@ class Options(C.Structure):
         ("evidence_count", C.c_int32),
         ("tolerance", C.c_double),
         ("time_limit", C.c_double),
+        ("precision", C.c_int32),
     ]
 
 

@@ -1251,6 +1251,10 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
     hbp::set_error("tolerance must be nonnegative");
     return HBP_EINVAL;
   }
+  if (opt->precision != 0) {
+    hbp::set_error("the single-graph executor runs fp64 only (fp32 mode: hbp_sweep_run)");
+    return HBP_EINVAL;
+  }
   HBP_CUDA(cudaSetDevice(g->device));
   const size_t n = (size_t)opt->max_iterations + 2;
   hbp_status st = ensure_ctrl(g, n);

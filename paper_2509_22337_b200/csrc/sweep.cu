@@ -506,6 +506,70 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
   }
 }
 
+// ---- precision-generic lane view and helpers of the staged kernel ---------------------------
+
+template <typename T>
+struct SwLaneT {
+  typename Ar<T>::T2 *vtof, *ftov;  // &X[g][0][lane]
+  T *p0;
+  const unsigned char *ev;
+  int s;                            // the set (control arrays are indexed by set)
+};
+
+template <typename T>
+struct SwBufsT {
+  typename Ar<T>::T2 *ftov, *vtof;
+  T *p0;
+  unsigned char *ev;
+  int parity;  // 0: the pass's original p0 / ev buffers, 1: the alternates
+};
+
+template <typename T>
+__device__ __forceinline__ SwLaneT<T> sw_lane_bt(const SwBufsT<T> &B, int slot, int set, int E,
+                                                 int V) {
+  const int g = slot >> 5, lane = slot & 31;
+  SwLaneT<T> L;
+  L.vtof = B.vtof + (size_t)g * E * 32 + lane;
+  L.ftov = B.ftov + (size_t)g * E * 32 + lane;
+  L.p0 = B.p0 + (size_t)g * V * 32 + lane;
+  L.ev = B.ev + (size_t)g * V * 32 + lane;
+  L.s = set;
+  return L;
+}
+
+template <typename T>
+__device__ __forceinline__ void sw_clamp_t(unsigned code, T &a0, T &a1) {
+  using A = Ar<T>;
+  if (code & 1u) {  // observed false: (1, 0)
+    a0 = A::mul(a0, T(1));
+    a1 = A::mul(a1, T(0));
+  }
+  if (code & 2u) {  // observed true: (0, 1)
+    a0 = A::mul(a0, T(0));
+    a1 = A::mul(a1, T(1));
+  }
+}
+
+// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572);
+// for T = double exactly sw_marginal; |dP1| is widened (exactly) to double bits
+template <typename T>
+__device__ __forceinline__ void sw_marginal_t(const SweepParams &P, const SwLaneT<T> &L, int v,
+                                             int it, T q0, T q1, T prev_p0,
+                                             unsigned long long &dmax) {
+  using A = Ar<T>;
+  const T t = A::add(q0, q1);
+  if (t < A::min_sum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], P.vorig[v]);
+  const T p0 = A::div(q0, t);
+  const T p1 = A::sub(T(1), p0);
+  const T prev = it == 2 ? T(0.5) : A::sub(T(1), prev_p0);  // prev P1 starts at 0.5
+  const double diff = (double)A::sub(p1, prev);
+  const unsigned long long raw = (unsigned long long)__double_as_longlong(diff);
+  unsigned long long bits;
+  asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
+  dmax = bits > dmax ? bits : dmax;
+  L.p0[v * 32] = p0;
+}
+
 // ---- TMA-staged, warp-specialised sweep kernel (default) ------------------------------------
 // The persistent kernel above issues a node's loads and then computes, so a
 // warp has no memory in flight while it multiplies: HBM-latency bound at
@@ -551,10 +615,11 @@ constexpr int kChN = 16;   // nodes per chunk
 constexpr int kRing = HBP_WS_RING;  // chunks in flight per CTA
 constexpr int kPad = 8;    // index arrays are padded so aligned windows stay in bounds
 
-template <int NS>
+template <int NS, typename T>
 struct __align__(16) WsChunk {
-  double2 msg[NS][kChR][32];      // message rows of the chunk, one 512-byte row per slot and group
-  double p0[NS][kChN][32];        // variable side: P0 of the previous iteration per node
+  using T2 = typename Ar<T>::T2;
+  T2 msg[NS][kChR][32];           // message rows of the chunk, one row (32 lanes) per slot and group
+  T p0[NS][kChN][32];             // variable side: P0 of the previous iteration per node
   unsigned char ev[NS][kChN][32]; // variable side: evidence codes per node
   double2 fpar[kChN];             // factor side: (p1, p2) per node
   int rp[kChN + 8];               // row pointers, aligned window from (n0 & ~3)
@@ -562,9 +627,9 @@ struct __align__(16) WsChunk {
   int n0, n1, r0, heavy;          // header written by the producer before arming
 };
 
-template <int NS>
+template <int NS, typename T>
 struct WsShared {
-  WsChunk<NS> ring[kRing];
+  WsChunk<NS, T> ring[kRing];
   unsigned long long full[kRing], empty[kRing];
   unsigned long long red[WsCfg<NS>::consumers][NS][32];
 };
@@ -602,113 +667,121 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 // Variable node of degree D for NS sets (set u: rows x[u][k*32], lane view
 // L[u]); twins tw[k] are shared. Per set exactly the single-set operation
 // order; the NS chains are independent and interleave.
-template <int D, int NS, bool NORM>
-__device__ __forceinline__ void ws_var(const SweepParams &P, const SwLane *L, int v,
-                                      const double2 *const *x, const int *tw,
-                                      const unsigned *code, const double *prev_p0, int it,
+template <int D, int NS, bool NORM, typename T>
+__device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L, int v,
+                                      const typename Ar<T>::T2 *const *x, const int *tw,
+                                      const unsigned *code, const T *prev_p0, int it,
                                       bool write_vtof, const bool *alive,
                                       unsigned long long *dmax, unsigned *uf) {
-  double x0[NS][D], x1[NS][D];
+  using A = Ar<T>;
+  using T2 = typename A::T2;
+  T x0[NS][D], x1[NS][D];
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const double2 m = x[u][k * 32];
+      const T2 m = x[u][k * 32];
       x0[u][k] = m.x;
       x1[u][k] = m.y;
     }
-  double a0[NS], a1[NS];
+  T a0[NS], a1[NS];
 #pragma unroll
-  for (int u = 0; u < NS; ++u) a0[u] = a1[u] = 1.0;
+  for (int u = 0; u < NS; ++u) a0[u] = a1[u] = T(1);
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     const unsigned t = (unsigned)tw[j];
     if (write_vtof && !(t & kUnaryBit)) {
 #pragma unroll
       for (int u = 0; u < NS; ++u) {
-        double b0 = a0[u], b1 = a1[u];
+        T b0 = a0[u], b1 = a1[u];
 #pragma unroll
         for (int k = j + 1; k < D; ++k) {
-          b0 = mul(b0, x0[u][k]);
-          b1 = mul(b1, x1[u][k]);
+          b0 = A::mul(b0, x0[u][k]);
+          b1 = A::mul(b1, x1[u][k]);
         }
-        if (code[u]) sw_clamp(code[u], b0, b1);
+        if (code[u]) sw_clamp_t<T>(code[u], b0, b1);
         if (NORM) {
-          const double tt = add(b0, b1);
-          uf[u] = tt < kMinMessageSum ? t + 1 : uf[u];  // last underflowing slot + 1 (rare)
-          div2_rn(b0, b1, tt, b0, b1);
+          const T tt = A::add(b0, b1);
+          uf[u] = tt < A::min_sum ? t + 1 : uf[u];  // last underflowing slot + 1 (rare)
+          A::div2(b0, b1, tt, b0, b1);
         }
-        if (NS == 1 || alive[u]) L[u].vtof[t * 32] = make_double2(b0, b1);
+        if (NS == 1 || alive[u]) L[u].vtof[t * 32] = A::make2(b0, b1);
       }
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
-      a0[u] = mul(a0[u], x0[u][j]);
-      a1[u] = mul(a1[u], x1[u][j]);
+      a0[u] = A::mul(a0[u], x0[u][j]);
+      a1[u] = A::mul(a1[u], x1[u][j]);
     }
   }
 #pragma unroll
   for (int u = 0; u < NS; ++u) {
     if (NS > 1 && !alive[u]) continue;
-    if (code[u]) sw_clamp(code[u], a0[u], a1[u]);
-    sw_marginal(P, L[u], v, it, a0[u], a1[u], prev_p0[u], dmax[u]);
+    if (code[u]) sw_clamp_t<T>(code[u], a0[u], a1[u]);
+    sw_marginal_t<T>(P, L[u], v, it, a0[u], a1[u], prev_p0[u], dmax[u]);
   }
 }
 
 // any degree, one set, rows re-read per target (heavy nodes: global memory)
-template <bool NORM>
-__device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLane &L, int v,
-                                        const double2 *x, int d, const int *tw, unsigned code,
-                                        double prev_p0, int it, bool write_vtof,
+template <bool NORM, typename T>
+__device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &L, int v,
+                                        const typename Ar<T>::T2 *x, int d, const int *tw,
+                                        unsigned code, T prev_p0, int it, bool write_vtof,
                                         unsigned long long &dmax, unsigned &uf) {
+  using A = Ar<T>;
+  using T2 = typename A::T2;
   if (write_vtof) {
     for (int j = 0; j < d; ++j) {
       const unsigned t = (unsigned)tw[j];
       if (t & kUnaryBit) continue;
-      double b0 = 1.0, b1 = 1.0;
+      T b0 = T(1), b1 = T(1);
       for (int k = 0; k < d; ++k) {
         if (k == j) continue;
-        const double2 m = x[k * 32];
-        b0 = mul(b0, m.x);
-        b1 = mul(b1, m.y);
+        const T2 m = x[k * 32];
+        b0 = A::mul(b0, m.x);
+        b1 = A::mul(b1, m.y);
       }
-      if (code) sw_clamp(code, b0, b1);
+      if (code) sw_clamp_t<T>(code, b0, b1);
       if (NORM) {
-        const double tt = add(b0, b1);
-        uf = tt < kMinMessageSum ? t + 1 : uf;
-        div2_rn(b0, b1, tt, b0, b1);
+        const T tt = A::add(b0, b1);
+        uf = tt < A::min_sum ? t + 1 : uf;
+        A::div2(b0, b1, tt, b0, b1);
       }
-      L.vtof[t * 32] = make_double2(b0, b1);
+      L.vtof[t * 32] = A::make2(b0, b1);
     }
   }
-  double q0 = 1.0, q1 = 1.0;
+  T q0 = T(1), q1 = T(1);
   for (int k = 0; k < d; ++k) {
-    const double2 m = x[k * 32];
-    q0 = mul(q0, m.x);
-    q1 = mul(q1, m.y);
+    const T2 m = x[k * 32];
+    q0 = A::mul(q0, m.x);
+    q1 = A::mul(q1, m.y);
   }
-  if (code) sw_clamp(code, q0, q1);
-  sw_marginal(P, L, v, it, q0, q1, prev_p0, dmax);
+  if (code) sw_clamp_t<T>(code, q0, q1);
+  sw_marginal_t<T>(P, L, v, it, q0, q1, prev_p0, dmax);
 }
 
-template <bool NORM>
-__device__ __forceinline__ void ws_put(const SwLane &L, int t, double o0, double o1, unsigned &uf,
+template <bool NORM, typename T>
+__device__ __forceinline__ void ws_put(const SwLaneT<T> &L, int t, T o0, T o1, unsigned &uf,
                                       bool store) {
+  using A = Ar<T>;
   if (NORM) {
-    const double tt = add(o0, o1);
-    uf = tt < kMinMessageSum ? (unsigned)t + 1 : uf;
-    div2_rn(o0, o1, tt, o0, o1);
+    const T tt = A::add(o0, o1);
+    uf = tt < A::min_sum ? (unsigned)t + 1 : uf;
+    A::div2(o0, o1, tt, o0, o1);
   }
-  if (store) L.ftov[t * 32] = make_double2(o0, o1);
+  if (store) L.ftov[t * 32] = A::make2(o0, o1);
 }
 
 // Factor node of degree D for NS sets; FIRST: iteration 1 (every vtof message
 // is the uniform one, so nothing is read).
-template <int D, int KIND, int NS, bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_fac(const SwLane *L, const double2 *const *x, const int *tw,
-                                      double2 pp, const bool *alive, unsigned *uf) {
-  double m0[NS][D], m1[NS][D];
-  const double c = NORM ? 0.5 : 1.0;
+template <int D, int KIND, int NS, bool NORM, bool FIRST, typename T>
+__device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>::T2 *const *x,
+                                      const int *tw, typename Ar<T>::T2 pp, const bool *alive,
+                                      unsigned *uf) {
+  using A = Ar<T>;
+  using T2 = typename A::T2;
+  T m0[NS][D], m1[NS][D];
+  const T c = NORM ? T(0.5) : T(1);
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
@@ -717,125 +790,128 @@ __device__ __forceinline__ void ws_fac(const SwLane *L, const double2 *const *x,
         m0[u][k] = c;
         m1[u][k] = c;
       } else {
-        const double2 m = x[u][k * 32];
+        const T2 m = x[u][k * 32];
         m0[u][k] = m.x;
         m1[u][k] = m.y;
       }
     }
-  double sm[NS][D];
+  T sm[NS][D];
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
-    for (int k = 1; k < D; ++k) sm[u][k] = add(m0[u][k], m1[u][k]);
+    for (int k = 1; k < D; ++k) sm[u][k] = A::add(m0[u][k], m1[u][k]);
 #pragma unroll
   for (int u = 0; u < NS; ++u) {
-    double h1 = 1.0, h2 = 1.0;
+    T h1 = T(1), h2 = T(1);
 #pragma unroll
     for (int k = 1; k < D; ++k) {
-      h1 = mul(h1, sm[u][k]);
-      h2 = mul(h2, KIND == 0 ? m1[u][k] : m0[u][k]);
+      h1 = A::mul(h1, sm[u][k]);
+      h2 = A::mul(h2, KIND == 0 ? m1[u][k] : m0[u][k]);
     }
-    double o0, o1;
-    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    ws_put<NORM>(L[u], tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
+    T o0, o1;
+    head_message_t<KIND, T>(pp.x, pp.y, h1, h2, o0, o1);
+    ws_put<NORM, T>(L[u], tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
   }
   if (D > 1) {
-    double a1[NS], a2[NS];
+    T a1[NS], a2[NS];
 #pragma unroll
-    for (int u = 0; u < NS; ++u) head_slot_terms<KIND>(pp.x, pp.y, m0[u][0], m1[u][0], a1[u], a2[u]);
+    for (int u = 0; u < NS; ++u) head_slot_terms_t<KIND, T>(pp.x, pp.y, m0[u][0], m1[u][0], a1[u], a2[u]);
 #pragma unroll
     for (int j = 1; j < D; ++j) {
 #pragma unroll
       for (int u = 0; u < NS; ++u) {
-        double b1 = a1[u], b2 = a2[u];
+        T b1 = a1[u], b2 = a2[u];
 #pragma unroll
         for (int k = j + 1; k < D; ++k) {
-          b1 = mul(b1, sm[u][k]);
-          b2 = mul(b2, KIND == 0 ? m1[u][k] : m0[u][k]);
+          b1 = A::mul(b1, sm[u][k]);
+          b2 = A::mul(b2, KIND == 0 ? m1[u][k] : m0[u][k]);
         }
-        double o0, o1;
-        body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-        ws_put<NORM>(L[u], tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
-        a1[u] = mul(a1[u], sm[u][j]);
-        a2[u] = mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
+        T o0, o1;
+        body_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
+        ws_put<NORM, T>(L[u], tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
+        a1[u] = A::mul(a1[u], sm[u][j]);
+        a2[u] = A::mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
       }
     }
   }
 }
 
-template <int KIND, bool NORM, bool FIRST>
-__device__ __noinline__ void ws_fac_any(const SwLane &L, const double2 *x, int d, const int *tw,
-                                        double2 pp, unsigned &uf) {
-  const double c = NORM ? 0.5 : 1.0;
+template <int KIND, bool NORM, bool FIRST, typename T>
+__device__ __noinline__ void ws_fac_any(const SwLaneT<T> &L, const typename Ar<T>::T2 *x, int d,
+                                        const int *tw, typename Ar<T>::T2 pp, unsigned &uf) {
+  using A = Ar<T>;
+  using T2 = typename A::T2;
+  const T c = NORM ? T(0.5) : T(1);
   for (int j = 0; j < d; ++j) {
-    double b1 = 1.0, b2 = 1.0;
+    T b1 = T(1), b2 = T(1);
     for (int k = 0; k < d; ++k) {
       if (k == j) continue;
-      const double2 m = FIRST ? make_double2(c, c) : x[k * 32];
-      double f1, f2;
+      const T2 m = FIRST ? A::make2(c, c) : x[k * 32];
+      T f1, f2;
       if (k == 0) {
-        head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
+        head_slot_terms_t<KIND, T>(pp.x, pp.y, m.x, m.y, f1, f2);
       } else {
-        f1 = add(m.x, m.y);
+        f1 = A::add(m.x, m.y);
         f2 = KIND == 0 ? m.y : m.x;
       }
-      b1 = mul(b1, f1);
-      b2 = mul(b2, f2);
+      b1 = A::mul(b1, f1);
+      b2 = A::mul(b2, f2);
     }
-    double o0, o1;
+    T o0, o1;
     if (j == 0)
-      head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+      head_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
     else
-      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-    ws_put<NORM>(L, tw[j], o0, o1, uf, true);
+      body_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
+    ws_put<NORM, T>(L, tw[j], o0, o1, uf, true);
   }
 }
 
 // degree dispatch; NS = 2 keeps the register path to degree 4 (two sets of rows)
-template <int KIND, int NS, bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_fac_k(const SwLane *L, const double2 *const *x, int d,
-                                        const int *tw, double2 pp, const bool *alive,
+template <int KIND, int NS, bool NORM, bool FIRST, typename T>
+__device__ __forceinline__ void ws_fac_k(const SwLaneT<T> *L, const typename Ar<T>::T2 *const *x,
+                                        int d, const int *tw, typename Ar<T>::T2 pp,
+                                        const bool *alive,
                                         unsigned *uf) {
   switch (d) {
-    case 1: ws_fac<1, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
-    case 2: ws_fac<2, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
-    case 3: ws_fac<3, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
-    case 4: ws_fac<4, KIND, NS, NORM, FIRST>(L, x, tw, pp, alive, uf); break;
+    case 1: ws_fac<1, KIND, NS, NORM, FIRST, T>(L, x, tw, pp, alive, uf); break;
+    case 2: ws_fac<2, KIND, NS, NORM, FIRST, T>(L, x, tw, pp, alive, uf); break;
+    case 3: ws_fac<3, KIND, NS, NORM, FIRST, T>(L, x, tw, pp, alive, uf); break;
+    case 4: ws_fac<4, KIND, NS, NORM, FIRST, T>(L, x, tw, pp, alive, uf); break;
 #if HBP_WS_DMAX > 4
     case 5:
       if (NS == 1) {
-        ws_fac<5, KIND, 1, NORM, FIRST>(L, x, tw, pp, alive, uf);
+        ws_fac<5, KIND, 1, NORM, FIRST, T>(L, x, tw, pp, alive, uf);
         break;
       }
 #endif
     default:
 #pragma unroll
       for (int u = 0; u < NS; ++u)
-        if (NS == 1 || alive[u]) ws_fac_any<KIND, NORM, FIRST>(L[u], x[u], d, tw, pp, uf[u]);
+        if (NS == 1 || alive[u]) ws_fac_any<KIND, NORM, FIRST, T>(L[u], x[u], d, tw, pp, uf[u]);
       break;
   }
 }
 
-template <int NS, bool NORM>
-__device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, int v,
-                                        const double2 *const *x, int d, const int *tw,
-                                        const unsigned *code, const double *prev_p0, int it,
+template <int NS, bool NORM, typename T>
+__device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLaneT<T> *L, int v,
+                                        const typename Ar<T>::T2 *const *x, int d, const int *tw,
+                                        const unsigned *code, const T *prev_p0, int it,
                                         bool write_vtof, const bool *alive,
                                         unsigned long long *dmax, unsigned *uf) {
   switch (d) {
-    case 1: ws_var<1, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
-    case 2: ws_var<2, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
-    case 3: ws_var<3, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
-    case 4: ws_var<4, NS, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 1: ws_var<1, NS, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 2: ws_var<2, NS, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 3: ws_var<3, NS, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
+    case 4: ws_var<4, NS, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf); break;
 #if HBP_WS_DMAX > 4
     case 5:
       if (NS == 1) {
-        ws_var<5, 1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
+        ws_var<5, 1, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
         break;
       }
     case 6:
       if (NS == 1) {
-        ws_var<6, 1, NORM>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
+        ws_var<6, 1, NORM, T>(P, L, v, x, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
         break;
       }
 #endif
@@ -843,7 +919,7 @@ __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, 
 #pragma unroll
       for (int u = 0; u < NS; ++u)
         if (NS == 1 || alive[u])
-          ws_var_any<NORM>(P, L[u], v, x[u], d, tw, code[u], prev_p0[u], it, write_vtof, dmax[u],
+          ws_var_any<NORM, T>(P, L[u], v, x[u], d, tw, code[u], prev_p0[u], it, write_vtof, dmax[u],
                            uf[u]);
       break;
   }
@@ -857,15 +933,16 @@ __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLane *L, 
 // degrees, so the phases stay balanced without atomics.
 // side 0 = variables (ftov rows + P0 rows if want_p0 + evidence rows),
 // side 1 = factors (vtof rows unless iteration 1, + factor parameters).
-template <int NS>
-__device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B, WsShared<NS> &sh,
+template <int NS, typename T>
+__device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufsT<T> &B,
+                                           WsShared<NS, T> &sh,
                                            int side, const int4 *chunks, int cfirst, int count,
                                            unsigned *claim, bool want_msg, bool want_p0, int g0,
                                            unsigned &seq) {
   const int lane = threadIdx.x & 31;
   const int *rowptr = side == 0 ? P.vrow : P.frow;
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
-  const double2 *msg = side == 0 ? B.ftov : B.vtof;
+  const typename Ar<T>::T2 *msg = side == 0 ? B.ftov : B.vtof;
   if (lane != 0) return;
   // chunks are claimed two at a time from the CTA row's counter; the next
   // claim is in flight while the current pair is staged
@@ -879,7 +956,7 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B
       const int c = cfirst + (int)k + h;
       const unsigned slot = seq % kRing;
       mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
-      WsChunk<NS> &ch = sh.ring[slot];
+      WsChunk<NS, T> &ch = sh.ring[slot];
       ++seq;
       if (c >= count) {  // end of the phase's chunks: a sentinel, no bytes
         ch.n0 = -1;
@@ -898,8 +975,8 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B
       const int tw_lo = r0 & ~3, tw_hi = (r1 + 3) & ~3;
       const unsigned b_rp = (rp_hi - rp_lo) * 4;
       const unsigned b_tw = heavy ? 0u : (unsigned)(tw_hi - tw_lo) * 4;
-      const unsigned b_msg = (heavy || !want_msg) ? 0u : (unsigned)(r1 - r0) * 512;
-      const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 256 : 0u;
+      const unsigned b_msg = (heavy || !want_msg) ? 0u : (unsigned)(r1 - r0) * 32 * sizeof(typename Ar<T>::T2);
+      const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 32 * sizeof(T) : 0u;
       const unsigned b_ev = side == 0 ? (unsigned)m * 32 : 0u;
       const unsigned b_fp = side == 1 ? (unsigned)m * 16 : 0u;
       mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_fp + NS * (b_msg + b_p0 + b_ev));
@@ -920,9 +997,9 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufs &B
 
 // Consumers: node i of the phase's node stream goes to warp (i mod consumers),
 // so the warps stay balanced across chunks of any size.
-template <int NS, bool NORM, bool FIRST>
-__device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS> &sh,
-                                               const SwLane *L, int cw, const bool *alive,
+template <int NS, bool NORM, bool FIRST, typename T>
+__device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS, T> &sh,
+                                               const SwLaneT<T> *L, int cw, const bool *alive,
                                                unsigned &seq, unsigned *uf, bool unary = false) {
   const int lane = threadIdx.x & 31;
   bool any = false;
@@ -932,7 +1009,7 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
   for (;;) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk<NS> &ch = sh.ring[slot];
+    const WsChunk<NS, T> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     if (n0 < 0) {  // the producer's end-of-phase sentinel
       __syncwarp();
@@ -948,7 +1025,8 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
         const int d = ch.rp[f + 1 - rp_lo] - r;
         // unary: a constant message, written in iteration 1 (and again after a compaction)
         if (!FIRST && !unary && d == 1) continue;
-        const double2 pp = ch.fpar[f - n0];
+        const double2 ppd = ch.fpar[f - n0];
+        const typename Ar<T>::T2 pp = Ar<T>::make2((T)ppd.x, (T)ppd.y);
         const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
         if (ch.heavy) {
           // rows not staged: twins and messages from global memory
@@ -956,17 +1034,17 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
 #pragma unroll
           for (int u = 0; u < NS; ++u) {
             if (!alive[u]) continue;
-            const double2 *x = L[u].vtof + (size_t)r * 32;
-            if (!is_or) ws_fac_any<0, NORM, FIRST>(L[u], x, d, tw, pp, uf[u]);
-            else ws_fac_any<1, NORM, FIRST>(L[u], x, d, tw, pp, uf[u]);
+            const typename Ar<T>::T2 *x = L[u].vtof + (size_t)r * 32;
+            if (!is_or) ws_fac_any<0, NORM, FIRST, T>(L[u], x, d, tw, pp, uf[u]);
+            else ws_fac_any<1, NORM, FIRST, T>(L[u], x, d, tw, pp, uf[u]);
           }
         } else {
           const int *tw = ch.tw + (r - tw_lo);
-          const double2 *x[NS];
+          const typename Ar<T>::T2 *x[NS];
 #pragma unroll
           for (int u = 0; u < NS; ++u) x[u] = &ch.msg[u][r - r0][lane];
-          if (!is_or) ws_fac_k<0, NS, NORM, FIRST>(L, x, d, tw, pp, alive, uf);
-          else ws_fac_k<1, NS, NORM, FIRST>(L, x, d, tw, pp, alive, uf);
+          if (!is_or) ws_fac_k<0, NS, NORM, FIRST, T>(L, x, d, tw, pp, alive, uf);
+          else ws_fac_k<1, NS, NORM, FIRST, T>(L, x, d, tw, pp, alive, uf);
         }
       }
     }
@@ -977,9 +1055,9 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
   }
 }
 
-template <int NS, bool NORM>
-__device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS> &sh,
-                                               const SwLane *L, int cw, int it, bool write_vtof,
+template <int NS, bool NORM, typename T>
+__device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS, T> &sh,
+                                               const SwLaneT<T> *L, int cw, int it, bool write_vtof,
                                                const bool *alive, unsigned &seq,
                                                unsigned long long *dmax, unsigned *uf) {
   const int lane = threadIdx.x & 31;
@@ -990,7 +1068,7 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
   for (;;) {
     const unsigned slot = seq % kRing;
     mbar_wait(&sh.full[slot], (seq / kRing) & 1);
-    const WsChunk<NS> &ch = sh.ring[slot];
+    const WsChunk<NS, T> &ch = sh.ring[slot];
     const int n0 = ch.n0, n1 = ch.n1, r0 = ch.r0;
     if (n0 < 0) {  // the producer's end-of-phase sentinel
       __syncwarp();
@@ -1005,26 +1083,26 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
         const int r = ch.rp[v - rp_lo];
         const int d = ch.rp[v + 1 - rp_lo] - r;
         unsigned code[NS];
-        double prev_p0[NS];
+        T prev_p0[NS];
 #pragma unroll
         for (int u = 0; u < NS; ++u) {
           code[u] = ch.ev[u][v - n0][lane];
-          prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : 0.5;
+          prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : T(0.5);
         }
         if (ch.heavy) {
 #pragma unroll
           for (int u = 0; u < NS; ++u)
             if (alive[u])
-              ws_var_any<NORM>(P, L[u], v, L[u].ftov + (size_t)r * 32, d,
+              ws_var_any<NORM, T>(P, L[u], v, L[u].ftov + (size_t)r * 32, d,
                                (const int *)P.ftov_twin + r, code[u], prev_p0[u], it, write_vtof,
                                dmax[u], uf[u]);
           continue;
         }
         const int *tw = ch.tw + (r - tw_lo);
-        const double2 *x[NS];
+        const typename Ar<T>::T2 *x[NS];
 #pragma unroll
         for (int u = 0; u < NS; ++u) x[u] = &ch.msg[u][r - r0][lane];
-        ws_var_k<NS, NORM>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
+        ws_var_k<NS, NORM, T>(P, L, v, x, d, tw, code, prev_p0, it, write_vtof, alive, dmax, uf);
       }
     }
     base += n1 - n0;
@@ -1068,13 +1146,14 @@ constexpr int kMaxCompact = 1024;  // passes up to this many slots may compact
 //    alternate buffers), slot2set is rewritten and the buffers swap. Per-set
 //    control data is indexed by set, not slot, and res_pos records where each
 //    set's final marginals are.
-template <bool NORM, int NS>
+template <bool NORM, int NS, typename T>
 __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     sweep_ws(const __grid_constant__ SweepParams P) {
+  using T2 = typename Ar<T>::T2;
   constexpr int kWsConsumers = WsCfg<NS>::consumers;
   constexpr int kWarps = kWsConsumers + 1;
   extern __shared__ __align__(128) unsigned char ws_smem[];
-  WsShared<NS> &sh = *reinterpret_cast<WsShared<NS> *>(ws_smem);
+  WsShared<NS, T> &sh = *reinterpret_cast<WsShared<NS, T> *>(ws_smem);
   __shared__ unsigned umask[kMaxUnits][NS];  // running sets per unit, one bit per lane
   __shared__ int ulist[kMaxUnits];            // running units, ascending
   __shared__ int s_nunits, s_nrun;
@@ -1085,13 +1164,13 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   const int units = gridDim.y;
   const int S = P.S;
   const unsigned nblocks = gridDim.x * gridDim.y;
-  SwBufs B;
-  B.ftov = P.ftov;
-  B.vtof = P.vtof;
-  B.p0 = P.p0;
+  SwBufsT<T> B;
+  B.ftov = (T2 *)P.ftov;
+  B.vtof = (T2 *)P.vtof;
+  B.p0 = (T *)P.p0;
   B.ev = const_cast<unsigned char *>(P.ev);
   B.parity = 0;
-  SwLane L[NS];
+  SwLaneT<T> L[NS];
   bool alive[NS];
   int sidx[NS];  // slots
   int sset[NS];  // their sets
@@ -1162,7 +1241,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     for (int u = 0; u < NS; ++u) {
       sidx[u] = (t * NS + u) * 32 + lane;
       sset[u] = set_of(sidx[u]);
-      L[u] = sw_lane_b(B, sidx[u], sset[u], P.E, P.V);
+      L[u] = sw_lane_bt<T>(B, sidx[u], sset[u], P.E, P.V);
       alive[u] = (umask[t][u] >> lane) & 1u;
     }
   };
@@ -1225,17 +1304,17 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         const int o = n2o[k];
         const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
         const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
-        P.p0_alt[dst] = B.p0[src];
+        ((T *)P.p0_alt)[dst] = B.p0[src];
         P.ev_alt[dst] = B.ev[src];
       }
     }
     if (blockIdx.x == 0 && blockIdx.y == 0)
       for (int k = threadIdx.x; k < S; k += blockDim.x) P.slot2set[k] = k < R ? s2s_old[n2o[k]] : -1;
     sw_grid_sync(P.bar, expected, nblocks);
-    double2 *nv = B.ftov;  // holds the packed vtof rows
+    T2 *nv = B.ftov;  // holds the packed vtof rows
     B.ftov = B.vtof;
     B.vtof = nv;
-    B.p0 = P.p0_alt;
+    B.p0 = (T *)P.p0_alt;
     B.ev = P.ev_alt;
     B.parity = 1;
     compacted = true;
@@ -1260,10 +1339,10 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         bind_unit(t);
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, B, sh, 0, P.vchunks, 0, P.n_vchunks,
+          ws_produce<NS, T>(P, B, sh, 0, P.vchunks, 0, P.n_vchunks,
                          P.claim + (size_t)((2 * it) & 1) * units + t, true, it > 2, t * NS, seq);
         } else {
-          ws_consume_var<NS, NORM>(P, sh, L, warp, it, !final_pass, alive, seq, dmax, uf);
+          ws_consume_var<NS, NORM, T>(P, sh, L, warp, it, !final_pass, alive, seq, dmax, uf);
         }
         if (!producer)
 #pragma unroll
@@ -1325,13 +1404,13 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         const int c0 = (first || rewrite_unary) ? 0 : P.fchunk_nonunary;
         if (producer) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          ws_produce<NS>(P, B, sh, 1, P.fchunks, c0, P.n_fchunks,
+          ws_produce<NS, T>(P, B, sh, 1, P.fchunks, c0, P.n_fchunks,
                          P.claim + (size_t)((2 * it + 1) & 1) * units + t, !first, false, t * NS,
                          seq);
         } else if (first) {
-          ws_consume_fac<NS, NORM, true>(P, sh, L, warp, alive, seq, uf);
+          ws_consume_fac<NS, NORM, true, T>(P, sh, L, warp, alive, seq, uf);
         } else {
-          ws_consume_fac<NS, NORM, false>(P, sh, L, warp, alive, seq, uf, rewrite_unary);
+          ws_consume_fac<NS, NORM, false, T>(P, sh, L, warp, alive, seq, uf, rewrite_unary);
         }
         if (!producer)
 #pragma unroll
@@ -1374,16 +1453,17 @@ __device__ __forceinline__ size_t final_pos(const int *res_pos, int s, int vi, i
   return tile_pos(vi, rp & 0x3fffffff, V);
 }
 
-__global__ void sweep_marginals_kernel(const double *p0, const double *p0_alt, const int *res_pos,
+template <typename T>
+__global__ void sweep_marginals_kernel(const T *p0, const T *p0_alt, const int *res_pos,
                                        const int *vinv, const int *sel, int nsel,
                                        int V, int nsets, int set_base, double *out_pair,
                                        double *out_p1) {
-  __shared__ double tile[32][33];
+  __shared__ T tile[32][33];
   const int k0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // blockDim 256: 8 rows per step
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r, s = s0 + tx;
-    double v = 0.0;
+    T v = T(0);
     if (k < nsel && s < nsets) {
       const int var = sel ? sel[k] : k;
       int par;
@@ -1396,13 +1476,14 @@ __global__ void sweep_marginals_kernel(const double *p0, const double *p0_alt, c
   for (int r = ty; r < 32; r += 8) {
     const int s = s0 + r, k = k0 + tx;
     if (k < nsel && s < nsets) {
-      const double q = tile[tx][r];
+      const T q = tile[tx][r];
+      const double p1 = (double)Ar<T>::sub(T(1), q);  // P1 = 1 - P0 in the run's precision
       const size_t o = (size_t)(set_base + s) * nsel + k;
       if (out_pair) {
-        out_pair[2 * o] = q;
-        out_pair[2 * o + 1] = sub(1.0, q);
+        out_pair[2 * o] = (double)q;
+        out_pair[2 * o + 1] = p1;
       }
-      if (out_p1) out_p1[o] = sub(1.0, q);
+      if (out_p1) out_p1[o] = p1;
     }
   }
 }
@@ -1411,7 +1492,8 @@ __global__ void sweep_marginals_kernel(const double *p0, const double *p0_alt, c
 // ties by ascending id. One CTA per set; bitonic sort of (~bits(P1), position)
 // in shared memory -- P1 >= 0, so its bit pattern orders like its value, and
 // positions index the id-sorted selection. Labeled = clamped in this set.
-__global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, const double *p0_alt,
+template <typename T>
+__global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *p0_alt,
                                                            const unsigned char *ev,
                                                            const unsigned char *ev_alt,
                                                            const int *res_pos,
@@ -1428,7 +1510,7 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const double *p0, cons
       int par;
       const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
       if ((par ? ev_alt : ev)[at] == 0) {
-        const double p1 = sub(1.0, (par ? p0_alt : p0)[at]);
+        const double p1 = (double)Ar<T>::sub(T(1), (par ? p0_alt : p0)[at]);
         k = ~(unsigned long long)__double_as_longlong(p1);
       }
     }
@@ -1469,6 +1551,9 @@ struct hbp_sweep {
   int cap = 0;           // sets per pass (multiple of 32)
   int grid_x_max = 0;    // co-resident CTAs for the cooperative launch
   const void *kernel = nullptr, *kernel_nonorm = nullptr;
+  const void *kernel32 = nullptr, *kernel32_nonorm = nullptr;  // fp32 mode
+  size_t smem32 = 0;
+  int grid_x_max32 = 0;
   int ns = 1;           // sets per lane of the staged kernel (pass sizes are multiples of 32 * ns)
   int threads = 0;
   int *d_vinv = nullptr;
@@ -1543,16 +1628,26 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
       const char *nenv = getenv("HBP_SWEEP_NS");
       sw->ns = nenv ? (atoi(nenv) == 2 ? 2 : 1) : hbp::kSweepNS;
       if (sw->ns == 2) {
-        sw->smem = sizeof(hbp::WsShared<2>);
+        sw->smem = sizeof(hbp::WsShared<2, double>);
         sw->threads = hbp::WsCfg<2>::threads;
-        sw->kernel = (const void *)hbp::sweep_ws<true, 2>;
-        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 2>;
+        sw->kernel = (const void *)hbp::sweep_ws<true, 2, double>;
+        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 2, double>;
       } else {
-        sw->smem = sizeof(hbp::WsShared<1>);
+        sw->smem = sizeof(hbp::WsShared<1, double>);
         sw->threads = hbp::WsCfg<1>::threads;
-        sw->kernel = (const void *)hbp::sweep_ws<true, 1>;
-        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 1>;
+        sw->kernel = (const void *)hbp::sweep_ws<true, 1, double>;
+        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 1, double>;
       }
+      // fp32 mode (opt-in per run): the same staged kernel on float messages
+      sw->smem32 = sizeof(hbp::WsShared<1, float>);
+      sw->kernel32 = (const void *)hbp::sweep_ws<true, 1, float>;
+      sw->kernel32_nonorm = (const void *)hbp::sweep_ws<false, 1, float>;
+      for (const void *k : {sw->kernel32, sw->kernel32_nonorm})
+        HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem32));
+      int per_sm32 = 0;
+      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, sw->kernel32,
+                                                             hbp::WsCfg<1>::threads, sw->smem32));
+      sw->grid_x_max32 = std::max(1, per_sm32) * g->num_sms;
       for (const void *k : {sw->kernel, sw->kernel_nonorm})
         HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem));
       HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, sw->threads,
@@ -1663,6 +1758,15 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   }
   if (opt->record_history) {
     hbp::set_error("record_history is not supported by the sweep");
+    return HBP_EINVAL;
+  }
+  if (opt->precision != 0 && opt->precision != 1) {
+    hbp::set_error("precision must be 0 (fp64) or 1 (fp32)");
+    return HBP_EINVAL;
+  }
+  const bool fp32 = opt->precision == 1;
+  if (fp32 && !sw->ws) {
+    hbp::set_error("fp32 mode needs the staged sweep kernel");
     return HBP_EINVAL;
   }
   hbp_graph *g = sw->g;
@@ -1855,11 +1959,14 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
     if (sw->ws) {
-      const int gy = groups / sw->ns;
-      const int nxw = std::max(1, std::min(sw->grid_x_max / gy, sw->n_vchunks));
-      HBP_CUDA(cudaLaunchCooperativeKernel(P.normalize ? sw->kernel : sw->kernel_nonorm,
-                                           dim3(nxw, gy), dim3(sw->threads), args, sw->smem,
-                                           st));
+      const int gy = groups / (fp32 ? 1 : sw->ns);
+      const int gxm = fp32 ? sw->grid_x_max32 : sw->grid_x_max;
+      const int nxw = std::max(1, std::min(gxm / gy, sw->n_vchunks));
+      const void *k = fp32 ? (P.normalize ? sw->kernel32 : sw->kernel32_nonorm)
+                           : (P.normalize ? sw->kernel : sw->kernel_nonorm);
+      HBP_CUDA(cudaLaunchCooperativeKernel(k, dim3(nxw, gy),
+                                           dim3(fp32 ? hbp::WsCfg<1>::threads : sw->threads), args,
+                                           fp32 ? sw->smem32 : sw->smem, st));
     } else {
       HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups), dim3(hbp::kSwThreads), args,
                                            0, st));
@@ -1870,8 +1977,13 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     if (out->marginals) {
       double *dst = marg_dev ? out->marginals : stage_marg;
       const int bbase = marg_dev ? base : 0;
-      hbp::sweep_marginals_kernel<<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
+      if (fp32)
+        hbp::sweep_marginals_kernel<float><<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
+            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V,
+            L.V, ns, bbase, dst, nullptr);
+      else
+        hbp::sweep_marginals_kernel<double><<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
+            sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
       ++launches;
       if (!marg_dev)
         HBP_CUDA(cudaMemcpyAsync(out->marginals + (size_t)base * L.V * 2, stage_marg,
@@ -1880,8 +1992,13 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     if (out->p1_select && nsel) {
       double *dst = p1_dev ? out->p1_select : stage_p1;
       const int bbase = p1_dev ? base : 0;
-      hbp::sweep_marginals_kernel<<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
-          sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
+      if (fp32)
+        hbp::sweep_marginals_kernel<float><<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
+            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel,
+            L.V, ns, bbase, nullptr, dst);
+      else
+        hbp::sweep_marginals_kernel<double><<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
+            sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
       ++launches;
       if (!p1_dev)
         HBP_CUDA(cudaMemcpyAsync(out->p1_select + (size_t)base * nsel, stage_p1,
@@ -1891,12 +2008,20 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       int *dst = rk_dev ? out->ranked : stage_rk;
       const int bbase = rk_dev ? base : 0;
       const size_t smem = (size_t)std::max(npow2, 2) * 12;
-      if (smem > 48 * 1024)
-        HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel,
+      if (smem > 48 * 1024) {
+        HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel<double>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      hbp::sweep_rank_kernel<<<ns, 1024, smem, st>>>(sw->d_p0, sw->d_p0_alt, sw->d_ev, sw->d_ev_alt,
-                                                     d_rpos, sw->d_vinv, d_sel, nsel,
-                                                     std::max(npow2, 2), L.V, bbase, out->topk, dst);
+        HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel<float>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      }
+      if (fp32)
+        hbp::sweep_rank_kernel<float><<<ns, 1024, smem, st>>>(
+            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, sw->d_ev, sw->d_ev_alt, d_rpos,
+            sw->d_vinv, d_sel, nsel, std::max(npow2, 2), L.V, bbase, out->topk, dst);
+      else
+        hbp::sweep_rank_kernel<double><<<ns, 1024, smem, st>>>(
+            sw->d_p0, sw->d_p0_alt, sw->d_ev, sw->d_ev_alt, d_rpos, sw->d_vinv, d_sel, nsel,
+            std::max(npow2, 2), L.V, bbase, out->topk, dst);
       ++launches;
       if (!rk_dev)
         HBP_CUDA(cudaMemcpyAsync(out->ranked + (size_t)base * out->topk, stage_rk,

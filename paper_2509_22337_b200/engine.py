@@ -64,8 +64,13 @@ class EngineOptions:
     normalize_messages: bool = True
     time_limit: Optional[float] = None
     record_history: bool = False
+    # extension (not in the reference): "fp64" -- bitwise with the reference --
+    # or "fp32" messages for run_many (marginals within 1e-5 of fp64)
+    precision: str = "fp64"
 
     def validate(self) -> None:
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
         if self.max_iterations < 1:
             raise ValueError("max_iterations must be at least 1")
         if self.tolerance < 0:
@@ -158,7 +163,8 @@ class _Plan:
     def options(self, options: EngineOptions) -> _native.Options:
         return _native.Options(int(options.max_iterations), int(bool(options.normalize_messages)),
                                int(bool(options.record_history)), 0, float(options.tolerance),
-                               float(options.time_limit) if options.time_limit else 0.0)
+                               float(options.time_limit) if options.time_limit else 0.0,
+                               1 if options.precision == "fp32" else 0)
 
     def run(self, options: EngineOptions, graph: FactorGraph) -> InferenceResult:
         V = self.dg.num_variables
@@ -334,6 +340,8 @@ def run(graph: FactorGraph, schedule: Schedule, options: Optional[EngineOptions]
     max |dP1| < tolerance after an iteration."""
     options = options or EngineOptions()
     options.validate()
+    if options.precision != "fp64":
+        raise ValueError("run() is fp64 only (bitwise with the reference); fp32 mode: run_many")
     _resolve_workers(workers)
     dg = device_graph(graph)
     return dg.plan(schedule, graph).run(options, graph)

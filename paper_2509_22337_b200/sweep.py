@@ -140,6 +140,8 @@ def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Str
     if topk and sel is None:
         raise ValueError("topk needs a selection (the alarm variables)")
     if not _is_parall(strategy):
+        if options.precision != "fp64":
+            raise ValueError("fp32 mode needs the PARALL sweep")
         return _run_materialised(graph, off, var, val, strategy, options, marginals, deltas, sel,
                                  topk)
     device_out = device_out or {}
@@ -180,7 +182,8 @@ def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Str
                           _native.ptr(val, C.c_int8))
     opt = _native.Options(int(options.max_iterations), int(bool(options.normalize_messages)), 0,
                           0, float(options.tolerance),
-                          float(options.time_limit) if options.time_limit else 0.0)
+                          float(options.time_limit) if options.time_limit else 0.0,
+                          1 if options.precision == "fp32" else 0)
     st = _native.lib().hbp_sweep_run(sw.handle, C.byref(opt), C.byref(ev), C.byref(outs))
     if st != _native.HBP_OK:
         if st == _native.HBP_EINVAL:

@@ -200,3 +200,30 @@ def test_sweep_ftp_many_sets_vs_oracle():
         o, _ = oracle_set(g, list(zip(ids.tolist(), labels.tolist())), opts)
         assert res.iterations[j] == o["iterations"], j
         assert res.marginals[j].tobytes() == o["marginals"].tobytes(), j
+
+
+@pytest.mark.parametrize("name,n", [("hedc", 64), ("ftp", 16)])
+def test_sweep_fp32_mode_within_1e5_of_fp64(name, n):
+    """Optional fp32 mode (north star: marginals within 1e-5 of the fp64
+    reference): float messages / marginals in the same staged kernel."""
+    g, alarms = W.graph(name)
+    sets = [W.evidence_set(alarms, j, size=min(8, len(alarms))) for j in range(n)]
+    opts64 = EngineOptions(1000, 1e-9)
+    opts32 = EngineOptions(1000, 1e-9, precision="fp32")
+    r64 = P.run_many(g, sets, None, opts64)
+    r32 = P.run_many(g, sets, None, opts32)
+    assert r32.converged.all()
+    assert np.abs(r32.marginals - r64.marginals).max() < 1e-5
+    assert (np.abs(r32.iterations - r64.iterations) <= 3).all()
+    for j in range(min(4, n)):  # and against the oracle directly
+        ids, labels = sets[j]
+        o, _ = oracle_set(g, list(zip(ids.tolist(), labels.tolist())), opts64)
+        assert np.abs(r32.marginals[j] - o["marginals"]).max() < 1e-5
+
+
+def test_fp32_is_sweep_only():
+    g, _ = W.graph("weblech")
+    with pytest.raises(ValueError):
+        P.run(g, Strategy.parall().compile(g), EngineOptions(precision="fp32"))
+    with pytest.raises(ValueError):
+        P.run_many(g, [[]], Strategy.seqfix(), EngineOptions(precision="fp32"))
