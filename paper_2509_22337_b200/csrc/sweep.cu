@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
 template <typename T>
 struct SwLaneT {
   typename Ar<T>::T2 *vtof, *ftov;  // &X[g][0][lane]
-  T *p0;
+  double *p0;                       // marginals are fp64 in both precisions
   const unsigned char *ev;
   int s;                            // the set (control arrays are indexed by set)
 };
@@ -519,7 +519,7 @@ struct SwLaneT {
 template <typename T>
 struct SwBufsT {
   typename Ar<T>::T2 *ftov, *vtof;
-  T *p0;
+  double *p0;
   unsigned char *ev;
   int parity;  // 0: the pass's original p0 / ev buffers, 1: the alternates
 };
@@ -550,24 +550,22 @@ __device__ __forceinline__ void sw_clamp_t(unsigned code, T &a0, T &a1) {
   }
 }
 
-// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572);
-// for T = double exactly sw_marginal; |dP1| is widened (exactly) to double bits
-template <typename T>
-__device__ __forceinline__ void sw_marginal_t(const SweepParams &P, const SwLaneT<T> &L, int v,
-                                             int it, T q0, T q1, T prev_p0,
+// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572),
+// always in fp64 -- for fp64 runs exactly sw_marginal; fp32 runs feed it the
+// fp64 product of their fp32 messages
+__device__ __forceinline__ void sw_marginal_d(const SweepParams &P, double *p0_slot, int set, int v,
+                                             int it, double q0, double q1, double prev_p0,
                                              unsigned long long &dmax) {
-  using A = Ar<T>;
-  const T t = A::add(q0, q1);
-  if (t < A::min_sum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], P.vorig[v]);
-  const T p0 = A::div(q0, t);
-  const T p1 = A::sub(T(1), p0);
-  const T prev = it == 2 ? T(0.5) : A::sub(T(1), prev_p0);  // prev P1 starts at 0.5
-  const double diff = (double)A::sub(p1, prev);
-  const unsigned long long raw = (unsigned long long)__double_as_longlong(diff);
+  const double t = add(q0, q1);
+  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + set], P.vorig[v]);
+  const double p0 = div_rn(q0, t);
+  const double p1 = sub(1.0, p0);
+  const double prev = it == 2 ? 0.5 : sub(1.0, prev_p0);  // prev P1 starts at 0.5
+  const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, prev));
   unsigned long long bits;
   asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
   dmax = bits > dmax ? bits : dmax;
-  L.p0[v * 32] = p0;
+  *p0_slot = p0;
 }
 
 // ---- TMA-staged, warp-specialised sweep kernel (default) ------------------------------------
@@ -619,7 +617,7 @@ template <int NS, typename T>
 struct __align__(16) WsChunk {
   using T2 = typename Ar<T>::T2;
   T2 msg[NS][kChR][32];           // message rows of the chunk, one row (32 lanes) per slot and group
-  T p0[NS][kChN][32];             // variable side: P0 of the previous iteration per node
+  double p0[NS][kChN][32];        // variable side: P0 of the previous iteration per node
   unsigned char ev[NS][kChN][32]; // variable side: evidence codes per node
   double2 fpar[kChN];             // factor side: (p1, p2) per node
   int rp[kChN + 8];               // row pointers, aligned window from (n0 & ~3)
@@ -670,7 +668,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 template <int D, int NS, bool NORM, typename T>
 __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L, int v,
                                       const typename Ar<T>::T2 *const *x, const int *tw,
-                                      const unsigned *code, const T *prev_p0, int it,
+                                      const unsigned *code, const double *prev_p0, int it,
                                       bool write_vtof, const bool *alive,
                                       unsigned long long *dmax, unsigned *uf) {
   using A = Ar<T>;
@@ -717,8 +715,21 @@ __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L
 #pragma unroll
   for (int u = 0; u < NS; ++u) {
     if (NS > 1 && !alive[u]) continue;
-    if (code[u]) sw_clamp_t<T>(code[u], a0[u], a1[u]);
-    sw_marginal_t<T>(P, L[u], v, it, a0[u], a1[u], prev_p0[u], dmax[u]);
+    double q0, q1;
+    if (sizeof(T) == sizeof(double)) {  // fp64: the message prefix IS the row product
+      q0 = (double)a0[u];
+      q1 = (double)a1[u];
+    } else {  // fp32: the row product in fp64 from the fp32 messages
+      q0 = 1.0;
+      q1 = 1.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        q0 = mul(q0, (double)x0[u][k]);
+        q1 = mul(q1, (double)x1[u][k]);
+      }
+    }
+    if (code[u]) sw_clamp(code[u], q0, q1);
+    sw_marginal_d(P, L[u].p0 + v * 32, L[u].s, v, it, q0, q1, prev_p0[u], dmax[u]);
   }
 }
 
@@ -726,7 +737,7 @@ __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L
 template <bool NORM, typename T>
 __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &L, int v,
                                         const typename Ar<T>::T2 *x, int d, const int *tw,
-                                        unsigned code, T prev_p0, int it, bool write_vtof,
+                                        unsigned code, double prev_p0, int it, bool write_vtof,
                                         unsigned long long &dmax, unsigned &uf) {
   using A = Ar<T>;
   using T2 = typename A::T2;
@@ -750,14 +761,14 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &
       L.vtof[t * 32] = A::make2(b0, b1);
     }
   }
-  T q0 = T(1), q1 = T(1);
+  double q0 = 1.0, q1 = 1.0;
   for (int k = 0; k < d; ++k) {
     const T2 m = x[k * 32];
-    q0 = A::mul(q0, m.x);
-    q1 = A::mul(q1, m.y);
+    q0 = mul(q0, (double)m.x);
+    q1 = mul(q1, (double)m.y);
   }
-  if (code) sw_clamp_t<T>(code, q0, q1);
-  sw_marginal_t<T>(P, L, v, it, q0, q1, prev_p0, dmax);
+  if (code) sw_clamp(code, q0, q1);
+  sw_marginal_d(P, L.p0 + v * 32, L.s, v, it, q0, q1, prev_p0, dmax);
 }
 
 template <bool NORM, typename T>
@@ -895,7 +906,7 @@ __device__ __forceinline__ void ws_fac_k(const SwLaneT<T> *L, const typename Ar<
 template <int NS, bool NORM, typename T>
 __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLaneT<T> *L, int v,
                                         const typename Ar<T>::T2 *const *x, int d, const int *tw,
-                                        const unsigned *code, const T *prev_p0, int it,
+                                        const unsigned *code, const double *prev_p0, int it,
                                         bool write_vtof, const bool *alive,
                                         unsigned long long *dmax, unsigned *uf) {
   switch (d) {
@@ -976,7 +987,7 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufsT<T
       const unsigned b_rp = (rp_hi - rp_lo) * 4;
       const unsigned b_tw = heavy ? 0u : (unsigned)(tw_hi - tw_lo) * 4;
       const unsigned b_msg = (heavy || !want_msg) ? 0u : (unsigned)(r1 - r0) * 32 * sizeof(typename Ar<T>::T2);
-      const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 32 * sizeof(T) : 0u;
+      const unsigned b_p0 = (side == 0 && want_p0) ? (unsigned)m * 256 : 0u;
       const unsigned b_ev = side == 0 ? (unsigned)m * 32 : 0u;
       const unsigned b_fp = side == 1 ? (unsigned)m * 16 : 0u;
       mbar_expect_tx(&sh.full[slot], b_rp + b_tw + b_fp + NS * (b_msg + b_p0 + b_ev));
@@ -1083,11 +1094,11 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
         const int r = ch.rp[v - rp_lo];
         const int d = ch.rp[v + 1 - rp_lo] - r;
         unsigned code[NS];
-        T prev_p0[NS];
+        double prev_p0[NS];
 #pragma unroll
         for (int u = 0; u < NS; ++u) {
           code[u] = ch.ev[u][v - n0][lane];
-          prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : T(0.5);
+          prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : 0.5;
         }
         if (ch.heavy) {
 #pragma unroll
@@ -1167,7 +1178,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   SwBufsT<T> B;
   B.ftov = (T2 *)P.ftov;
   B.vtof = (T2 *)P.vtof;
-  B.p0 = (T *)P.p0;
+  B.p0 = P.p0;
   B.ev = const_cast<unsigned char *>(P.ev);
   B.parity = 0;
   SwLaneT<T> L[NS];
@@ -1304,7 +1315,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         const int o = n2o[k];
         const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
         const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
-        ((T *)P.p0_alt)[dst] = B.p0[src];
+        P.p0_alt[dst] = B.p0[src];
         P.ev_alt[dst] = B.ev[src];
       }
     }
@@ -1314,7 +1325,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     T2 *nv = B.ftov;  // holds the packed vtof rows
     B.ftov = B.vtof;
     B.vtof = nv;
-    B.p0 = (T *)P.p0_alt;
+    B.p0 = P.p0_alt;
     B.ev = P.ev_alt;
     B.parity = 1;
     compacted = true;
@@ -1977,12 +1988,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     if (out->marginals) {
       double *dst = marg_dev ? out->marginals : stage_marg;
       const int bbase = marg_dev ? base : 0;
-      if (fp32)
-        hbp::sweep_marginals_kernel<float><<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
-            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V,
-            L.V, ns, bbase, dst, nullptr);
-      else
-        hbp::sweep_marginals_kernel<double><<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
+      hbp::sweep_marginals_kernel<double><<<dim3((L.V + 31) / 32, groups), 256, 0, st>>>(
             sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, nullptr, L.V, L.V, ns, bbase, dst, nullptr);
       ++launches;
       if (!marg_dev)
@@ -1992,12 +1998,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     if (out->p1_select && nsel) {
       double *dst = p1_dev ? out->p1_select : stage_p1;
       const int bbase = p1_dev ? base : 0;
-      if (fp32)
-        hbp::sweep_marginals_kernel<float><<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
-            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel,
-            L.V, ns, bbase, nullptr, dst);
-      else
-        hbp::sweep_marginals_kernel<double><<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
+      hbp::sweep_marginals_kernel<double><<<dim3((nsel + 31) / 32, groups), 256, 0, st>>>(
             sw->d_p0, sw->d_p0_alt, d_rpos, sw->d_vinv, d_sel, nsel, L.V, ns, bbase, nullptr, dst);
       ++launches;
       if (!p1_dev)
@@ -2011,15 +2012,8 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       if (smem > 48 * 1024) {
         HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel<double>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel<float>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       }
-      if (fp32)
-        hbp::sweep_rank_kernel<float><<<ns, 1024, smem, st>>>(
-            (const float *)sw->d_p0, (const float *)sw->d_p0_alt, sw->d_ev, sw->d_ev_alt, d_rpos,
-            sw->d_vinv, d_sel, nsel, std::max(npow2, 2), L.V, bbase, out->topk, dst);
-      else
-        hbp::sweep_rank_kernel<double><<<ns, 1024, smem, st>>>(
+      hbp::sweep_rank_kernel<double><<<ns, 1024, smem, st>>>(
             sw->d_p0, sw->d_p0_alt, sw->d_ev, sw->d_ev_alt, d_rpos, sw->d_vinv, d_sel, nsel,
             std::max(npow2, 2), L.V, bbase, out->topk, dst);
       ++launches;
