@@ -537,17 +537,17 @@ __device__ __forceinline__ SwLaneT<T> sw_lane_bt(const SwBufsT<T> &B, int slot, 
   return L;
 }
 
-template <typename T>
-__device__ __forceinline__ void sw_clamp_t(unsigned code, T &a0, T &a1) {
-  using A = Ar<T>;
-  if (code & 1u) {  // observed false: (1, 0)
-    a0 = A::mul(a0, T(1));
-    a1 = A::mul(a1, T(0));
-  }
-  if (code & 2u) {  // observed true: (0, 1)
-    a0 = A::mul(a0, T(0));
-    a1 = A::mul(a1, T(1));
-  }
+// message loads / stores of the staged kernel: arithmetic is always fp64 (the
+// bitwise contract); the fp32 mode only stores messages as float (one
+// rounding per stored message) and widens them back on load
+__device__ __forceinline__ double2 ld2(const double2 *p) { return *p; }
+__device__ __forceinline__ double2 ld2(const float2 *p) {
+  const float2 v = *p;
+  return make_double2((double)v.x, (double)v.y);
+}
+__device__ __forceinline__ void st2(double2 *p, double a, double b) { *p = make_double2(a, b); }
+__device__ __forceinline__ void st2(float2 *p, double a, double b) {
+  *p = make_float2(__double2float_rn(a), __double2float_rn(b));
 }
 
 // marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572),
@@ -671,128 +671,108 @@ __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L
                                       const unsigned *code, const double *prev_p0, int it,
                                       bool write_vtof, const bool *alive,
                                       unsigned long long *dmax, unsigned *uf) {
-  using A = Ar<T>;
-  using T2 = typename A::T2;
-  T x0[NS][D], x1[NS][D];
+  double x0[NS][D], x1[NS][D];
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const T2 m = x[u][k * 32];
+      const double2 m = ld2(x[u] + k * 32);
       x0[u][k] = m.x;
       x1[u][k] = m.y;
     }
-  T a0[NS], a1[NS];
+  double a0[NS], a1[NS];
 #pragma unroll
-  for (int u = 0; u < NS; ++u) a0[u] = a1[u] = T(1);
+  for (int u = 0; u < NS; ++u) a0[u] = a1[u] = 1.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     const unsigned t = (unsigned)tw[j];
     if (write_vtof && !(t & kUnaryBit)) {
 #pragma unroll
       for (int u = 0; u < NS; ++u) {
-        T b0 = a0[u], b1 = a1[u];
+        double b0 = a0[u], b1 = a1[u];
 #pragma unroll
         for (int k = j + 1; k < D; ++k) {
-          b0 = A::mul(b0, x0[u][k]);
-          b1 = A::mul(b1, x1[u][k]);
+          b0 = mul(b0, x0[u][k]);
+          b1 = mul(b1, x1[u][k]);
         }
-        if (code[u]) sw_clamp_t<T>(code[u], b0, b1);
+        if (code[u]) sw_clamp(code[u], b0, b1);
         if (NORM) {
-          const T tt = A::add(b0, b1);
-          uf[u] = tt < A::min_sum ? t + 1 : uf[u];  // last underflowing slot + 1 (rare)
-          A::div2(b0, b1, tt, b0, b1);
+          const double tt = add(b0, b1);
+          uf[u] = tt < kMinMessageSum ? t + 1 : uf[u];  // last underflowing slot + 1 (rare)
+          div2_rn(b0, b1, tt, b0, b1);
         }
-        if (NS == 1 || alive[u]) L[u].vtof[t * 32] = A::make2(b0, b1);
+        if (NS == 1 || alive[u]) st2(L[u].vtof + t * 32, b0, b1);
       }
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
-      a0[u] = A::mul(a0[u], x0[u][j]);
-      a1[u] = A::mul(a1[u], x1[u][j]);
+      a0[u] = mul(a0[u], x0[u][j]);
+      a1[u] = mul(a1[u], x1[u][j]);
     }
   }
 #pragma unroll
   for (int u = 0; u < NS; ++u) {
     if (NS > 1 && !alive[u]) continue;
-    double q0, q1;
-    if (sizeof(T) == sizeof(double)) {  // fp64: the message prefix IS the row product
-      q0 = (double)a0[u];
-      q1 = (double)a1[u];
-    } else {  // fp32: the row product in fp64 from the fp32 messages
-      q0 = 1.0;
-      q1 = 1.0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        q0 = mul(q0, (double)x0[u][k]);
-        q1 = mul(q1, (double)x1[u][k]);
-      }
-    }
-    if (code[u]) sw_clamp(code[u], q0, q1);
-    sw_marginal_d(P, L[u].p0 + v * 32, L[u].s, v, it, q0, q1, prev_p0[u], dmax[u]);
+    if (code[u]) sw_clamp(code[u], a0[u], a1[u]);
+    sw_marginal_d(P, L[u].p0 + v * 32, L[u].s, v, it, a0[u], a1[u], prev_p0[u], dmax[u]);
   }
 }
 
 // any degree, one set, rows re-read per target (heavy nodes: global memory)
 template <bool NORM, typename T>
 __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &L, int v,
-                                        const typename Ar<T>::T2 *x, int d, const int *tw,
-                                        unsigned code, double prev_p0, int it, bool write_vtof,
+                                        const typename Ar<T>::T2 *x, int d, const int *tw, unsigned code,
+                                        double prev_p0, int it, bool write_vtof,
                                         unsigned long long &dmax, unsigned &uf) {
-  using A = Ar<T>;
-  using T2 = typename A::T2;
   if (write_vtof) {
     for (int j = 0; j < d; ++j) {
       const unsigned t = (unsigned)tw[j];
       if (t & kUnaryBit) continue;
-      T b0 = T(1), b1 = T(1);
+      double b0 = 1.0, b1 = 1.0;
       for (int k = 0; k < d; ++k) {
         if (k == j) continue;
-        const T2 m = x[k * 32];
-        b0 = A::mul(b0, m.x);
-        b1 = A::mul(b1, m.y);
+        const double2 m = ld2(x + k * 32);
+        b0 = mul(b0, m.x);
+        b1 = mul(b1, m.y);
       }
-      if (code) sw_clamp_t<T>(code, b0, b1);
+      if (code) sw_clamp(code, b0, b1);
       if (NORM) {
-        const T tt = A::add(b0, b1);
-        uf = tt < A::min_sum ? t + 1 : uf;
-        A::div2(b0, b1, tt, b0, b1);
+        const double tt = add(b0, b1);
+        uf = tt < kMinMessageSum ? t + 1 : uf;
+        div2_rn(b0, b1, tt, b0, b1);
       }
-      L.vtof[t * 32] = A::make2(b0, b1);
+      st2(L.vtof + t * 32, b0, b1);
     }
   }
   double q0 = 1.0, q1 = 1.0;
   for (int k = 0; k < d; ++k) {
-    const T2 m = x[k * 32];
-    q0 = mul(q0, (double)m.x);
-    q1 = mul(q1, (double)m.y);
+    const double2 m = ld2(x + k * 32);
+    q0 = mul(q0, m.x);
+    q1 = mul(q1, m.y);
   }
   if (code) sw_clamp(code, q0, q1);
   sw_marginal_d(P, L.p0 + v * 32, L.s, v, it, q0, q1, prev_p0, dmax);
 }
 
 template <bool NORM, typename T>
-__device__ __forceinline__ void ws_put(const SwLaneT<T> &L, int t, T o0, T o1, unsigned &uf,
+__device__ __forceinline__ void ws_put(const SwLaneT<T> &L, int t, double o0, double o1, unsigned &uf,
                                       bool store) {
-  using A = Ar<T>;
   if (NORM) {
-    const T tt = A::add(o0, o1);
-    uf = tt < A::min_sum ? (unsigned)t + 1 : uf;
-    A::div2(o0, o1, tt, o0, o1);
+    const double tt = add(o0, o1);
+    uf = tt < kMinMessageSum ? (unsigned)t + 1 : uf;
+    div2_rn(o0, o1, tt, o0, o1);
   }
-  if (store) L.ftov[t * 32] = A::make2(o0, o1);
+  if (store) st2(L.ftov + t * 32, o0, o1);
 }
 
 // Factor node of degree D for NS sets; FIRST: iteration 1 (every vtof message
 // is the uniform one, so nothing is read).
 template <int D, int KIND, int NS, bool NORM, bool FIRST, typename T>
 __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>::T2 *const *x,
-                                      const int *tw, typename Ar<T>::T2 pp, const bool *alive,
-                                      unsigned *uf) {
-  using A = Ar<T>;
-  using T2 = typename A::T2;
-  T m0[NS][D], m1[NS][D];
-  const T c = NORM ? T(0.5) : T(1);
+                                      const int *tw,
+                                      double2 pp, const bool *alive, unsigned *uf) {
+  double m0[NS][D], m1[NS][D];
+  const double c = NORM ? 0.5 : 1.0;
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
@@ -801,47 +781,47 @@ __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>
         m0[u][k] = c;
         m1[u][k] = c;
       } else {
-        const T2 m = x[u][k * 32];
+        const double2 m = ld2(x[u] + k * 32);
         m0[u][k] = m.x;
         m1[u][k] = m.y;
       }
     }
-  T sm[NS][D];
+  double sm[NS][D];
 #pragma unroll
   for (int u = 0; u < NS; ++u)
 #pragma unroll
-    for (int k = 1; k < D; ++k) sm[u][k] = A::add(m0[u][k], m1[u][k]);
+    for (int k = 1; k < D; ++k) sm[u][k] = add(m0[u][k], m1[u][k]);
 #pragma unroll
   for (int u = 0; u < NS; ++u) {
-    T h1 = T(1), h2 = T(1);
+    double h1 = 1.0, h2 = 1.0;
 #pragma unroll
     for (int k = 1; k < D; ++k) {
-      h1 = A::mul(h1, sm[u][k]);
-      h2 = A::mul(h2, KIND == 0 ? m1[u][k] : m0[u][k]);
+      h1 = mul(h1, sm[u][k]);
+      h2 = mul(h2, KIND == 0 ? m1[u][k] : m0[u][k]);
     }
-    T o0, o1;
-    head_message_t<KIND, T>(pp.x, pp.y, h1, h2, o0, o1);
+    double o0, o1;
+    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
     ws_put<NORM, T>(L[u], tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
   }
   if (D > 1) {
-    T a1[NS], a2[NS];
+    double a1[NS], a2[NS];
 #pragma unroll
-    for (int u = 0; u < NS; ++u) head_slot_terms_t<KIND, T>(pp.x, pp.y, m0[u][0], m1[u][0], a1[u], a2[u]);
+    for (int u = 0; u < NS; ++u) head_slot_terms<KIND>(pp.x, pp.y, m0[u][0], m1[u][0], a1[u], a2[u]);
 #pragma unroll
     for (int j = 1; j < D; ++j) {
 #pragma unroll
       for (int u = 0; u < NS; ++u) {
-        T b1 = a1[u], b2 = a2[u];
+        double b1 = a1[u], b2 = a2[u];
 #pragma unroll
         for (int k = j + 1; k < D; ++k) {
-          b1 = A::mul(b1, sm[u][k]);
-          b2 = A::mul(b2, KIND == 0 ? m1[u][k] : m0[u][k]);
+          b1 = mul(b1, sm[u][k]);
+          b2 = mul(b2, KIND == 0 ? m1[u][k] : m0[u][k]);
         }
-        T o0, o1;
-        body_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
+        double o0, o1;
+        body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
         ws_put<NORM, T>(L[u], tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
-        a1[u] = A::mul(a1[u], sm[u][j]);
-        a2[u] = A::mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
+        a1[u] = mul(a1[u], sm[u][j]);
+        a2[u] = mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
       }
     }
   }
@@ -849,39 +829,37 @@ __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>
 
 template <int KIND, bool NORM, bool FIRST, typename T>
 __device__ __noinline__ void ws_fac_any(const SwLaneT<T> &L, const typename Ar<T>::T2 *x, int d,
-                                        const int *tw, typename Ar<T>::T2 pp, unsigned &uf) {
-  using A = Ar<T>;
-  using T2 = typename A::T2;
-  const T c = NORM ? T(0.5) : T(1);
+                                        const int *tw,
+                                        double2 pp, unsigned &uf) {
+  const double c = NORM ? 0.5 : 1.0;
   for (int j = 0; j < d; ++j) {
-    T b1 = T(1), b2 = T(1);
+    double b1 = 1.0, b2 = 1.0;
     for (int k = 0; k < d; ++k) {
       if (k == j) continue;
-      const T2 m = FIRST ? A::make2(c, c) : x[k * 32];
-      T f1, f2;
+      const double2 m = FIRST ? make_double2(c, c) : ld2(x + k * 32);
+      double f1, f2;
       if (k == 0) {
-        head_slot_terms_t<KIND, T>(pp.x, pp.y, m.x, m.y, f1, f2);
+        head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
       } else {
-        f1 = A::add(m.x, m.y);
+        f1 = add(m.x, m.y);
         f2 = KIND == 0 ? m.y : m.x;
       }
-      b1 = A::mul(b1, f1);
-      b2 = A::mul(b2, f2);
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
     }
-    T o0, o1;
+    double o0, o1;
     if (j == 0)
-      head_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
+      head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
     else
-      body_message_t<KIND, T>(pp.x, pp.y, b1, b2, o0, o1);
+      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
     ws_put<NORM, T>(L, tw[j], o0, o1, uf, true);
   }
 }
 
 // degree dispatch; NS = 2 keeps the register path to degree 4 (two sets of rows)
 template <int KIND, int NS, bool NORM, bool FIRST, typename T>
-__device__ __forceinline__ void ws_fac_k(const SwLaneT<T> *L, const typename Ar<T>::T2 *const *x,
-                                        int d, const int *tw, typename Ar<T>::T2 pp,
-                                        const bool *alive,
+__device__ __forceinline__ void ws_fac_k(const SwLaneT<T> *L, const typename Ar<T>::T2 *const *x, int d,
+                                        const int *tw, double2 pp, const bool *alive,
                                         unsigned *uf) {
   switch (d) {
     case 1: ws_fac<1, KIND, NS, NORM, FIRST, T>(L, x, tw, pp, alive, uf); break;
@@ -1036,8 +1014,7 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
         const int d = ch.rp[f + 1 - rp_lo] - r;
         // unary: a constant message, written in iteration 1 (and again after a compaction)
         if (!FIRST && !unary && d == 1) continue;
-        const double2 ppd = ch.fpar[f - n0];
-        const typename Ar<T>::T2 pp = Ar<T>::make2((T)ppd.x, (T)ppd.y);
+        const double2 pp = ch.fpar[f - n0];
         const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
         if (ch.heavy) {
           // rows not staged: twins and messages from global memory
