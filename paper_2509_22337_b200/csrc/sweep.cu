@@ -1465,7 +1465,7 @@ __global__ void sweep_marginals_kernel(const T *p0, const T *p0_alt, const int *
     const int s = s0 + r, k = k0 + tx;
     if (k < nsel && s < nsets) {
       const T q = tile[tx][r];
-      const double p1 = (double)Ar<T>::sub(T(1), q);  // P1 = 1 - P0 in the run's precision
+      const double p1 = sub(1.0, (double)q);  // P1 = 1 - P0 (engine.py:520-522)
       const size_t o = (size_t)(set_base + s) * nsel + k;
       if (out_pair) {
         out_pair[2 * o] = (double)q;
@@ -1498,7 +1498,7 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *
       int par;
       const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
       if ((par ? ev_alt : ev)[at] == 0) {
-        const double p1 = (double)Ar<T>::sub(T(1), (par ? p0_alt : p0)[at]);
+        const double p1 = sub(1.0, (double)(par ? p0_alt : p0)[at]);
         k = ~(unsigned long long)__double_as_longlong(p1);
       }
     }
