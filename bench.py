@@ -420,12 +420,32 @@ def run_ours_sweep(args) -> None:
         line["cpu_baseline"] = {"value": u / s, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"sets 0..{len(sample) - 1}, one per core, C oracle "
                                           "single-threaded runs (clamp + PARALL compile + run)"}
+        line["fp32_mode"] = measure_fp32(P, g, sets, sel, p1.cpu().numpy(), rk.cpu().numpy())
         line["single_graph"] = measure_single(torch, "c4", steps=20, warmup=5)
         line["interaction_loop"] = measure_loop(g, alarms, cores)
     print(json.dumps(line), flush=True)
     if multi:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---- optional fp32 mode ------------------------------------------------
+
+def measure_fp32(P, g, sets, sel, p1_64, rk_64) -> dict:
+    """The same sweep with fp32 message storage (fp64 arithmetic and
+    marginals), against this run's fp64 outputs: north-star bar 1e-5."""
+    opts = P.EngineOptions(1000, 1e-9, precision="fp32")
+    P.run_many(g, sets[:64], None, opts, marginals=False, deltas=False)
+    ks, last = [], None
+    for _ in range(3):
+        last = P.run_many(g, sets, None, opts, marginals=False, deltas=False, select=sel, topk=TOPK)
+        ks.append(last.kernel_ms)
+    k = min(ks)
+    return {"value": last.total_updates() / (k * 1e-3), "unit": UNIT, "kernel_ms": k,
+            "dtype": "f32 messages, f64 arithmetic and marginals",
+            "max_abs_p1_diff_vs_f64": float(np.abs(last.p1_select - p1_64).max()),
+            "top100_identical_sets": int((last.ranked == rk_64).all(axis=1).sum()),
+            "sets": len(sets)}
 
 
 # ---- device-resident interaction loop (SURVEY.md 8(f) F1) ------------------------------------
