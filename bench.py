@@ -386,7 +386,7 @@ def run_ours_sweep(args) -> None:
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
-        if tj.get("kernel") == "sweep_persistent" and tj.get("sets") == m:
+        if tj.get("kernel") == "sweep_ws" and tj.get("sets") == m:
             traffic = float(tj["dram_bytes_per_launch"])
     except (OSError, KeyError, ValueError):
         pass
@@ -407,7 +407,7 @@ def run_ours_sweep(args) -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}), burst copy",
-                     "kernel": "hbp::sweep_persistent (rank 0's whole slice in one launch)",
+                     "kernel": "hbp::sweep_ws<1,1> (rank 0's whole slice in one launch)",
                      "bytes_per_launch": bytes_launch, "sets_per_launch": m,
                      "kernel_ms": statistics.mean(kernel_ms)},
         "clocks": clk.summary(),

@@ -205,7 +205,8 @@ def test_sweep_ftp_many_sets_vs_oracle():
 @pytest.mark.parametrize("name,n", [("hedc", 64), ("ftp", 16)])
 def test_sweep_fp32_mode_within_1e5_of_fp64(name, n):
     """Optional fp32 mode (north star: marginals within 1e-5 of the fp64
-    reference): float messages / marginals in the same staged kernel."""
+    reference): fp32 message storage, fp64 arithmetic and marginals, in the
+    same staged kernel."""
     g, alarms = W.graph(name)
     sets = [W.evidence_set(alarms, j, size=min(8, len(alarms))) for j in range(n)]
     opts64 = EngineOptions(1000, 1e-9)
