@@ -178,6 +178,11 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
  * reference order (rowptr_ftov [V+1], ftov_to_vtof [E]). */
 hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to_vtof);
 
+/* Self-check of the device-built layout (hbp_graph_create builds it with
+ * kernels): every device array against the host builder's, *mismatches = the
+ * number of arrays that differ (0 expected). */
+hbp_status hbp_graph_layout_check(hbp_graph *g, int64_t *mismatches);
+
 /* Self-test of the shared-reciprocal division against __ddiv_rn on the device:
  * q_fast/q_ref [2n]: a[i]/b[i] and a[(i+1)%n]/b[i]. */
 hbp_status hbp_selftest_division(int64_t n, const double *a, const double *b, double *q_fast,

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhbp.so")
 
-SOURCES = ["engine.cu", "sweep.cu", "layout.cpp", "compiler.cpp", "capi.cpp"]
+SOURCES = ["engine.cu", "sweep.cu", "layout_dev.cu", "layout.cpp", "compiler.cpp", "capi.cpp"]
 HEADERS = ["internal.h", "device.h", "lbp_kernels.cuh", os.path.join("..", "..", "include", "hornbp_gpu.h")]
 
 NVCC_FLAGS = [

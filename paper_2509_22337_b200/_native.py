@@ -148,6 +148,7 @@ def lib() -> C.CDLL:
             "hbp_graph_set_evidence": (C.c_int32, [vp, C.c_int32, i32p, i8p]),
             "hbp_graph_rank": (C.c_int32, [vp, C.c_int32, i32p, C.c_int32, i32p, f64p]),
             "hbp_graph_layout": (C.c_int32, [vp, i64p, i64p]),
+            "hbp_graph_layout_check": (C.c_int32, [vp, i64p]),
             "hbp_plan_create": (C.c_int32, [vp, C.c_int64, i64p, i32p, i64p, i32p, C.POINTER(vp)]),
             "hbp_plan_destroy": (None, [vp]),
             "hbp_run": (C.c_int32, [vp, C.POINTER(Options), f64p, f64p, f64p, C.POINTER(Result)]),
@@ -176,7 +177,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ("hbp_compile", "hbp_toposort", "hbp_schedule_sizes", "hbp_schedule_copy",
             "hbp_schedule_destroy", "hbp_graph_create", "hbp_graph_destroy", "hbp_graph_set_stream", "hbp_graph_set_evidence",
-            "hbp_graph_rank", "hbp_graph_layout",
+            "hbp_graph_rank", "hbp_graph_layout", "hbp_graph_layout_check",
             "hbp_plan_create", "hbp_plan_destroy", "hbp_run", "hbp_run_device", "hbp_pass",
             "hbp_marginals", "hbp_sweep_create", "hbp_sweep_capacity", "hbp_sweep_run",
             "hbp_sweep_destroy", "hbp_last_launch_count", "hbp_selftest_division", "hbp_last_error",

@@ -49,6 +49,17 @@ struct hbp_graph {
   int2 *d_vslot = nullptr, *d_fslot = nullptr;
   double2 *d_fpar = nullptr, *d_vtof = nullptr, *d_ftov = nullptr, *d_marg = nullptr;
   double *d_prev = nullptr;
+  // one allocation for everything below up to d_canon2v, plus the layout
+  // build's scratch (reused by the PARALL shape test of hbp_plan_create)
+  void *d_block = nullptr;
+  void *d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // canonical graph arrays (the device layout build's input; the lazy host
+  // layout downloads them) and canonical edge -> internal vtof position
+  int64_t *d_rowptr = nullptr;
+  int *d_evar = nullptr, *d_canon2v = nullptr;
+  int8_t *d_kind = nullptr;
+  double *d_p1 = nullptr, *d_p2 = nullptr;
   // evidence (clamp_evidence without a graph rebuild) + ranking scratch
   unsigned char *d_ev = nullptr;
   bool has_ev = false;
@@ -68,16 +79,23 @@ struct hbp_graph {
 
   ~hbp_graph() {
     cudaSetDevice(device);
-    for (void *p : {(void *)d_vslot, (void *)d_vtof_twin, (void *)d_fslot, (void *)d_ftov_twin,
-                    (void *)d_vorig, (void *)d_fpar, (void *)d_vtof, (void *)d_ftov,
-                    (void *)d_marg, (void *)d_prev, (void *)d_ev, (void *)d_vinv, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace,
-                    (void *)d_vrow, (void *)d_frow})
+    // the layout, message buffers and layout scratch live in d_block
+    for (void *p : {d_block, (void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
+
+namespace hbp {
+// layout_dev.cu: the device layout build (hbp_graph_create), the host layout
+// on first host-side use, and the PARALL shape test of a one-batch schedule
+hbp_status build_layout_device(const hbp_graph_desc &desc, hbp_graph *g);
+hbp_status ensure_host_layout(hbp_graph *g);
+hbp_status parall_check_device(hbp_graph *g, int64_t ns, const int32_t *s_edges, int64_t nt,
+                               const int32_t *t_edges, bool *is_parall);
+}  // namespace hbp
 
 struct hbp_plan {
   hbp_graph *g = nullptr;

@@ -1091,8 +1091,7 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   *out = nullptr;
   std::unique_ptr<hbp_graph> g(new (std::nothrow) hbp_graph());
   if (!g) return HBP_ENOMEM;
-  hbp_status st = hbp::build_layout(*desc, g->L);
-  if (st != HBP_OK) return st;
+  hbp_status st;
   g->device = device;
   HBP_CUDA(cudaSetDevice(device));
   HBP_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
@@ -1147,23 +1146,11 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
       }
     }
   }
-  const hbp::HostLayout &L = g->L;
-  cudaStream_t s = g->stream;
-  std::vector<double2> fpar((size_t)L.F);
-  for (int32_t i = 0; i < L.F; ++i) fpar[i] = make_double2(L.p1[L.fperm[i]], L.p2[L.fperm[i]]);
-  std::vector<int2> vslot((size_t)L.E), fslot((size_t)L.E);
-  std::memcpy(vslot.data(), L.vslot.data(), (size_t)L.E * 8);
-  std::memcpy(fslot.data(), L.fslot.data(), (size_t)L.E * 8);
-  if ((st = upload(&g->d_vrow, L.vrow, s)) || (st = upload(&g->d_frow, L.frow, s)) ||
-      (st = upload(&g->d_vslot, vslot, s)) || (st = upload(&g->d_vtof_twin, L.vtof_twin, s)) ||
-      (st = upload(&g->d_fslot, fslot, s)) || (st = upload(&g->d_ftov_twin, L.ftov_twin, s)) ||
-      (st = upload(&g->d_vorig, L.vperm, s)) || (st = upload(&g->d_fpar, fpar, s)))
-    return st;
-  HBP_CUDA(cudaMalloc(&g->d_vtof, (size_t)L.E * sizeof(double2)));
-  HBP_CUDA(cudaMalloc(&g->d_ftov, (size_t)L.E * sizeof(double2)));
-  HBP_CUDA(cudaMalloc(&g->d_marg, (size_t)std::max(1, L.V) * sizeof(double2)));
-  HBP_CUDA(cudaMalloc(&g->d_prev, (size_t)std::max(1, L.V) * sizeof(double)));
-  HBP_CUDA(cudaStreamSynchronize(s));
+  // the layout is built on the device (layout_dev.cu); the host copy of it
+  // only when a host-side consumer needs it (hbp::ensure_host_layout)
+  hbp::set_last_launches(0);
+  if ((st = hbp::build_layout_device(*desc, g.get())) != HBP_OK) return st;
+  HBP_CUDA(cudaStreamSynchronize(g->stream));
   *out = g.release();
   return HBP_OK;
 }
@@ -1181,6 +1168,8 @@ hbp_status hbp_graph_set_stream(hbp_graph *g, void *stream) {
 
 hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to_vtof) {
   // reference layout (storage.py:55-63) recomputed from the device-side maps
+  hbp_status st = hbp::ensure_host_layout(g);
+  if (st != HBP_OK) return st;
   const hbp::HostLayout &L = g->L;
   std::vector<int64_t> cnt((size_t)L.V + 1, 0);
   for (int64_t e = 0; e < L.E; ++e) cnt[(size_t)L.edge_var[e] + 1]++;
@@ -1207,9 +1196,21 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   p->g = g;
   // levels smaller than two items per thread of cluster 0 run on cluster 0 only
   const int32_t small = g->csize > 1 ? 2 * g->csize * g->threads : 3072;
-  hbp_status st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small);
-  if (st != HBP_OK) return st;
   HBP_CUDA(cudaSetDevice(g->device));
+  hbp_status st;
+  bool parall = false;
+  // a one-batch schedule of PARALL shape is recognised on the device and
+  // needs no host layout; anything else is planned by the host builder
+  if (k == 1 && s_off && t_off && s_off[0] == 0 && t_off[0] == 0 && s_off[1] >= 0 && t_off[1] >= 0 &&
+      (st = hbp::parall_check_device(g, s_off[1], s_edges, t_off[1], t_edges, &parall)) != HBP_OK)
+    return st;
+  if (parall) {
+    hbp::parall_plan(g->L, s_off[1], t_off[1], p->host, small);
+  } else {
+    if ((st = hbp::ensure_host_layout(g)) != HBP_OK) return st;
+    if ((st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small)) != HBP_OK)
+      return st;
+  }
   cudaStream_t s = g->stream;
   if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)))
     return st;
@@ -1356,6 +1357,8 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
       const int kind = (int)((where >> 32) & 1);
       const int32_t pos = (int32_t)(where & 0xFFFFFFFFu);
       res->underflow_kind = kind == 0 ? 1 : 2;
+      hbp_status hs = hbp::ensure_host_layout(g);
+      if (hs != HBP_OK) return hs;
       res->underflow_index = kind == 0 ? g->L.vtof2canon[pos] : g->L.ftov2canon[pos];
     } else {
       res->underflow_kind = 3;
@@ -1413,6 +1416,8 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
     hbp::set_error("null argument");
     return HBP_EINVAL;
   }
+  hbp_status hs = hbp::ensure_host_layout(g);
+  if (hs != HBP_OK) return hs;
   const hbp::HostLayout &L = g->L;
   if (underflow_index) *underflow_index = -1;
   if (n == 0) return HBP_OK;
@@ -1496,6 +1501,8 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
     hbp::set_error("null argument");
     return HBP_EINVAL;
   }
+  hbp_status hs = hbp::ensure_host_layout(g);
+  if (hs != HBP_OK) return hs;
   const hbp::HostLayout &L = g->L;
   if (underflow_var) *underflow_var = -1;
   HBP_CUDA(cudaSetDevice(g->device));
@@ -1556,8 +1563,6 @@ hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var,
   }
   HBP_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
-  hbp_status st;
-  if (!g->d_vinv && (st = upload(&g->d_vinv, L.vinv, s))) return st;
   if (!g->d_ev) HBP_CUDA(cudaMalloc(&g->d_ev, (size_t)L.V + 4));
   HBP_CUDA(cudaMemsetAsync(g->d_ev, 0, (size_t)L.V + 4, s));
   g->has_ev = n > 0;
@@ -1601,8 +1606,6 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
   }
   HBP_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
-  hbp_status st;
-  if (!g->d_vinv && (st = upload(&g->d_vinv, L.vinv, s))) return st;
   const size_t need = (size_t)num_select * 4 + (size_t)topk * 12 + 64;
   if (g->rank_cap < need) {
     if (g->d_rank) cudaFree(g->d_rank);

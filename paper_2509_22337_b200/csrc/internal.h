@@ -92,6 +92,11 @@ struct HostLayout {
   // [light AND | light OR | heavy AND | heavy OR]
   int32_t f_or_light = 0, f_heavy = 0, f_or_heavy = 0;
   int32_t v_heavy = 0;  // internal variables >= this have degree > kNodeMax
+  int32_t vrow_heavy = 0, frow_heavy = 0;  // vrow[v_heavy], frow[f_heavy]
+  int64_t n_unary = 0;                     // factors of degree 1
+  // false: only the scalars above are set (the device built the arrays);
+  // ensure_host_layout fills the vectors on first host-side use
+  bool host_ready = false;
   bool factor_is_or(int32_t fi) const {
     return (fi >= f_or_light && fi < f_heavy) || fi >= f_or_heavy;
   }
@@ -111,6 +116,12 @@ struct PlanHost {
   int64_t updates_per_iter = 0;        // sum |s_i| + |t_i|
   int32_t max_items = 0;               // largest phase (work items)
 };
+
+// the two whole-graph phases of a PARALL schedule (every edge once on the
+// factor side, every non-unary slot once on the variable side), from the
+// layout's scalars alone
+void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
+                 int32_t small_threshold);
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,

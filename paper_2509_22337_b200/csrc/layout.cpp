@@ -58,6 +58,8 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
       return HBP_EINVAL;
     }
   L.max_fdeg = maxdeg;
+  L.n_unary = 0;
+  for (int32_t f = 0; f < F; ++f) L.n_unary += L.rowptr[f + 1] - L.rowptr[f] == 1;
 
   // factors: stable counting sort by (heavy, kind, degree) -> warp-uniform role
   // and trip count across consecutive ids; heavy rows form the slot tail
@@ -158,6 +160,8 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     node[0] = lo;
     rowstart[0] = row[lo];
   };
+  L.vrow_heavy = L.vrow[L.v_heavy];
+  L.frow_heavy = L.frow[L.f_heavy];
   classes(L.vrow, 0, L.v_heavy, L.vc_node, L.vc_row);
   classes(L.frow, 0, L.f_or_light, L.fa_node, L.fa_row);
   classes(L.frow, L.f_or_light, L.f_heavy, L.fo_node, L.fo_row);
@@ -200,7 +204,36 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
     const bool unary = L.rowptr[f + 1] - L.rowptr[f] == 1;
     L.ftov_twin[L.canon2f[e]] = (uint32_t)L.canon2v[e] | (unary ? kUnaryBit : 0u);
   }
+  L.host_ready = true;
   return HBP_OK;
+}
+
+void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
+                 int32_t small_threshold) {
+  P.updates_per_iter = ns + nt;
+  P.phases.clear();
+  P.items.clear();
+  Phase v{};
+  v.type = 0;
+  v.grid = 1;  // phase 0 carries the convergence test
+  v.list = 2;
+  v.marg = 1;
+  v.begin = 0;
+  v.end = L.v_heavy;
+  v.sbegin = L.vrow_heavy;
+  v.send = (int32_t)L.E;
+  Phase f{};
+  f.type = 1;
+  f.list = 2;
+  f.begin = 0;
+  f.end = L.f_heavy;
+  f.sbegin = L.frow_heavy;
+  f.send = (int32_t)L.E;
+  const int32_t nv = L.v_heavy + (v.send - v.sbegin), nf = L.f_heavy + (f.send - f.sbegin);
+  f.grid = nf >= small_threshold;  // smaller phases run on cluster 0 only
+  P.phases.push_back(v);
+  P.phases.push_back(f);
+  P.max_items = std::max(nv, nf);
 }
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
@@ -265,24 +298,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       m |= 2;
     }
     if (ok) {
-      Phase v{};
-      v.type = 0;
-      v.list = 2;
-      v.marg = 1;
-      v.begin = 0;
-      v.end = L.v_heavy;
-      v.sbegin = L.vrow[L.v_heavy];
-      v.send = (int32_t)E;
-      push_phase(v, L.v_heavy + (v.send - v.sbegin));
-      P.phases.back().grid = 1;  // phase 0 carries the convergence test
-      Phase f{};
-      f.type = 1;
-      f.list = 2;
-      f.begin = 0;
-      f.end = L.f_heavy;
-      f.sbegin = L.frow[L.f_heavy];
-      f.send = (int32_t)E;
-      push_phase(f, L.f_heavy + (f.send - f.sbegin));
+      parall_plan(L, ns, nt, P, small_threshold);
       return HBP_OK;
     }
   }

@@ -1603,6 +1603,8 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   std::unique_ptr<hbp_sweep> sw(new (std::nothrow) hbp_sweep());
   if (!sw) return HBP_ENOMEM;
   sw->g = g;
+  hbp_status hs = hbp::ensure_host_layout(g);
+  if (hs != HBP_OK) return hs;
   const hbp::HostLayout &L = g->L;
   int per_sm = 0;
   {
