@@ -40,6 +40,7 @@ using namespace dev;
 
 constexpr int kThreads = 768;  // default block size: 80 registers, fewest spills (measured best)
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
+constexpr int kChunkTrace = 16384;  // HBP_TRACE=1: per-chunk ns of iteration 3, PARALL phases 0/1
 
 struct Ctrl {
   unsigned int bar;  // grid barrier arrivals (monotonic)
@@ -196,7 +197,7 @@ __device__ __forceinline__ void apply_clamp(unsigned code, double &a0, double &a
 // is unary (PARALL range mode).
 
 // rows longer than 8 (rare): same left-to-right products, loads in groups of 4
-__device__ __noinline__ void v_row_long(const KParams &P, int r, int d, int j, bool marg,
+__device__ __forceinline__ void v_row_long(const KParams &P, int r, int d, int j, bool marg,
                                         double &a0, double &a1, double &q0, double &q1) {
   for (int base = 0; base < d; base += 4) {
     double2 m[4];
@@ -283,7 +284,7 @@ __device__ __forceinline__ bool factor_is_or(const KParams &P, int f) {
 }
 
 template <int KIND>
-__device__ __noinline__ void f_row_long(const KParams &P, int r, int d, int j, double2 pp,
+__device__ __forceinline__ void f_row_long(const KParams &P, int r, int d, int j, double2 pp,
                                         double &b1, double &b2) {
   for (int base = 0; base < d; base += 4) {
     double2 m[4];
@@ -533,6 +534,12 @@ __device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool f
 // --------------------------------------------------------------------------------------
 // one phase over its slots, grid- or CTA-strided
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, int pidx, int it,
                                            bool do_marg, bool do_vtof,
                                            unsigned long long &dmax) {
@@ -557,43 +564,60 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     const int hn = ph.send - ph.sbegin;
     const int total = nn + hn;
     // warp chunks of 32 consecutive items (coalesced rows, uniform degree)
-    // dealt round-robin over CTAs, so every SM gets the same degree mix
-    // (heavy rows sit at the end of the degree-sorted order)
     const int lane = threadIdx.x & 31;
-    int c0, cstride;
-    if (ph.grid) {
-      c0 = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-      cstride = gridDim.x * (blockDim.x >> 5);
-    } else {
-      c0 = (threadIdx.x >> 5) * P.csize + blockIdx.x;
-      cstride = P.csize * (blockDim.x >> 5);
-    }
-    if (ph.type == 0) {
-      const bool marg = do_marg && ph.marg;
-      if (marg || do_vtof)
-        for (int c = c0; c * 32 < total; c += cstride) {
-          const int i = c * 32 + lane;
-          if (i >= total) break;
-          if (i >= hn) {
-            vnode(P, ph.begin + (i - hn), marg, do_vtof, it, pidx, dmax, ufkey,
-                  it == 1 && pidx == 0);
-          } else {
-            const int q = ph.sbegin + i;
-            v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
-                   pidx, dmax, ufkey, it == 1 && pidx == 0);
-          }
+    const bool marg = do_marg && ph.marg;
+    if (ph.type == 0 && !(marg || do_vtof)) return;
+    // Chunk map: round r (G consecutive chunks, G = the CTAs of the phase)
+    // goes to warp r % (warps per CTA) of every CTA, dealt boustrophedon --
+    // CTA b takes position b on even rounds and G-1-b on odd ones. Chunk
+    // cost grows with the row length along the degree-sorted order, so a
+    // plain deal (position b every round) hands the high CTA ids the dearer
+    // chunk of every round; per-CTA phase times then differ by up to 25 %,
+    // stably across iterations (measured at ftp: rotating the map per
+    // iteration decorrelates them -- the imbalance is data, not the SM).
+    const int nchunks = (total + 31) / 32;
+    const int G = ph.grid ? (int)gridDim.x : P.csize;
+    const int wpc = blockDim.x >> 5;
+    const int wib = threadIdx.x >> 5;
+    unsigned long long *ctr = (P.trace && it == 3 && P.nphases == 2 && nchunks <= kChunkTrace)
+                                  ? P.trace + (size_t)kTraceIters * 2 * gridDim.x * 2 + pidx * kChunkTrace
+                                  : nullptr;
+    auto run_chunks = [&](auto &&chunk) {
+      for (int r = wib; r * G < nchunks; r += wpc) {
+        const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+        if (k >= nchunks) continue;
+        const unsigned long long t0 = ctr ? globaltimer() : 0;
+        chunk(k);
+        if (ctr) {
+          __syncwarp();
+          if (lane == 0) ctr[k] = globaltimer() - t0;
         }
-    } else {
-      for (int c = c0; c * 32 < total; c += cstride) {
+      }
+    };
+    if (ph.type == 0) {
+      run_chunks([&](int c) {
         const int i = c * 32 + lane;
-        if (i >= total) break;
+        if (i >= total) return;
+        if (i >= hn) {
+          vnode(P, ph.begin + (i - hn), marg, do_vtof, it, pidx, dmax, ufkey,
+                it == 1 && pidx == 0);
+        } else {
+          const int q = ph.sbegin + i;
+          v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
+                 pidx, dmax, ufkey, it == 1 && pidx == 0);
+        }
+      });
+    } else {
+      run_chunks([&](int c) {
+        const int i = c * 32 + lane;
+        if (i >= total) return;
         if (i >= hn) {
           fnode(P, ph.begin + (i - hn), pidx, it == 1, ufkey);
         } else {
           const int p = ph.sbegin + i;
           f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
         }
-      }
+      });
     }
     flush_underflow(P, it, ufkey);
     return;
@@ -673,18 +697,18 @@ __device__ __forceinline__ unsigned long long block_max(unsigned long long v) {
   return v;  // valid in thread 0
 }
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // debug timeline (HBP_TRACE=1): per CTA, phase start / end after a CTA sync
 __device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int which) {
   if (P.trace == nullptr || it < 2 || it >= 2 + kTraceIters) return;
   __syncthreads();
-  if (threadIdx.x == 0)
-    P.trace[(((size_t)(it - 2) * P.nphases + p) * gridDim.x + blockIdx.x) * 2 + which] = globaltimer();
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    // ns timer (low 52 bits) << 8 | SM id
+    P.trace[(((size_t)(it - 2) * P.nphases + p) * gridDim.x + blockIdx.x) * 2 + which] =
+        ((globaltimer() & ((1ull << 52) - 1)) << 8) | (smid & 0xff);
+  }
 }
 
 // barrier of cluster 0 between two small levels (release/acquire at cluster
@@ -1293,7 +1317,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.ev = g->has_ev ? g->d_ev : nullptr;
   P.trace = nullptr;
   if (getenv("HBP_TRACE")) {
-    const size_t n_tr = (size_t)hbp::kTraceIters * P.nphases * p->grid * 2;
+    const size_t n_tr = (size_t)hbp::kTraceIters * P.nphases * p->grid * 2 + 2 * hbp::kChunkTrace;
     if (g->trace_cap < n_tr) {
       if (g->d_trace) cudaFree(g->d_trace);
       HBP_CUDA(cudaMalloc(&g->d_trace, n_tr * 8));
@@ -1644,7 +1668,8 @@ void hbp_debug_plan_info(hbp_plan *p, int32_t *nphases, int32_t *grid, int32_t *
 // Debug timeline of the last run with HBP_TRACE=1 (not part of the public header).
 int64_t hbp_debug_trace(hbp_plan *p, unsigned long long *out, int64_t cap) {
   hbp_graph *g = p->g;
-  const int64_t n = (int64_t)hbp::kTraceIters * (int64_t)p->host.phases.size() * p->grid * 2;
+  const int64_t n = (int64_t)hbp::kTraceIters * (int64_t)p->host.phases.size() * p->grid * 2 +
+                    (p->host.phases.size() == 2 ? 2 * hbp::kChunkTrace : 0);
   if (!g->d_trace || cap < n) return -n;
   cudaMemcpy(out, g->d_trace, (size_t)n * 8, cudaMemcpyDeviceToHost);
   return n;
