@@ -6,7 +6,8 @@ import numpy as np
 import paper_2509_22337_b200 as P
 from paper_2509_22337_b200 import _native, workloads as W
 name = sys.argv[1]
-w = W.build(name)
+wl = W.build(name)
+w = wl
 sched = w.strategy.compile(w.graph)
 opts = P.EngineOptions(max_iterations=w.max_iterations, tolerance=w.tolerance)
 t = time.time()
@@ -76,3 +77,63 @@ if chunk_ns is not None:
         # mean by 100-chunk bucket
         b = [int(c[i:i + 500].mean()) for i in range(0, nch, 500)]
         print("   mean ns per 500-chunk bucket:", b)
+
+# per-warp totals under the boustrophedon map, and what an LPT round->warp
+# map (measured round costs) would give
+if chunk_ns is not None:
+    import heapq
+    wpc = thr.value // 32
+    for ph in range(2):
+        cn = chunk_ns[ph]
+        nz = np.nonzero(cn)[0]
+        if not len(nz):
+            continue
+        nch = nz.max() + 1
+        c = cn[:nch].astype(np.float64)
+        R = -(-nch // G)
+        tot = np.zeros((G, wpc))
+        for k in range(nch):
+            r, p = divmod(k, G)
+            b = p if r % 2 == 0 else G - 1 - p
+            tot[b, r % wpc] += c[k]
+        rc = np.array([c[r * G:(r + 1) * G].mean() for r in range(R)])
+        rmax = np.array([c[r * G:(r + 1) * G].max() for r in range(R)])
+        # LPT: rounds by cost desc onto the least-loaded warp
+        heap = [(0.0, w) for w in range(wpc)]
+        assign = {}
+        for r in np.argsort(-rc):
+            load, w = heapq.heappop(heap)
+            assign[r] = w
+            heapq.heappush(heap, (load + rc[r], w))
+        tot2 = np.zeros((G, wpc))
+        for k in range(nch):
+            r, p = divmod(k, G)
+            b = p if r % 2 == 0 else G - 1 - p
+            tot2[b, assign[r]] += c[k]
+        print(f"phase {ph}: rounds {R}, warp totals now: max {tot.max()/1e3:.2f} us, per-CTA max-warp median {np.median(tot.max(1))/1e3:.2f}; "
+              f"LPT rounds: max {tot2.max()/1e3:.2f} us, per-CTA median {np.median(tot2.max(1))/1e3:.2f}; ideal mean {tot.sum()/G/wpc/1e3:.2f}")
+
+# chunk cost by item class (pure chunks only): the cost model's input
+if chunk_ns is not None:
+    g = wl.graph
+    vdeg = np.bincount(np.asarray(g.vars), minlength=g.num_variables)
+    fdeg = np.diff(np.asarray(g.rowptr))
+    fkind = np.asarray(g.kind)
+    K = 4
+    # phase 0 items
+    hv = np.sort(vdeg[vdeg > K])
+    items0 = np.concatenate([np.repeat(hv, hv) + 1000, np.sort(vdeg[vdeg <= K])])  # +1000 marks heavy slots
+    # phase 1 items: heavy AND slots, heavy OR slots, light AND nodes, light OR nodes
+    hA = np.sort(fdeg[(fdeg > K) & (fkind == 0)]); hO = np.sort(fdeg[(fdeg > K) & (fkind == 1)])
+    lA = np.sort(fdeg[(fdeg <= K) & (fkind == 0)]); lO = np.sort(fdeg[(fdeg <= K) & (fkind == 1)])
+    items1 = np.concatenate([np.repeat(hA, hA) + 1000, np.repeat(hO, hO) + 2000, lA, lO + 100])
+    for ph, items in ((0, items0), (1, items1)):
+        c = chunk_ns[ph][: -(-len(items) // 32)].astype(np.float64)
+        cls = {}
+        for k in range(len(c)):
+            u = np.unique(items[32 * k: 32 * k + 32])
+            key = tuple(int(x) for x in u)
+            cls.setdefault(key, []).append(c[k])
+        rows = sorted(cls.items(), key=lambda kv: kv[0])
+        print(f"phase {ph} class costs (item code: deg, +100 OR light, +1000 heavy AND/var slot, +2000 heavy OR slot):")
+        print("   " + "; ".join(f"{k}: n={len(v)} {np.mean(v):.0f}" for k, v in rows if len(v) >= 1))
