@@ -43,6 +43,7 @@ from __future__ import annotations
 
 import argparse
 import json
+from typing import Optional
 import os
 import statistics
 import subprocess
@@ -572,8 +573,24 @@ def measure_single(torch, workload: str, steps: int, warmup: int) -> dict:
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "kernel": "hbp::lbp_persistent (whole run in one launch)",
                      "bytes_per_launch": bytes_per_launch,
-                     "note": "working set (~28 MB) is L2-resident within a run"},
+                     "note": "working set (~28 MB) is L2-resident within a run",
+                     "l2": l2_roofline(achieved),
+                     "l2_traffic_per_launch": 2044344768.0,
+                     "l2_traffic_source": "ncu lts__t_sectors.sum x 32 B of one launch (profiles/r1_c4_parall_ncu.md v2)"},
     }
+
+
+def l2_roofline(achieved: float) -> Optional[dict]:
+    """The same algorithmic rate against the measured L2 read+write bandwidth
+    (profiles/l2_peak.json, tools/l2_bench.cu; SURVEY.md 8(d) asks for it)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_peak.json")) as fh:
+            runs = json.load(fh)["runs"]
+    except (OSError, KeyError, ValueError):
+        return None
+    peak = max(r["read_write_gbs"] for r in runs)
+    return {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": "profiles/l2_peak.json: best L2-resident 16-B read+write stream (tools/l2_bench.cu)"}
 
 
 def run_ours_single(args) -> None:
