@@ -79,8 +79,9 @@ struct hbp_graph {
 
   ~hbp_graph() {
     cudaSetDevice(device);
-    // the layout, message buffers and layout scratch live in d_block
-    for (void *p : {d_block, (void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace})
+    // the layout, message buffers and layout scratch live in d_block (pool)
+    if (d_block) cudaFreeAsync(d_block, own_stream ? own_stream : stream);
+    for (void *p : {(void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);

@@ -830,10 +830,30 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
           sync_point(C, sy, P.csize, in0, true);
         }
       }
+      // Look-ahead for levelled schedules: the next list phase's first item
+      // of this thread is loaded now (read-only plan data, L1-cached) and its
+      // slot word and twin lines are prefetched into L1 once this phase is
+      // done, so a small level's dependent chain starts at the message rows.
+      int nx = -1;  // slot | type << 30
+      if (p + 1 < P.nphases) {
+        const Phase &np = P.phases[p + 1];
+        const bool mine = np.grid || (int)blockIdx.x < P.csize;
+        const int i = blockIdx.x * blockDim.x + threadIdx.x;
+        if (np.list == 1 && mine && i < np.end - np.begin)
+          nx = (__ldg(P.items + np.begin + i) & (kWriteBit - 1)) | (np.type << 30);
+      }
       unsigned long long unused = 0;
       trace_mark(P, it, p, 0);
       exec_phase(P, ph, p, it, false, true, unused);
       trace_mark(P, it, p, 1);
+      if (nx >= 0) {
+        const int q = nx & (kWriteBit - 1);
+        const bool fac = nx >> 30;
+        const void *a = fac ? (const void *)(P.fslot + q) : (const void *)(P.vslot + q);
+        const void *b = fac ? (const void *)(P.vtof_twin + q) : (const void *)(P.ftov_twin + q);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(b));
+      }
     }
     // transition last phase -> phase 0 of the next iteration (a grid phase)
     if (P.nphases > 1) {

@@ -305,8 +305,19 @@ hbp_status build_layout_device(const hbp_graph_desc &desc, hbp_graph *g) {
                          4 * (5 * (size_t)(F + 2) + 5 * (size_t)(V + 2) + 3 * nE + (size_t)maxn + 256);
   // the PARALL shape test needs 2E ints + 2 bitmaps
   const size_t scratch_all = std::max(scratch, 4 * (2 * nE + 2 * ((nE + 31) / 32) + 64) + 512);
+  // from the device's stream-ordered pool, which keeps freed blocks (release
+  // threshold raised once per device): a fresh graph of a size seen before
+  // costs no cudaMalloc, and destroying one no cudaFree
+  static bool pool_ready[64] = {};
+  if (g->device >= 0 && g->device < 64 && !pool_ready[g->device]) {
+    cudaMemPool_t pool;
+    HBP_CUDA(cudaDeviceGetDefaultMemPool(&pool, g->device));
+    uint64_t keep = ~0ull;
+    HBP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pool_ready[g->device] = true;
+  }
   void *block = nullptr;
-  HBP_CUDA(cudaMalloc(&block, persistent + scratch_all));
+  HBP_CUDA(cudaMallocAsync(&block, persistent + scratch_all, s));
   g->d_block = block;
   P.base = (char *)block;
   P.off = 0;
