@@ -1243,16 +1243,21 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   HBP_CUDA(cudaSetDevice(g->device));
   hbp_status st;
   bool parall = false;
+  // HBP_GROUPING=1|0 (A/B of the message grouping, see build_plan): slot items
+  // in degree order / in EdgeId order instead of whole degree-sorted nodes
+  const char *ge = getenv("HBP_GROUPING");
+  const int grouping = ge ? std::max(0, std::min(2, atoi(ge))) : 2;
   // a one-batch schedule of PARALL shape is recognised on the device and
   // needs no host layout; anything else is planned by the host builder
-  if (k == 1 && s_off && t_off && s_off[0] == 0 && t_off[0] == 0 && s_off[1] >= 0 && t_off[1] >= 0 &&
+  if (grouping == 2 && k == 1 && s_off && t_off && s_off[0] == 0 && t_off[0] == 0 && s_off[1] >= 0 && t_off[1] >= 0 &&
       (st = hbp::parall_check_device(g, s_off[1], s_edges, t_off[1], t_edges, &parall)) != HBP_OK)
     return st;
   if (parall) {
     hbp::parall_plan(g->L, s_off[1], t_off[1], p->host, small);
   } else {
     if ((st = hbp::ensure_host_layout(g)) != HBP_OK) return st;
-    if ((st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small)) != HBP_OK)
+    if ((st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small,
+                              grouping)) != HBP_OK)
       return st;
   }
   cudaStream_t s = g->stream;

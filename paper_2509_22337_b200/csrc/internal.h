@@ -123,8 +123,12 @@ struct PlanHost {
 void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
                  int32_t small_threshold);
 
+// grouping (the A/B of the paper's message grouping):
+// 2 = whole degree-sorted nodes per thread where a phase covers every node
+// (default), 1 = one slot per thread in slot (= degree-sorted) order,
+// 0 = one slot per thread in the schedule's own (EdgeId) order.
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P, int32_t small_threshold);
+                      PlanHost &P, int32_t small_threshold, int grouping = 2);
 
 }  // namespace hbp

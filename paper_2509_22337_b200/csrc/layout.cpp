@@ -238,7 +238,7 @@ void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P, int32_t small_threshold) {
+                      PlanHost &P, int32_t small_threshold, int grouping) {
   const int32_t V = L.V;
   const int64_t E = L.E;
   if (k < 0 || (k > 0 && (s_off[0] != 0 || t_off[0] != 0))) {
@@ -282,7 +282,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
 
   // PARALL fast path: one batch holding every edge once and every slot of a
   // non-unary factor once compiles to the two whole-graph phases directly
-  if (k == 1 && ns == E && nt == nonunary_total) {
+  if (grouping == 2 && k == 1 && ns == E && nt == nonunary_total) {
     std::vector<uint8_t> seen((size_t)E, 0);
     bool ok = true;
     for (int64_t i = 0; i < ns && ok; ++i) {
@@ -325,7 +325,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       Phase ph{};
       ph.type = 0;
       ph.marg = b == 0;
-      if (b == 0 && n_nonunary == nonunary_total && !has_unary) {
+      if (grouping == 2 && b == 0 && n_nonunary == nonunary_total && !has_unary) {
         // PARALL: every non-unary vtof slot + every marginal == every variable
         // node in full
         ph.list = 2;
@@ -347,9 +347,10 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
             if (!tgt[vi]) items.push_back(L.vrow[vi]);
         }
         // ascending slot order == (degree, variable) order: warp-uniform trip counts
-        std::sort(items.begin(), items.end(), [](int32_t a, int32_t c) {
-          return (a & (kWriteBit - 1)) < (c & (kWriteBit - 1));
-        });
+        if (grouping >= 1)
+          std::sort(items.begin(), items.end(), [](int32_t a, int32_t c) {
+            return (a & (kWriteBit - 1)) < (c & (kWriteBit - 1));
+          });
         ph.list = 1;
         ph.begin = (int32_t)P.items.size();
         P.items.insert(P.items.end(), items.begin(), items.end());
@@ -371,7 +372,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       }
       Phase ph{};
       ph.type = 1;
-      if ((int64_t)slots.size() == E) {
+      if (grouping == 2 && (int64_t)slots.size() == E) {
         ph.list = 2;  // every factor node in full
         ph.begin = 0;
         ph.end = L.f_heavy;
@@ -380,7 +381,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
         push_phase(ph, L.f_heavy + (ph.send - ph.sbegin));
       } else if (!slots.empty()) {
         // ascending vtof slot == (kind, degree, factor) order: warp-uniform role
-        std::sort(slots.begin(), slots.end());
+        if (grouping >= 1) std::sort(slots.begin(), slots.end());
         ph.list = 1;
         ph.begin = (int32_t)P.items.size();
         P.items.insert(P.items.end(), slots.begin(), slots.end());
