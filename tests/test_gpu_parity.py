@@ -382,3 +382,26 @@ def test_long_rows_bitwise_vs_oracle():
             assert res.iterations == o["iterations"]
             assert res.marginals.tobytes() == o["marginals"].tobytes(), (trial, strat.kind)
             assert np.asarray(res.deltas).tobytes() == o["deltas"].tobytes()
+
+
+@pytest.mark.parametrize("grouping", ["1", "0"])
+def test_grouping_modes_bitwise_identical(grouping, monkeypatch):
+    """HBP_GROUPING (the grouping A/B of profiles/r1_grouping_ab.md) only moves
+    work between threads: slot items in degree order (1) or in EdgeId order
+    (0) give the default node-grouped plan's bits."""
+    rng = np.random.default_rng(99)
+    graphs = [W.graph("hedc")[0]] + [random_graph(rng, max_vars=20, max_factors=20, max_body=5)
+                                     for _ in range(6)]
+    for g in graphs:
+        for strat in (Strategy.parall(), Strategy.seqfix()):
+            opts = EngineOptions(60, 1e-9)
+            monkeypatch.delenv("HBP_GROUPING", raising=False)
+            P.engine.clear_device_cache()
+            ref = P.run(g, strat.compile(g), opts)
+            monkeypatch.setenv("HBP_GROUPING", grouping)
+            P.engine.clear_device_cache()
+            got = P.run(g, strat.compile(g), opts)
+            assert got.iterations == ref.iterations
+            assert got.marginals.tobytes() == ref.marginals.tobytes()
+            assert np.asarray(got.deltas).tobytes() == np.asarray(ref.deltas).tobytes()
+    P.engine.clear_device_cache()
