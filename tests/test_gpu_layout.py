@@ -68,3 +68,35 @@ def test_parall_plan_without_host_layout_is_bitwise():
     a2 = P.run(g, Strategy.parall().compile(g), opts)
     assert a.marginals.tobytes() == a2.marginals.tobytes() and a.iterations == a2.iterations
     assert b.marginals.tobytes() == b2.marginals.tobytes() and b.iterations == b2.iterations
+
+
+def _create(V, rowptr, evar, kind):
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    evar = np.asarray(evar, dtype=np.int32)
+    kind = np.asarray(kind, dtype=np.int8)
+    F = len(rowptr) - 1
+    p = np.full(max(F, 1), 0.5)
+    desc = _native.GraphDesc(V, F, int(len(evar)), _native.ptr(rowptr, C.c_int64),
+                             _native.ptr(evar, C.c_int32), _native.ptr(kind, C.c_int8),
+                             _native.ptr(p, C.c_double), _native.ptr(p, C.c_double))
+    h = C.c_void_p()
+    st = _native.lib().hbp_graph_create(C.byref(desc), 0, C.byref(h))
+    if st == _native.HBP_OK:
+        _native.lib().hbp_graph_destroy(h)
+        return None
+    return st, _native.last_error()
+
+
+@pytest.mark.parametrize("case,want", [
+    ((3, [0, 2, 2], [0, 1], [0, 0]), "factor 1: degree must be in [1, 65535]"),
+    ((3, [0, 2, 3], [0, 1, 2], [0, 7]), "factor 1: bad kind"),
+    ((3, [0, 2, 3], [0, 1, 5], [0, 0]), "edge variable out of range"),
+    ((4, [0, 2, 3], [0, 1, 2], [0, 1]), "variable 3 appears in no factor"),
+    ((3, [0, 2, 4], [0, 1, 2], [0, 1]), "factor_rowptr does not span the edge array"),
+])
+def test_device_layout_rejects_like_the_host_builder(case, want):
+    """hbp_graph_create validates on the device; the errors are the host
+    builder's (layout.cpp), in its order."""
+    err = _create(*case)
+    assert err is not None and err[0] == _native.HBP_EINVAL
+    assert want in err[1], err[1]
