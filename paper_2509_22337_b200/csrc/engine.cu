@@ -40,6 +40,7 @@ using namespace dev;
 
 constexpr int kThreads = 768;  // default block size: 80 registers, fewest spills (measured best)
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
+constexpr int kPhaseCache = 1024;  // phase descriptors staged in shared memory (32 KB)
 constexpr int kChunkTrace = 16384;  // HBP_TRACE=1: per-chunk ns of iteration 3, PARALL phases 0/1
 
 struct Ctrl {
@@ -739,7 +740,15 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
   // PARALL (two whole-graph phases): iteration 1 needs no initial messages --
   // its variable side writes the normalised uniform message directly, and its
   // factor side then writes every factor-to-variable message
-  const bool parall = P.nphases == 2 && P.phases[0].list == 2 && P.phases[1].list == 2;
+  // the phase descriptors (a levelled schedule has two per level: 952 at ftp
+  // SEQFIX) are staged in shared memory once, so a small level's start does
+  // not wait on a global load of its descriptor
+  __shared__ Phase s_ph[kPhaseCache];
+  __shared__ int s_nx[THREADS];  // look-ahead items (levelled schedules)
+  for (int i = threadIdx.x; i < P.nphases && i < kPhaseCache; i += blockDim.x) s_ph[i] = P.phases[i];
+  __syncthreads();
+  auto phase_at = [&](int i) -> const Phase & { return i < kPhaseCache ? s_ph[i] : P.phases[i]; };
+  const bool parall = P.nphases == 2 && s_ph[0].list == 2 && s_ph[1].list == 2;
   auto grid_sync = [&]() {
     if (multi) sync_point(C, sy, G, true, true);
     else __syncthreads();
@@ -762,7 +771,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
     trace_mark(P, it, 0, 0);
-    exec_phase(P, P.phases[0], 0, it, it > 1, !final_pass, dmax);
+    exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
     trace_mark(P, it, 0, 1);
     if (it > 1) {
       unsigned long long m = block_max(dmax);
@@ -814,9 +823,9 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
     }
     // remaining phases of this iteration
     for (int p = 1; p < P.nphases; ++p) {
-      const Phase ph = P.phases[p];
+      const Phase ph = phase_at(p);
       if (p > 1) {  // transition p-1 -> p (phase 0 -> 1 was the full barrier above)
-        const int prev_grid = P.phases[p - 1].grid;
+        const int prev_grid = phase_at(p - 1).grid;
         const bool in0 = (int)blockIdx.x < P.csize;
         if (!multi) {
           __syncthreads();
@@ -831,24 +840,30 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
         }
       }
       // Look-ahead for levelled schedules: the next list phase's first item
-      // of this thread is loaded now (read-only plan data, L1-cached) and its
-      // slot word and twin lines are prefetched into L1 once this phase is
-      // done, so a small level's dependent chain starts at the message rows.
-      int nx = -1;  // slot | type << 30
+      // of this thread is copied into shared memory now (cp.async: no
+      // register waits on it) and, once this phase is done, its slot word and
+      // twin lines are prefetched into L1 -- so a small level's dependent
+      // chain starts at the message rows.
+      bool look = false;
       if (p + 1 < P.nphases) {
-        const Phase &np = P.phases[p + 1];
-        const bool mine = np.grid || (int)blockIdx.x < P.csize;
+        const Phase &np = phase_at(p + 1);
         const int i = blockIdx.x * blockDim.x + threadIdx.x;
-        if (np.list == 1 && mine && i < np.end - np.begin)
-          nx = (__ldg(P.items + np.begin + i) & (kWriteBit - 1)) | (np.type << 30);
+        look = np.list == 1 && (np.grid || (int)blockIdx.x < P.csize) && i < np.end - np.begin;
+        if (look) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_nx[threadIdx.x]);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" ::"r"(dst),
+                       "l"(P.items + np.begin + i)
+                       : "memory");
+        }
       }
       unsigned long long unused = 0;
       trace_mark(P, it, p, 0);
       exec_phase(P, ph, p, it, false, true, unused);
       trace_mark(P, it, p, 1);
-      if (nx >= 0) {
-        const int q = nx & (kWriteBit - 1);
-        const bool fac = nx >> 30;
+      if (look) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        const int q = s_nx[threadIdx.x] & (kWriteBit - 1);
+        const bool fac = phase_at(p + 1).type == 1;
         const void *a = fac ? (const void *)(P.fslot + q) : (const void *)(P.vslot + q);
         const void *b = fac ? (const void *)(P.vtof_twin + q) : (const void *)(P.ftov_twin + q);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
@@ -857,7 +872,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
     }
     // transition last phase -> phase 0 of the next iteration (a grid phase)
     if (P.nphases > 1) {
-      const int last_grid = P.phases[P.nphases - 1].grid;
+      const int last_grid = phase_at(P.nphases - 1).grid;
       if (!multi) {
         __syncthreads();
       } else if (last_grid) {
