@@ -138,8 +138,34 @@ def _raise_status(status: int, what: str, result: Optional[_native.Result] = Non
     raise RuntimeError(f"{what}: {msg}")
 
 
+class _GraphHandle:
+    """Owns one hbp_graph. Plans and sweeps hold this (not the _DeviceGraph
+    that caches them), so the ownership graph has no cycle: dropping a
+    _DeviceGraph frees its plans, sweeps and device memory at once, by
+    reference count, instead of at some later cyclic-GC pass."""
+
+    def __init__(self, arrays, num_variables: int, num_edges: int, device: int):
+        self.num_variables = num_variables
+        self.num_edges = num_edges
+        self.device = device
+        h = C.c_void_p()
+        st = _native.lib().hbp_graph_create(C.byref(arrays.desc), device, C.byref(h))
+        if st != _native.HBP_OK:
+            _raise_status(st, "hbp_graph_create")
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _native.lib().hbp_graph_destroy(h)
+            except Exception:  # interpreter shutdown: the module may be gone
+                pass
+            self.handle = None
+
+
 class _Plan:
-    def __init__(self, dg: "_DeviceGraph", arrays):
+    def __init__(self, dg: "_GraphHandle", arrays):
         s_off, s_e, t_off, t_e = arrays
         self.dg = dg
         self.updates = int(len(s_e) + len(t_e))
@@ -157,7 +183,10 @@ class _Plan:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:
-            _native.lib().hbp_plan_destroy(h)
+            try:
+                _native.lib().hbp_plan_destroy(h)
+            except Exception:  # interpreter shutdown: the module may be gone
+                pass
             self.handle = None
 
     def options(self, options: EngineOptions) -> _native.Options:
@@ -199,7 +228,7 @@ class _Plan:
 
 
 class _Sweep:
-    def __init__(self, dg: "_DeviceGraph", capacity: int):
+    def __init__(self, dg: "_GraphHandle", capacity: int):
         self.dg = dg
         h = C.c_void_p()
         st = _native.lib().hbp_sweep_create(dg.handle, int(capacity), C.byref(h))
@@ -211,7 +240,10 @@ class _Sweep:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:
-            _native.lib().hbp_sweep_destroy(h)
+            try:
+                _native.lib().hbp_sweep_destroy(h)
+            except Exception:  # interpreter shutdown: the module may be gone
+                pass
             self.handle = None
 
 
@@ -223,11 +255,8 @@ class _DeviceGraph:
         self.num_variables = graph.num_variables
         self.num_edges = graph.num_edges
         self.device = device
-        h = C.c_void_p()
-        st = _native.lib().hbp_graph_create(C.byref(self.arrays.desc), device, C.byref(h))
-        if st != _native.HBP_OK:
-            _raise_status(st, "hbp_graph_create")
-        self.handle = h
+        self.h = _GraphHandle(self.arrays, graph.num_variables, graph.num_edges, device)
+        self.handle = self.h.handle
         self._plans: "OrderedDict[int, tuple[weakref.ref, _Plan]]" = OrderedDict()
         self._sweeps: dict = {}
 
@@ -237,7 +266,7 @@ class _DeviceGraph:
         if hit is not None and hit[0]() is schedule:
             self._plans.move_to_end(key)
             return hit[1]
-        p = _Plan(self, schedule.arrays(graph))
+        p = _Plan(self.h, schedule.arrays(graph))
         self._plans[key] = (weakref.ref(schedule), p)
         while len(self._plans) > 8:
             self._plans.popitem(last=False)
@@ -280,7 +309,7 @@ class _DeviceGraph:
         sw = self._sweeps.get(capacity)
         if sw is None:
             self._sweeps.clear()  # one set of sweep buffers per graph
-            sw = _Sweep(self, capacity)
+            sw = _Sweep(self.h, capacity)
             self._sweeps[capacity] = sw
         return sw
 
@@ -291,12 +320,10 @@ class _DeviceGraph:
         return int(graph.num_edges + deg[deg > 1].sum())
 
     def __del__(self):
+        # plans and sweeps first (they hold self.h); the graph goes with the
+        # last reference to self.h
         self._sweeps = {}
         self._plans = OrderedDict()
-        h = getattr(self, "handle", None)
-        if h:
-            _native.lib().hbp_graph_destroy(h)
-            self.handle = None
 
 
 def device_graph(graph: FactorGraph) -> _DeviceGraph:
