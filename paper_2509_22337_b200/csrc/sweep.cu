@@ -32,7 +32,6 @@
 // CTA whose 32 sets have all stopped skips the phase. No host round trip until
 // every set of the pass has stopped.
 #include <cuda_runtime.h>
-#include <type_traits>
 
 #include <chrono>
 #include <cstdlib>
@@ -1009,47 +1008,7 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
     }
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
     const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
-    // a chunk of one kind and one degree (factors are sorted by kind, then
-    // degree) takes the dispatch once instead of per factor
-    const int d_first = ch.rp[n0 + 1 - rp_lo] - ch.rp[n0 - rp_lo];
-    const int d_last = ch.rp[n1 - rp_lo] - ch.rp[n1 - 1 - rp_lo];
-    auto crosses = [&](int b) { return n0 < b && b < n1; };
-    bool done_uniform = false;
-    if (any && !ch.heavy && d_first == d_last && d_first <= 5 && !crosses(P.f_or_light) &&
-        !crosses(P.f_heavy) && !crosses(P.f_or_heavy)) {
-      done_uniform = true;
-      const bool is_or = (n0 >= P.f_or_light && n0 < P.f_heavy) || n0 >= P.f_or_heavy;
-      const int rf = ch.rp[n0 - rp_lo];
-      auto run = [&](auto dc, auto kc) {
-        constexpr int D = decltype(dc)::value, KIND = decltype(kc)::value;
-        if (!FIRST && !unary && D == 1) return;  // unary: constants
-        for (int f = n0 + start; f < n1; f += WsCfg<NS>::consumers) {
-          const int r = rf + (f - n0) * D;
-          const typename Ar<T>::T2 *x[NS];
-#pragma unroll
-          for (int u = 0; u < NS; ++u) x[u] = &ch.msg[u][r - r0][lane];
-          ws_fac<D, KIND, NS, NORM, FIRST, T>(L, x, ch.tw + (r - tw_lo), ch.fpar[f - n0], alive, uf);
-        }
-      };
-      auto by_kind = [&](auto dc) {
-        if (is_or) run(dc, std::integral_constant<int, 1>{});
-        else run(dc, std::integral_constant<int, 0>{});
-      };
-      switch (d_first) {
-        case 1: by_kind(std::integral_constant<int, 1>{}); break;
-        case 2: by_kind(std::integral_constant<int, 2>{}); break;
-        case 3: by_kind(std::integral_constant<int, 3>{}); break;
-        case 4: by_kind(std::integral_constant<int, 4>{}); break;
-#if HBP_WS_DMAX > 4
-        case 5:
-          if (NS == 1) by_kind(std::integral_constant<int, 5>{});
-          else done_uniform = false;
-          break;
-#endif
-        default: done_uniform = false; break;
-      }
-    }
-    if (any && !done_uniform) {
+    if (any) {
       for (int f = n0 + start; f < n1; f += WsCfg<NS>::consumers) {
         const int r = ch.rp[f - rp_lo];
         const int d = ch.rp[f + 1 - rp_lo] - r;
@@ -1107,50 +1066,7 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
     }
     const int rp_lo = n0 & ~3, tw_lo = r0 & ~3;
     const int start = (cw + WsCfg<NS>::consumers - base % WsCfg<NS>::consumers) % WsCfg<NS>::consumers;
-    // a chunk of one degree (nodes are degree-sorted: first == last) takes
-    // the degree dispatch once instead of per node
-    const int d_first = ch.rp[n0 + 1 - rp_lo] - ch.rp[n0 - rp_lo];
-    const int d_last = ch.rp[n1 - rp_lo] - ch.rp[n1 - 1 - rp_lo];
-    bool done_uniform = false;
-    if (any && !ch.heavy && d_first == d_last && d_first <= HBP_WS_DMAX) {
-      done_uniform = true;
-      const int rf = ch.rp[n0 - rp_lo];
-      auto run = [&](auto dc) {
-        constexpr int D = decltype(dc)::value;
-        for (int v = n0 + start; v < n1; v += WsCfg<NS>::consumers) {
-          const int r = rf + (v - n0) * D;
-          unsigned code[NS];
-          double prev_p0[NS];
-          const typename Ar<T>::T2 *x[NS];
-#pragma unroll
-          for (int u = 0; u < NS; ++u) {
-            code[u] = ch.ev[u][v - n0][lane];
-            prev_p0[u] = it > 2 ? ch.p0[u][v - n0][lane] : 0.5;
-            x[u] = &ch.msg[u][r - r0][lane];
-          }
-          ws_var<D, NS, NORM, T>(P, L, v, x, ch.tw + (r - tw_lo), code, prev_p0, it, write_vtof,
-                                 alive, dmax, uf);
-        }
-      };
-      switch (d_first) {
-        case 1: run(std::integral_constant<int, 1>{}); break;
-        case 2: run(std::integral_constant<int, 2>{}); break;
-        case 3: run(std::integral_constant<int, 3>{}); break;
-        case 4: run(std::integral_constant<int, 4>{}); break;
-#if HBP_WS_DMAX > 4
-        case 5:
-          if (NS == 1) run(std::integral_constant<int, 5>{});
-          else done_uniform = false;
-          break;
-        case 6:
-          if (NS == 1) run(std::integral_constant<int, 6>{});
-          else done_uniform = false;
-          break;
-#endif
-        default: done_uniform = false; break;
-      }
-    }
-    if (any && !done_uniform) {
+    if (any) {
       for (int v = n0 + start; v < n1; v += WsCfg<NS>::consumers) {
         const int r = ch.rp[v - rp_lo];
         const int d = ch.rp[v + 1 - rp_lo] - r;
