@@ -137,3 +137,13 @@ if chunk_ns is not None:
         rows = sorted(cls.items(), key=lambda kv: kv[0])
         print(f"phase {ph} class costs (item code: deg, +100 OR light, +1000 heavy AND/var slot, +2000 heavy OR slot):")
         print("   " + "; ".join(f"{k}: n={len(v)} {np.mean(v):.0f}" for k, v in rows if len(v) >= 1))
+
+# levelled schedules: CTA 0's per-phase compute time distribution (small levels)
+if nph > 8:
+    d0 = (a[1, :, 0, 1] - a[1, :, 0, 0]) / 1e3
+    d0 = d0[a[1, :, 0, 0] > 0]
+    typ = np.arange(len(d0)) % 2
+    for t in (0, 1):
+        x = d0[2:][typ[2:] == t]
+        print(f"CTA0 small phases type {t}: n={len(x)} min {x.min():.2f} p10 {np.percentile(x,10):.2f} "
+              f"median {np.median(x):.2f} p90 {np.percentile(x,90):.2f} max {x.max():.2f} us")
