@@ -1254,7 +1254,9 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   if (!p) return HBP_ENOMEM;
   p->g = g;
   // levels smaller than two items per thread of cluster 0 run on cluster 0 only
-  const int32_t small = g->csize > 1 ? 2 * g->csize * g->threads : 3072;
+  // levels below this many items run on cluster 0 alone (HBP_SMALL: A/B)
+  const char *se = getenv("HBP_SMALL");
+  const int32_t small = se ? atoi(se) : (g->csize > 1 ? 2 * g->csize * g->threads : 3072);
   HBP_CUDA(cudaSetDevice(g->device));
   hbp_status st;
   bool parall = false;
