@@ -1,4 +1,4 @@
-"""Scratch: single-graph e2e after the bench's 1,024-set sweeps (the bench's own order)."""
+"""Scratch probe (GPU box): single-graph e2e after the bench's 1,024-set sweeps (the bench's own order)."""
 import ctypes as C, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

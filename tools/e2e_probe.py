@@ -1,4 +1,4 @@
-"""Scratch: where the single-graph e2e time goes (fresh layout per run)."""
+"""Scratch probe (GPU box): where the single-graph e2e time goes (fresh layout per run)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

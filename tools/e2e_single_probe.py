@@ -1,4 +1,4 @@
-"""Scratch: the bench's single-graph e2e leg, with and without a sweep created first."""
+"""Scratch probe (GPU box): the bench's single-graph e2e leg, with and without a sweep created first."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

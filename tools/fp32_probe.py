@@ -1,4 +1,4 @@
-"""Scratch: C5 sweep in fp32 mode vs fp64."""
+"""Scratch probe (GPU box): C5 sweep in fp32 mode vs fp64."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -1,4 +1,4 @@
-"""Scratch: where the time of one device interaction round goes (ftp)."""
+"""Scratch probe (GPU box): where the time of one device interaction round goes (ftp)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

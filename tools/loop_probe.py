@@ -1,4 +1,4 @@
-"""Scratch: time the device-resident interaction loop (rounds until every true alarm is revealed)."""
+"""Scratch probe (GPU box): time the device-resident interaction loop (rounds until every true alarm is revealed)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -1,4 +1,4 @@
-"""Scratch: time the C5 multi-evidence sweep (ftp, N sets) on one GPU."""
+"""Scratch probe (GPU box): time the C5 multi-evidence sweep (ftp, N sets) on one GPU."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

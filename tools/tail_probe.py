@@ -1,4 +1,4 @@
-"""Scratch: kernel time of the C5 sweep capped at k iterations (tail cost)."""
+"""Scratch probe (GPU box): kernel time of the C5 sweep capped at k iterations (tail cost)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

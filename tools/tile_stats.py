@@ -1,4 +1,4 @@
-"""Scratch: per-32-set tile convergence spread of the C5 sweep (straggler overhead)."""
+"""Scratch probe (GPU box): per-32-set tile convergence spread of the C5 sweep (straggler overhead)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -1,4 +1,4 @@
-"""Scratch: warm the GPU, then time repeated runs of one config."""
+"""Scratch probe (GPU box): warm the GPU, then time repeated runs of one config."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -1,4 +1,4 @@
-"""Scratch: per-phase timeline from HBP_TRACE=1 (phase compute vs barrier)."""
+"""Scratch probe (GPU box): per-phase timeline from HBP_TRACE=1 (phase compute vs barrier)."""
 import ctypes as C, os, sys, time
 os.environ["HBP_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
