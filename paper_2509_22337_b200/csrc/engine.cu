@@ -1296,6 +1296,8 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
     p->grid = (int)std::min<int64_t>(want, g->cluster_grid);
   } else {
     p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
+    if (const char *ge = getenv("HBP_GRID"))  // A/B: force the CTA count
+      p->grid = std::max(1, std::min(atoi(ge), g->coop_blocks));
   }
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();
