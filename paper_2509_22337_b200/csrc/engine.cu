@@ -755,13 +755,17 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
   };
 
   // uniform start: all messages (1, 1), prev P1 = 0.5 (storage.py:91-94, engine.py:557)
+  // PARALL: iteration 1's variable side would only write the normalised
+  // (1, 1) into every vtof slot (no ftov is read, no marginal is due), so the
+  // start writes that constant directly and the phase -- with its barrier --
+  // is skipped
   {
     const int gs = gridDim.x * blockDim.x;
-    if (!parall)
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.E; i += gs) {
-        P.vtof[i] = make_double2(1.0, 1.0);
-        P.ftov[i] = make_double2(1.0, 1.0);
-      }
+    const double c = parall ? (P.normalize ? 0.5 : 1.0) : 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.E; i += gs) {
+      P.vtof[i] = make_double2(c, c);
+      if (!parall) P.ftov[i] = make_double2(1.0, 1.0);
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.p0[i] = 0.5;
     if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
     grid_sync();
@@ -770,18 +774,20 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
   for (int it = 1;; ++it) {
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
-    trace_mark(P, it, 0, 0);
-    exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
-    trace_mark(P, it, 0, 1);
-    if (it > 1) {
-      unsigned long long m = block_max(dmax);
-      if (threadIdx.x == 0) {
-        atomicMax(&P.delta_bits[it - 1], m);
-        if (blockIdx.x == 0 && P.time_limit_ns > 0)
-          P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
+    if (!(parall && it == 1)) {
+      trace_mark(P, it, 0, 0);
+      exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
+      trace_mark(P, it, 0, 1);
+      if (it > 1) {
+        unsigned long long m = block_max(dmax);
+        if (threadIdx.x == 0) {
+          atomicMax(&P.delta_bits[it - 1], m);
+          if (blockIdx.x == 0 && P.time_limit_ns > 0)
+            P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
+        }
       }
+      grid_sync();
     }
-    grid_sync();
     // Stop decision for iteration it-1 (all CTAs passed the barrier, so the
     // flags and delta are final). With two phases per iteration (PARALL)
     // the decision is applied at the end of this iteration instead, so its
