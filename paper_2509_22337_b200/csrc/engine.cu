@@ -138,7 +138,7 @@ __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, doub
                                             unsigned long long &ufkey) {
   if (P.normalize) {
     const double t = add(a0, a1);
-    if (t < kMinMessageSum) {
+    if (__builtin_expect(t < kMinMessageSum, 0)) {
       const unsigned long long key = ((unsigned long long)phase << 33) |
                                      ((unsigned long long)kind << 32) | (unsigned)slot;
       ufkey = key < ufkey ? key : ufkey;
@@ -160,7 +160,7 @@ __device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsign
 __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
                                              unsigned long long &dmax, double prev_p0, int orig) {
   double t = add(q0, q1);
-  if (t < kMinMessageSum) {
+  if (__builtin_expect(t < kMinMessageSum, 0)) {
     atomicOr(&P.uf_marg[it - 1], 1);
     atomicMin(&P.uf_mwhere[it - 1], orig);
   }
