@@ -49,6 +49,7 @@ struct Ctrl {
   int converged;
   int stop;          // 1 converged, 2 max_iterations, 3 time limit, 4 underflow
   unsigned long long t0;
+  unsigned long long last_delta;  // delta bits of the stopping iteration
 };
 
 struct KParams {
@@ -820,6 +821,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       if (s_stop) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
           C->iterations = done;
+          C->last_delta = db;
           C->converged = s_stop == 1;
           C->stop = s_stop;
         }
@@ -893,6 +895,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       if (s_stop) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
           C->iterations = done;
+          C->last_delta = db;
           C->converged = s_stop == 1;
           C->stop = s_stop;
         }
@@ -1414,10 +1417,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   res->iterations = hc.iterations;
   res->converged = hc.converged;
   res->device_ms = ms;
-  unsigned long long last = 0;
-  if (hc.iterations > 0)
-    HBP_CUDA(cudaMemcpy(&last, c.delta_bits + hc.iterations, 8, cudaMemcpyDeviceToHost));
-  std::memcpy(&res->last_delta, &last, 8);
+  std::memcpy(&res->last_delta, &hc.last_delta, 8);
   if (hc.stop == 4) {
     int um = 0, ug = 0, mw = 0;
     unsigned long long where = 0;
@@ -1656,7 +1656,8 @@ hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var,
     hbp::evidence_kernel<<<(n + 255) / 256, 256, 0, s>>>(g->d_ev, g->d_vinv, d_var, d_val, n);
     HBP_CUDA(cudaGetLastError());
   }
-  HBP_CUDA(cudaStreamSynchronize(s));
+  // no host sync: the codes are consumed by the next run on the same stream
+  // (the pageable sources were staged before cudaMemcpyAsync returned)
   return HBP_OK;
 }
 
