@@ -405,3 +405,18 @@ def test_grouping_modes_bitwise_identical(grouping, monkeypatch):
             assert got.marginals.tobytes() == ref.marginals.tobytes()
             assert np.asarray(got.deltas).tobytes() == np.asarray(ref.deltas).tobytes()
     P.engine.clear_device_cache()
+
+
+def test_more_phases_than_the_shared_memory_phase_cache():
+    """avrora under a random-permutation SEQFIX compiles to 660 levels = 1,320
+    phases, past the kernel's 1,024-entry shared-memory phase cache (the rest
+    are read from global memory): still bitwise equal to the oracle."""
+    g, _ = W.graph("avrora")
+    rng = np.random.default_rng(5)
+    order = [g.edge_at(int(i)) for i in rng.permutation(g.num_edges)]
+    sched = Strategy.seqfix(order).compile(g)
+    assert 2 * sched.num_batches > 1024
+    res, o = device_vs_oracle(g, sched, EngineOptions(max_iterations=50, tolerance=1e-6))
+    assert res.iterations == o["iterations"] and res.converged == o["converged"]
+    assert res.marginals.tobytes() == o["marginals"].tobytes()
+    assert np.asarray(res.deltas).tobytes() == o["deltas"].tobytes()
