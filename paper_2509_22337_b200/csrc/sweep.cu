@@ -86,7 +86,9 @@ struct SweepParams {
   unsigned char *ev_alt;
   int *slot2set;              // [S]
   int *res_pos;               // [S] per set: slot | buffer parity << 30 of its final P0
+                              // (alternate buffers: the absolute slot of the level's region)
   int compact;                // 1: pack the running sets when that halves the live tiles
+  int ccap;                   // slots of the alternate P0 / evidence buffers
   int debug;                  // HBP_SWEEP_DEBUG=1: device printf of tail events
   unsigned *bar;              // grid barrier arrivals
   unsigned long long *t0;
@@ -522,6 +524,7 @@ struct SwBufsT {
   double *p0;
   unsigned char *ev;
   int parity;  // 0: the pass's original p0 / ev buffers, 1: the alternates
+  int base;    // first slot of the alternates' region in use (a multiple of 32)
 };
 
 template <typename T>
@@ -1158,6 +1161,7 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   B.p0 = P.p0;
   B.ev = const_cast<unsigned char *>(P.ev);
   B.parity = 0;
+  B.base = 0;
   SwLaneT<T> L[NS];
   bool alive[NS];
   int sidx[NS];  // slots
@@ -1246,14 +1250,28 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
   // buffers swap roles, and the following factor phase rewrites the unary
   // factors' constant messages (the new ftov buffer does not hold them).
   // Inputs: umask / s_nrun / s_nunits from pick_unit(true, done).
-  bool compacted = false;
+  // Compactions go to disjoint regions of the alternate buffers (level 1:
+  // slots [0, ccap/2), level 2: the next ccap/4, level 3: the rest), so no
+  // compaction writes where a stopped set's final P0 lies: each level packs
+  // at most half the previous one's tiles.
+  int ncomp = 0;
+  auto level_base = [&](int l) {
+    const int h = (P.ccap / 2 + 31) & ~31, q = (P.ccap / 4 + 31) & ~31;
+    return l <= 1 ? 0 : (l == 2 ? h : h + q);
+  };
+  auto level_size = [&](int l) {
+    return (l >= 3 ? P.ccap : level_base(l + 1)) - level_base(l);
+  };
   auto maybe_compact = [&](int it) -> bool {
-    if (!P.compact || compacted || S > kMaxCompact) return false;
+    if (!P.compact || ncomp >= 3 || S > kMaxCompact) return false;
     const int nrun = s_nrun, live = s_nunits;
     const int need = (nrun + 32 * NS - 1) / (32 * NS);
     if (P.debug && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
       printf("it %d: running %d sets in %d units (packed: %d)\n", it, nrun, live, need);
-    if (!(nrun > 0 && 2 * need <= live)) return false;
+    if (!(nrun > 0 && 2 * need <= live && need * 32 * NS <= level_size(ncomp + 1))) return false;
+    const int nb = level_base(ncomp + 1);
+    double *p0_dst = P.p0_alt + (size_t)nb * P.V;
+    unsigned char *ev_dst = P.ev_alt + (size_t)nb * P.V;
     // n2o: running slots in ascending order; s2s_old: slot2set before
     for (int i = threadIdx.x; i < S; i += blockDim.x) s2s_old[i] = set_of(i);
     __syncthreads();
@@ -1292,8 +1310,8 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
         const int o = n2o[k];
         const size_t src = ((size_t)(o >> 5) * P.V + row) * 32 + (o & 31);
         const size_t dst = ((size_t)(k >> 5) * P.V + row) * 32 + (k & 31);
-        P.p0_alt[dst] = B.p0[src];
-        P.ev_alt[dst] = B.ev[src];
+        p0_dst[dst] = B.p0[src];
+        ev_dst[dst] = B.ev[src];
       }
     }
     if (blockIdx.x == 0 && blockIdx.y == 0)
@@ -1302,10 +1320,11 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
     T2 *nv = B.ftov;  // holds the packed vtof rows
     B.ftov = B.vtof;
     B.vtof = nv;
-    B.p0 = P.p0_alt;
-    B.ev = P.ev_alt;
+    B.p0 = p0_dst;
+    B.ev = ev_dst;
     B.parity = 1;
-    compacted = true;
+    B.base = nb;
+    ++ncomp;
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(P.nstop + 2, 1u);
     return true;
   };
@@ -1366,14 +1385,14 @@ __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
             const int stop = sw_decide(P, set, done);
             if (stop) {
               P.res_it[set] = done;
-              P.res_pos[set] = slot | (B.parity << 30);
+              P.res_pos[set] = (B.base + slot) | (B.parity << 30);
               P.res_stop[set] = stop;
               atomicAdd(P.nstop, 1u);
             }
           }
         }
       }
-      if (P.compact && !compacted && !final_pass) {
+      if (P.compact && ncomp < 3 && !final_pass) {
         pick_unit(true, done);
         rewrite_unary = maybe_compact(it);
       }
@@ -1881,6 +1900,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   P.ev_alt = sw->d_ev_alt;
   P.slot2set = d_s2s;
   P.res_pos = d_rpos;
+  P.ccap = sw->compact_cap;
   {
     const char *cenv = getenv("HBP_SWEEP_COMPACT");
     P.compact = (sw->d_p0_alt && !(cenv && atoi(cenv) == 0)) ? 1 : 0;  // per pass: S <= compact_cap
