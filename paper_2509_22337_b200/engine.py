@@ -316,8 +316,10 @@ class _DeviceGraph:
     def parall_updates(self, graph: FactorGraph) -> int:
         """sum |s_0| + |t_0| of the PARALL schedule: every edge plus every
         slot of a non-unary factor (schedule.py:293-312)."""
-        deg = np.diff(np.asarray(graph.rowptr, dtype=np.int64))
-        return int(graph.num_edges + deg[deg > 1].sum())
+        if getattr(self, "_parall_updates", None) is None:  # per graph, once
+            deg = np.diff(np.asarray(graph.rowptr, dtype=np.int64))
+            self._parall_updates = int(graph.num_edges + deg[deg > 1].sum())
+        return self._parall_updates
 
     def __del__(self):
         # plans and sweeps first (they hold self.h); the graph goes with the
