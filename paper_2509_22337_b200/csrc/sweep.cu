@@ -598,7 +598,7 @@ __device__ __forceinline__ void sw_marginal_d(const SweepParams &P, double *p0_s
 #define HBP_WS_CONSUMERS 8
 #endif
 #ifndef HBP_WS_RING
-#define HBP_WS_RING 4
+#define HBP_WS_RING 3  // measured on B200: 2 -> 153 ms, 3 -> 133-135 ms, 4 -> 135-136 ms, 5 -> 219 ms (1 CTA/SM)
 #endif
 #ifndef HBP_WS_MINB
 #define HBP_WS_MINB 2
