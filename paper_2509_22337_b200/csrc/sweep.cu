@@ -611,8 +611,14 @@ struct WsCfg {
   static constexpr int threads = 32 * (consumers + 1);
   static constexpr int min_blocks = NS == 1 ? HBP_WS_MINB : 1;
 };
-constexpr int kChR = 32;   // message rows per chunk
-constexpr int kChN = 16;   // nodes per chunk
+#ifndef HBP_WS_CHR
+#define HBP_WS_CHR 32
+#endif
+#ifndef HBP_WS_CHN
+#define HBP_WS_CHN 16
+#endif
+constexpr int kChR = HBP_WS_CHR;  // message rows per chunk
+constexpr int kChN = HBP_WS_CHN;  // nodes per chunk
 constexpr int kRing = HBP_WS_RING;  // chunks in flight per CTA
 constexpr int kPad = 8;    // index arrays are padded so aligned windows stay in bounds
 
