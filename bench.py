@@ -278,7 +278,9 @@ def run_ours_sweep(args) -> None:
     sets = [W.evidence_set(alarms, j) for j in range(n)]
     sel = np.sort(np.asarray(alarms.alarms, dtype=np.int32))
     lo, hi = D.partition(n, world, rank)
-    mine = sets[lo:hi]
+    # the rank's evidence sets as host CSR arrays, built once (like any input
+    # resident in host memory); every step still uploads them
+    mine = P.EvidenceCSR.from_sets(g, sets[lo:hi])
     m = hi - lo
     opts = P.EngineOptions(1000, 1e-9)
     p1 = torch.empty((m, len(sel)), dtype=torch.float64, device=dev)
@@ -404,7 +406,7 @@ def run_ours_sweep(args) -> None:
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(tt.item()) / len(e2e_s),
                 "path": ("paper_2509_22337_b200.run_many_distributed" if multi else
-                         "paper_2509_22337_b200.run_many") + " with host evidence lists"},
+                         "paper_2509_22337_b200.run_many") + " with host evidence (CSR arrays)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}), burst copy",

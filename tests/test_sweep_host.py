@@ -54,3 +54,26 @@ def test_sweep_algorithmic_bytes_formula():
         idx = n * (4 * (V + 1) + 4 * E + 4 * (F + 1) + 4 * E + 16 * F) / 32.0
         got = float(bench.sweep_set_bytes(g, np.array([n]), max_it)[0])
         assert got == fac + var + idx
+
+
+def test_evidence_csr_equals_the_list_form():
+    """EvidenceCSR (run_many's bulk input) is exactly the conversion of the
+    same sets in list / array-pair form; bad CSR and out-of-range variables
+    raise like the list form."""
+    import numpy as np
+    import pytest
+    from paper_2509_22337_b200 import EvidenceCSR, workloads as W
+    from paper_2509_22337_b200.graph import GraphError
+    from paper_2509_22337_b200.sweep import _normalise_sets
+    g, alarms = W.graph("weblech")
+    sets = [W.evidence_set(alarms, j, size=5) for j in range(7)] + [[(3, True), (4, 0)], []]
+    want = _normalise_sets(g, sets)
+    csr = EvidenceCSR.from_sets(g, sets)
+    got = _normalise_sets(g, csr)
+    for a, b in zip(want, got):
+        assert np.array_equal(a, b)
+    assert len(csr) == len(sets)
+    with pytest.raises(ValueError):
+        EvidenceCSR([0, 3], [1, 2], [1, 0])
+    with pytest.raises(GraphError):
+        _normalise_sets(g, EvidenceCSR([0, 1], [g.num_variables], [1]))
