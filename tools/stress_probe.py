@@ -15,6 +15,7 @@ n_graphs = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
 t0 = time.time()
 checked = 0
+ncompact = 0
 for trial in range(n_graphs):
     big = trial % 4 == 0
     g = random_graph(rng, max_vars=400 if big else 30, max_factors=400 if big else 30,
@@ -55,10 +56,11 @@ for trial in range(n_graphs):
         # evidence sweep of the same graph against clamp_evidence + PARALL
         V = g.num_variables
         sets = []
-        for _ in range(int(rng.integers(1, 80))):
+        for _ in range(int(rng.integers(200, 600)) if trial % 8 == 0 else int(rng.integers(1, 80))):
             k = int(rng.integers(0, min(6, V) + 1))
             sets.append([(int(v), bool(rng.integers(0, 2))) for v in rng.choice(V, k, replace=False)])
         sw = P.run_many(g, sets, None, opts)
+        ncompact += sw.compactions
         for j, pairs in enumerate(sets):
             cur = g
             for v, b in pairs:
@@ -71,4 +73,4 @@ for trial in range(n_graphs):
             assert sw.errors[j] is None, (trial, j)
             assert sw.iterations[j] == oo["iterations"], (trial, j)
             assert sw.marginals[j].tobytes() == oo["marginals"].tobytes(), (trial, j)
-print(f"stress ok: {checked} runs checked in {time.time() - t0:.0f} s")
+print(f"stress ok: {checked} runs checked ({ncompact} sweep compactions) in {time.time() - t0:.0f} s")
