@@ -255,3 +255,16 @@ def test_sweep_fp32_mode_with_compaction():
     assert np.abs(r32.p1_select - r64.p1_select).max() < 1e-5
     same = sum(r32.ranked[j].tolist() == r64.ranked[j].tolist() for j in range(len(sets)))
     assert same >= 0.99 * len(sets)
+
+
+def test_sweep_empty_and_csr_inputs():
+    """Zero sets (list or CSR) give empty results; an EvidenceCSR with a
+    duplicated observation equals the same sets in list form, bit for bit."""
+    g, _ = W.graph("weblech")
+    r = P.run_many(g, [])
+    assert len(r.iterations) == 0 and r.marginals.shape == (0, g.num_variables, 2)
+    assert len(P.run_many(g, P.EvidenceCSR([0], [], [])).iterations) == 0
+    a = P.run_many(g, P.EvidenceCSR([0, 0, 2], [5, 5], [1, 1]))
+    b = P.run_many(g, [[], [(5, True), (5, True)]])
+    assert a.marginals.tobytes() == b.marginals.tobytes()
+    assert list(a.iterations) == list(b.iterations) and a.errors == b.errors == [None, None]
