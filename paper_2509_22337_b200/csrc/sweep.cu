@@ -617,6 +617,10 @@ struct WsCfg {
 #ifndef HBP_WS_CHN
 #define HBP_WS_CHN 16
 #endif
+#ifndef HBP_WS_CLAIM
+#define HBP_WS_CLAIM 2
+#endif
+constexpr int kClaim = HBP_WS_CLAIM;  // chunks per claim
 constexpr int kChR = HBP_WS_CHR;  // message rows per chunk
 constexpr int kChN = HBP_WS_CHN;  // nodes per chunk
 constexpr int kRing = HBP_WS_RING;  // chunks in flight per CTA
@@ -942,15 +946,16 @@ __device__ __forceinline__ void ws_produce(const SweepParams &P, const SwBufsT<T
   const int *twin = side == 0 ? (const int *)P.ftov_twin : P.vtof_twin;
   const typename Ar<T>::T2 *msg = side == 0 ? B.ftov : B.vtof;
   if (lane != 0) return;
-  // chunks are claimed two at a time from the CTA row's counter; the next
-  // claim is in flight while the current pair is staged
-  unsigned k = atomicAdd(claim, 2u);
+  // chunks are claimed kClaim at a time from the CTA row's counter; the next
+  // claim is in flight while the current group is staged
+  unsigned k = atomicAdd(claim, (unsigned)kClaim);
   for (;;) {
-    // claim the next pair only if this pair is whole: every claim's result is
-    // then consumed before the producer leaves the phase (no atomic in flight
-    // when the counter is zeroed for a later phase)
-    const unsigned kn = (cfirst + (int)k + 1 < count) ? atomicAdd(claim, 2u) : 0u;
-    for (int h = 0; h < 2; ++h) {
+    // claim the next group only if this group is whole: every claim's result
+    // is then consumed before the producer leaves the phase (no atomic in
+    // flight when the counter is zeroed for a later phase)
+    const unsigned kn =
+        (cfirst + (int)k + kClaim - 1 < count) ? atomicAdd(claim, (unsigned)kClaim) : 0u;
+    for (int h = 0; h < kClaim; ++h) {
       const int c = cfirst + (int)k + h;
       const unsigned slot = seq % kRing;
       mbar_wait(&sh.empty[slot], ((seq / kRing) & 1) ^ 1);
