@@ -180,61 +180,191 @@ def oracle_sets(graph, sets, cores: int, max_it: int, tol: float):
     return upd, time.perf_counter() - t0
 
 
+REF_SITE = os.path.join(ROOT, "baseline", "_ref")  # the UNMODIFIED reference (pip --target)
+FTP_SPEC = (101583, 109592, 8, 0)
+
+
+def cpu_model() -> str:
+    """The host CPU model (lscpu's "Model name"), for the baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.strip().startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def import_reference():
+    """hornbp from baseline/_ref (installed from /root/reference with pip
+    --target; it travels to the GPU box with the snapshot)."""
+    if REF_SITE not in sys.path:
+        sys.path.insert(0, REF_SITE)
+    import hornbp
+
+    return hornbp
+
+
+def ref_flat(R, graph):
+    """A hornbp FactorGraph as the flat arrays the C port reads (canonical
+    factor-major edge order, graph.py:146-150): nothing of this repo's package."""
+    from oracle import orc
+
+    deg = [1 + len(f.body) for f in graph.factors]
+    rowptr = np.zeros(len(deg) + 1, dtype=np.int64)
+    np.cumsum(deg, out=rowptr[1:])
+    vars_ = np.fromiter((v for f in graph.factors for v in (f.head, *f.body)), dtype=np.int32,
+                        count=int(rowptr[-1]))
+    kind = np.fromiter((1 if f.kind is R.FactorKind.OR else 0 for f in graph.factors),
+                       dtype=np.int8, count=len(deg))
+    p1 = np.fromiter((f.p1 for f in graph.factors), dtype=np.float64, count=len(deg))
+    p2 = np.fromiter((f.p2 for f in graph.factors), dtype=np.float64, count=len(deg))
+    return orc.FlatGraph(graph.num_variables, rowptr, vars_, kind, p1, p2)
+
+
+def ref_evidence_set(alarms, j: int, size: int = 8):
+    """C5 set j: default_rng(j).choice(#alarms, 8), sorted,
+    clamped to the ground-truth labels."""
+    pick = np.sort(np.random.default_rng(j).choice(len(alarms), size, replace=False))
+    return (np.asarray(alarms.alarms, dtype=np.int64)[pick],
+            np.asarray(alarms.labels, dtype=bool)[pick])
+
+
+def ref_schedule_arrays(R, graph, sched):
+    """A hornbp Schedule as (s_off, s_edges, t_off, t_edges) canonical indices."""
+    rp = np.zeros(len(graph.factors) + 1, dtype=np.int64)
+    np.cumsum([1 + len(f.body) for f in graph.factors], out=rp[1:])
+
+    def flat(batches):
+        off = np.zeros(len(batches) + 1, dtype=np.int64)
+        np.cumsum([len(b) for b in batches], out=off[1:])
+        idx = np.fromiter((rp[e.factor] + e.slot for b in batches for e in b), dtype=np.int32,
+                          count=int(off[-1]))
+        return off, idx
+
+    s_off, s_e = flat(sched.s_batches)
+    t_off, t_e = flat(sched.t_batches)
+    return s_off, s_e, t_off, t_e
+
+
+def python_reference(R, graph, alarms, cores: int) -> dict:
+    """The reference's own Python engine: hornbp.run on the ftp
+    graph under PARALL, best of 3 with workers=1 (its fastest setting) and once
+    with workers=cores; plus one C5 set end to end through the reference API
+    (8 x clamp_evidence + compile + run + rank_alarms)."""
+    opts = R.EngineOptions(max_iterations=1000, tolerance=1e-9)
+    t0 = time.perf_counter()
+    sched = R.Strategy.parall().compile(graph)
+    compile_s = time.perf_counter() - t0
+    upd = sum(len(b) for b in sched.s_batches) + sum(len(b) for b in sched.t_batches)
+    best, its = None, 0
+    for _ in range(3):
+        t0 = time.perf_counter()
+        r = R.run(graph, sched, opts, workers=1)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+        its = r.iterations
+    t0 = time.perf_counter()
+    r = R.run(graph, sched, opts, workers=cores)
+    many = time.perf_counter() - t0
+    ids, labels = ref_evidence_set(alarms, 0)
+    t0 = time.perf_counter()
+    cur = graph
+    for v, lab in zip(ids.tolist(), labels.tolist()):
+        cur = R.clamp_evidence(cur, int(v), bool(lab))
+    s0 = R.Strategy.parall().compile(cur)
+    r0 = R.run(cur, s0, opts, workers=1)
+    R.rank_alarms(r0.marginals, alarms, ids.tolist())
+    set_s = time.perf_counter() - t0
+    upd0 = sum(len(b) for b in s0.s_batches) + sum(len(b) for b in s0.t_batches)
+    return {
+        "impl": "hornbp (the reference package, baseline/_ref), pure Python/numpy",
+        "c4_parall": {"iterations": its, "updates_per_iteration": upd, "compile_s": compile_s,
+                      "run_s_workers1_best_of_3": best, "updates_per_s_workers1": upd * its / best,
+                      "run_s_workers_cores": many, "workers_cores": cores,
+                      "updates_per_s_workers_cores": upd * its / many},
+        "c5_set0_end_to_end": {"seconds": set_s, "iterations": r0.iterations,
+                               "updates_per_s": upd0 * r0.iterations / set_s,
+                               "what": "8 x clamp_evidence + Strategy.parall().compile + run "
+                                       "(workers=1) + rank_alarms, one set, serial"},
+    }
+
+
 def run_reference(args) -> None:
+    """The reference arm. Imports nothing from this repo's package: the graph
+    and evidence come from the reference's own generator (hornbp.synth, from
+    baseline/_ref), the timed engine is the C port of hornbp's CPU path
+    (oracle/, pinned bit-for-bit to hornbp), and the reference's own Python
+    engine is timed beside it."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import orc
-    from paper_2509_22337_b200 import workloads as W
 
+    R = import_reference()
     cores = os.cpu_count() or 1
+    graph, alarms = R.generate(R.SynthSpec(*FTP_SPEC))
+    fg = ref_flat(R, graph)
     if args.workload in ("c4", "c4-seqfix"):
         key = "C4-SEQFIX" if args.workload == "c4-seqfix" else "C4-PARALL"
-        w = W.build(key)
-        sched = w.strategy.compile(w.graph)
-        arrs = sched.arrays(w.graph)
-        upd = sched.updates_per_iteration()
+        strat = R.Strategy.seqfix() if args.workload == "c4-seqfix" else R.Strategy.parall()
+        arrs = ref_schedule_arrays(R, graph, strat.compile(graph))
+        upd = len(arrs[1]) + len(arrs[3])
         for _ in range(args.warmup):
-            orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
+            orc.run(fg, arrs, 1000, 1e-9, threads=cores)
         times, iters = [], []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            o = orc.run(w.graph, arrs, w.max_iterations, w.tolerance, threads=cores)
+            o = orc.run(fg, arrs, 1000, 1e-9, threads=cores)
             times.append(time.perf_counter() - t0)
             iters.append(o["iterations"])
         value = upd * sum(iters) / sum(times)
-        config = {"workload": f"{key}: ftp SynthSpec(101583,109592,8,0), {w.strategy.kind}, "
-                              f"tol {w.tolerance}, run to convergence",
+        config = {"workload": f"{key}: ftp SynthSpec(101583,109592,8,0), "
+                              f"{'SEQFIX' if 'SEQ' in key else 'PARALL'}, tol 1e-9, run to convergence",
                   "iterations": iters[-1], "updates_per_iteration": upd}
-        sample = f"{args.steps} full {key} runs (C oracle, OpenMP over {cores} threads)"
+        sample = f"{args.steps} full {key} runs (C port, OpenMP over {cores} threads)"
         ms = 1e3 * sum(times) / args.steps
     else:
-        g, alarms = W.graph("ftp")
         n = args.sets
         per_step = cores  # one set per core per step: a bounded sample of the sweep
-        steps_sets = [[W.evidence_set(alarms, (k * per_step + i) % n) for i in range(per_step)]
+        steps_sets = [[ref_evidence_set(alarms, (k * per_step + i) % n) for i in range(per_step)]
                       for k in range(args.warmup + args.steps)]
         for k in range(args.warmup):
-            oracle_sets(g, steps_sets[k], cores, 1000, 1e-9)
+            oracle_sets(fg, steps_sets[k], cores, 1000, 1e-9)
         tot_upd, tot_s = 0, 0.0
         for k in range(args.warmup, args.warmup + args.steps):
-            u, s = oracle_sets(g, steps_sets[k], cores, 1000, 1e-9)
+            u, s_ = oracle_sets(fg, steps_sets[k], cores, 1000, 1e-9)
             tot_upd += u
-            tot_s += s
+            tot_s += s_
         value = tot_upd / tot_s
         config = sweep_config(n, args.gpus)
         sample = (f"{args.steps} steps x {per_step} evidence sets (sets "
-                  f"{args.warmup * per_step % n}..), one set per core, C oracle single-threaded runs")
+                  f"{args.warmup * per_step % n}..), one set per core, C port single-threaded runs "
+                  "(clamp + PARALL compile + run)")
         ms = 1e3 * tot_s / args.steps
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if args.workload == "sweep" else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (hornbp.synth.generate, the "
+        "reference's own generator)", "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if os.environ.get("HBP_BENCH_NO_PYREF") != "1":
+        line["python_reference"] = python_reference(R, graph, alarms, cores)
+    # the arm must not have touched the product (its native library included)
+    assert not any(m.split(".")[0] == "paper_2509_22337_b200" for m in sys.modules), \
+        "reference arm imported the product package"
     print(json.dumps(line), flush=True)
 
 

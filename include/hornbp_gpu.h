@@ -131,7 +131,11 @@ typedef struct {
   double last_delta;
   int32_t underflow_kind;     /* 0 none, 1 variable-to-factor, 2 factor-to-variable, 3 marginal */
   int32_t underflow_iteration;
-  int64_t underflow_index;    /* vtof/ftov canonical position or variable id */
+  int64_t underflow_index;    /* the reference's UnderflowError index (engine.py:155-165,
+                                 512-518): rows[argmin(total)] of the first failing pass --
+                                 vtof store position (= canonical edge), ftov store position
+                                 (MessageStore order, storage.py:55-63; of the clamped graph
+                                 when evidence is set), or variable id */
   double device_ms;           /* kernel time of the iteration loop (CUDA events) */
   double total_ms;            /* hbp_run wall time incl. copies              */
 } hbp_result;
@@ -141,6 +145,11 @@ typedef struct {
  * history_out: host [max_iterations][V][2] or NULL. */
 hbp_status hbp_run(hbp_plan *p, const hbp_options *opt, double *marginals_out,
                    double *deltas_out, double *history_out, hbp_result *res);
+
+/* History of the last run on this graph (record_history): out [iterations][V][2]
+ * float64, iterations <= the run's. Lets a caller size the buffer by the
+ * iterations actually run (engine.py:574-575) instead of max_iterations. */
+hbp_status hbp_graph_history(hbp_graph *g, int32_t iterations, double *out);
 
 /* Device-resident variant for benchmarking / composition: marginals stay on
  * the device (device pointer of [V][2] float64 returned), no D2H copy. */
@@ -209,7 +218,8 @@ typedef struct {
   int32_t iterations;
   int32_t converged;
   double last_delta;
-  int32_t underflow_kind;  /* 0 none, 1 vtof, 2 ftov (index = canonical edge), 3 marginal (variable) */
+  int32_t underflow_kind;  /* 0 none, 1 vtof, 2 ftov, 3 marginal; index as hbp_result's, for
+                              clamp_evidence(G, set j) (fp32 sets: fp64 re-run's, else -1) */
   int32_t underflow_iteration;
   int64_t underflow_index;
 } hbp_set_result;

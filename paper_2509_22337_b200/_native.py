@@ -152,6 +152,7 @@ def lib() -> C.CDLL:
             "hbp_plan_create": (C.c_int32, [vp, C.c_int64, i64p, i32p, i64p, i32p, C.POINTER(vp)]),
             "hbp_plan_destroy": (None, [vp]),
             "hbp_run": (C.c_int32, [vp, C.POINTER(Options), f64p, f64p, f64p, C.POINTER(Result)]),
+            "hbp_graph_history": (C.c_int32, [vp, C.c_int32, f64p]),
             "hbp_run_device": (C.c_int32, [vp, C.POINTER(Options), C.POINTER(Result),
                                            C.POINTER(C.c_void_p)]),
             "hbp_pass": (C.c_int32, [vp, C.c_int32, C.c_int64, i32p, C.c_int32, f64p, f64p,
@@ -178,7 +179,7 @@ def lib() -> C.CDLL:
 EXPORTED = ("hbp_compile", "hbp_toposort", "hbp_schedule_sizes", "hbp_schedule_copy",
             "hbp_schedule_destroy", "hbp_graph_create", "hbp_graph_destroy", "hbp_graph_set_stream", "hbp_graph_set_evidence",
             "hbp_graph_rank", "hbp_graph_layout", "hbp_graph_layout_check",
-            "hbp_plan_create", "hbp_plan_destroy", "hbp_run", "hbp_run_device", "hbp_pass",
+            "hbp_plan_create", "hbp_plan_destroy", "hbp_run", "hbp_graph_history", "hbp_run_device", "hbp_pass",
             "hbp_marginals", "hbp_sweep_create", "hbp_sweep_capacity", "hbp_sweep_run",
             "hbp_sweep_destroy", "hbp_last_launch_count", "hbp_selftest_division", "hbp_last_error",
             "hbp_version")

@@ -63,6 +63,8 @@ struct hbp_graph {
   // evidence (clamp_evidence without a graph rebuild) + ranking scratch
   unsigned char *d_ev = nullptr;
   bool has_ev = false;
+  std::vector<int32_t> ev_var;  // the clamps in order (host): row lengths / positions of
+  std::vector<int8_t> ev_val;   // the clamped graph for the underflow attribution
   int *d_vinv = nullptr;
   void *d_rank = nullptr;
   size_t rank_cap = 0;
@@ -73,6 +75,7 @@ struct hbp_graph {
   size_t ctrl_cap = 0;  // entries per array
   double2 *d_hist = nullptr;
   size_t hist_cap = 0;  // double2 entries
+  int hist_valid = 0;   // iterations of history the last run left in d_hist
   unsigned long long *d_trace = nullptr;
   size_t trace_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -105,10 +108,20 @@ struct hbp_plan {
   int *d_items = nullptr;
   int grid = 1;
   int csize = 1;  // CTAs of cluster 0 (small levels); 1 = no cluster launch
+  // the schedule as given (reference batch order), for the exact underflow
+  // attribution: device [s_edges | t_edges] (stream-ordered pool) + host offsets
+  int *d_sched = nullptr;
+  int64_t ns = 0;
+  std::vector<int64_t> s_off, t_off;
+  // evidence codes emulate clamp_evidence only for schedules whose batches do
+  // not change under clamping: one batch (PARALL) or canonical SEQFIX.
+  // -1 = not checked yet (checked on the first run with evidence)
+  int ev_ok = -1;
   ~hbp_plan() {
     cudaSetDevice(g->device);
     for (void *p : {(void *)d_phases, (void *)d_items})
       if (p) cudaFree(p);
+    if (d_sched) cudaFreeAsync(d_sched, g->stream);
   }
 };
 

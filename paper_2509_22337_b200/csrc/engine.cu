@@ -88,13 +88,18 @@ struct KParams {
   int *uf_mwhere;                  // [max_it + 2] smallest underflowing variable
   unsigned long long *uf_where;    // [max_it + 2] (phase<<33 | kind<<32 | slot)
   int *tflag;                      // [max_it + 2]
-  double2 *hist;                   // [max_it][V] or null
+  double2 *hist;                   // [hist_iters][V] or null
+  int hist_iters;                  // iterations the history buffer holds
   unsigned long long *trace;       // debug: [kTraceIters][nphases][grid][2] or null
   int csize;                       // CTAs of cluster 0, which runs the small levels
   int max_it;
   int normalize;
   double tol;
   long long time_limit_ns;
+  // underflow attribution re-run: stop at the START of phase halt_phase of
+  // iteration halt_it (0: run normally), leaving that phase's inputs intact
+  int halt_it, halt_phase;
+  const int *canon2v;         // canonical edge -> internal vtof slot (attribution)
 };
 
 // --------------------------------------------------------------------------------------
@@ -161,9 +166,12 @@ __device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsign
 __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
                                              unsigned long long &dmax, double prev_p0, int orig) {
   double t = add(q0, q1);
-  if (__builtin_expect(t < kMinMessageSum, 0)) {
-    atomicOr(&P.uf_marg[it - 1], 1);
-    atomicMin(&P.uf_mwhere[it - 1], orig);
+  // the reference raises iff min(total) < 1e-300 (engine.py:512-518); numpy's
+  // min propagates NaN, so one NaN total anywhere in the pass suppresses the
+  // raise: bit0 = some total below the bound, bit1 = some total NaN
+  if (__builtin_expect(!(t >= kMinMessageSum), 0)) {
+    atomicOr(&P.uf_marg[it - 1], t != t ? 2 : 1);
+    if (t == t) atomicMin(&P.uf_mwhere[it - 1], orig);
   }
   const double p0 = div_rn(q0, t);
   const double p1 = sub(1.0, p0);
@@ -177,7 +185,7 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
   dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
   P.p0[v] = p0;
   if (P.marg_direct) P.marg[orig] = make_double2(p0, p1);
-  if (P.hist) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
+  if (P.hist && it - 2 < P.hist_iters) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
 }
 
 // the clamp factors' messages (1,0) / (0,1), exact multiplications by 0 and 1
@@ -775,6 +783,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
   for (int it = 1;; ++it) {
     const bool final_pass = it == P.max_it + 1;
     unsigned long long dmax = 0;
+    if (it == P.halt_it && P.halt_phase == 0) return;  // attribution re-run
     if (!(parall && it == 1)) {
       trace_mark(P, it, 0, 0);
       exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
@@ -808,7 +817,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       db = ((const volatile unsigned long long *)P.delta_bits)[done];
     }
     auto decide = [&]() -> int {
-      if (ufm || ufg) return 4;
+      if (ufm || ufg == 1) return 4;  // ufg bit1 (a NaN total) suppresses the raise
       if (__longlong_as_double((long long)db) < P.tol) return 1;
       if (done == P.max_it) return 2;
       if (tf) return 3;
@@ -847,6 +856,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
           sync_point(C, sy, P.csize, in0, true);
         }
       }
+      if (it == P.halt_it && p == P.halt_phase) return;  // attribution re-run
       // Look-ahead for levelled schedules: the next list phase's first item
       // of this thread is copied into shared memory now (cp.async: no
       // register waits on it) and, once this phase is done, its slot word and
@@ -931,6 +941,98 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   flush_underflow(P, 1, ufkey);
 }
 
+// ---- exact underflow attribution (engine.py:155-165, :512-518) ------------------------
+// The reference raises in the FIRST failing pass of a batch -- vtof(t_b), then
+// the AND-body, AND-head, OR-body, OR-head groups of s_b (_FTOV_RUNNERS) --
+// naming rows[argmin(total)], the rows being that pass's targets stable-sorted
+// by descending row length (_compile_pass, engine.py:137-138): so the winner
+// is the minimum of (total, -row length, position in the batch). The run
+// stops at the start of the failing phase (halt_it / halt_phase), whose inputs
+// are then still intact, and this kernel recomputes every target's total in
+// the run kernels' exact arithmetic. Two launches: (1) the minimum total per
+// group, (2) among the targets at that total, the minimum (-rowlen, position).
+
+// total of the vtof message owned by ftov slot q (v_item without the write)
+__device__ double attr_vtof_total(const KParams &P, int q, int it, int &var) {
+  const int2 w = P.vslot[q];
+  const int d = w.y >> 16, j = w.y & 0xffff;
+  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
+  v_row_long(P, q - j, d, j, false, a0, a1, q0, q1);
+  const unsigned code = P.ev ? P.ev[w.x] : 0u;
+  if (code && it > 1) apply_clamp(code, a0, a1);
+  var = w.x;
+  return add(a0, a1);
+}
+
+// total of the ftov message owned by vtof slot p (f_item without the write)
+__device__ double attr_ftov_total(const KParams &P, int p, int &group, int &deg) {
+  const int2 w = P.fslot[p];
+  const int d = w.y >> 16, j = w.y & 0xffff;
+  const double2 pp = P.fpar[w.x];
+  const bool is_or = factor_is_or(P, w.x);
+  double b1 = 1.0, b2 = 1.0, o0, o1;
+  if (!is_or) {
+    f_row_long<0>(P, p - j, d, j, pp, b1, b2);
+    if (j == 0) head_message<0>(pp.x, pp.y, b1, b2, o0, o1);
+    else body_message<0>(pp.x, pp.y, b1, b2, o0, o1);
+  } else {
+    f_row_long<1>(P, p - j, d, j, pp, b1, b2);
+    if (j == 0) head_message<1>(pp.x, pp.y, b1, b2, o0, o1);
+    else body_message<1>(pp.x, pp.y, b1, b2, o0, o1);
+  }
+  group = (is_or ? 2 : 0) + (j == 0 ? 1 : 0);
+  deg = d;
+  return add(o0, o1);
+}
+
+// total of internal variable v's marginal (full row, clamps last)
+__device__ double attr_marg_total(const KParams &P, int v) {
+  const int r = P.vrow[v], d = P.vrow[v + 1] - r;
+  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
+  v_row_long(P, r, d, -1, true, a0, a1, q0, q1);
+  const unsigned code = P.ev ? P.ev[v] : 0u;
+  if (code) apply_clamp(code, q0, q1);
+  return add(q0, q1);
+}
+
+// IEEE order as an unsigned order (negative totals sort first)
+__device__ __forceinline__ unsigned long long ord_key(double t) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(t);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// mode 0: vtof targets list[0..n) (canonical edges, batch order); 1: ftov
+// targets; 2: the marginal pass (n = V, position = original variable id).
+// nclamp: clamp factors per original variable (evidence codes: each adds a
+// slot to its variable's row) or null. tk/sk: [4] per ftov group.
+__global__ void __launch_bounds__(256) uf_attr_kernel(const __grid_constant__ KParams P, int mode,
+                                                      const int *list, int n, int it,
+                                                      const int *nclamp, unsigned long long *tk,
+                                                      unsigned long long *sk, int second) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t;
+  int group = 0, rowlen, pos = i;
+  if (mode == 0) {
+    const int pv = P.canon2v[list[i]];
+    int v;
+    t = attr_vtof_total(P, P.vtof_twin[pv], it, v);
+    rowlen = (P.vrow[v + 1] - P.vrow[v]) + (nclamp ? nclamp[P.vorig[v]] : 0);
+  } else if (mode == 1) {
+    t = attr_ftov_total(P, P.canon2v[list[i]], group, rowlen);
+  } else {
+    t = attr_marg_total(P, i);
+    pos = P.vorig[i];
+    rowlen = (P.vrow[i + 1] - P.vrow[i]) + (nclamp ? nclamp[pos] : 0);
+  }
+  if (t != t) return;  // a NaN total never wins (and suppresses the raise, host side)
+  const unsigned long long key = ord_key(t);
+  if (!second)
+    atomicMin(&tk[group], key);
+  else if (key == tk[group])
+    atomicMin(&sk[group], ((unsigned long long)(0xFFFFFFFFu - (unsigned)rowlen) << 32) | (unsigned)pos);
+}
+
 // Alarm ranking of the last run (ranking.py:83-91): the selection's unlabeled
 // variables (no evidence code) by descending P1, ties by ascending position
 // in the id-sorted selection. One CTA. topk == 1: an argmax reduction;
@@ -946,7 +1048,7 @@ __global__ void __launch_bounds__(1024) rank_kernel(const double2 *marg, const u
     if (i >= nsel) return ~0ull;
     const int v = sel[i];
     if (ev && ev[vinv[v]]) return ~0ull;
-    return ~(unsigned long long)__double_as_longlong(marg[v].y);
+    return rank_key(marg[v].y);
   };
   if (topk == 1) {
     unsigned long long best = ~0ull;
@@ -1101,6 +1203,7 @@ hbp::KParams base_params(hbp_graph *g) {
   P.vtof_twin = g->d_vtof_twin;
   P.ftov_twin = g->d_ftov_twin;
   P.vorig = g->d_vorig;
+  P.canon2v = g->d_canon2v;
   P.V = g->L.V;
   P.F = g->L.F;
   P.E = (int)g->L.E;
@@ -1289,6 +1392,25 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   cudaStream_t s = g->stream;
   if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)))
     return st;
+  // keep the schedule in its reference order for the underflow attribution
+  // (a PARALL-shape batch is already on the device: the shape test's copy)
+  {
+    const int64_t ns = k > 0 ? s_off[k] : 0, nt = k > 0 ? t_off[k] : 0;
+    p->ns = ns;
+    if (k > 0) {
+      p->s_off.assign(s_off, s_off + k + 1);
+      p->t_off.assign(t_off, t_off + k + 1);
+    }
+    HBP_CUDA(cudaMallocAsync((void **)&p->d_sched, (size_t)std::max<int64_t>(1, ns + nt) * 4, s));
+    if (parall) {
+      HBP_CUDA(cudaMemcpyAsync(p->d_sched, g->d_scratch, (size_t)(ns + nt) * 4,
+                               cudaMemcpyDeviceToDevice, s));
+    } else {
+      if (ns) HBP_CUDA(cudaMemcpyAsync(p->d_sched, s_edges, (size_t)ns * 4, cudaMemcpyHostToDevice, s));
+      if (nt)
+        HBP_CUDA(cudaMemcpyAsync(p->d_sched + ns, t_edges, (size_t)nt * 4, cudaMemcpyHostToDevice, s));
+    }
+  }
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
   for (const auto &ph : p->host.phases)
@@ -1315,6 +1437,58 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
 
 void hbp_plan_destroy(hbp_plan *p) { delete p; }
 
+static hbp_status launch_kernel(hbp_plan *p, hbp::KParams &P);
+static hbp_status attribute_underflow(hbp_plan *p, const hbp::KParams &P0, int it, size_t nctrl,
+                               hbp_result *res);
+static hbp_status attribute_pass(hbp_graph *g, const hbp::KParams &P, int mode, const int *list, int n,
+                          int it, int *kind, int64_t *index, int *group_out = nullptr);
+
+// Evidence codes (hbp_graph_set_evidence) equal clamp_evidence only when the
+// clamped graph's schedule is the base schedule with the clamp edges appended
+// to the LAST batch (their ftov messages then first matter from iteration 2,
+// which is what the codes implement): true for a one-batch schedule (PARALL:
+// the clamp edges relate to nothing) and for canonical SEQFIX (the clamp
+// edges end the chain), SURVEY.md 8(a) A2. Any other plan is refused.
+static hbp_status evidence_eligible(hbp_plan *p, bool *ok) {
+  if (p->ev_ok < 0) {
+    const int64_t k = (int64_t)p->s_off.size() - 1;
+    if (k <= 1) {
+      p->ev_ok = 1;
+    } else {
+      hbp_graph *g = p->g;
+      hbp_status st = hbp::ensure_host_layout(g);
+      if (st != HBP_OK) return st;
+      const hbp::HostLayout &L = g->L;
+      const int64_t E = L.E;
+      std::vector<int32_t> before((size_t)std::max<int64_t>(0, E - 1)), after(before.size()),
+          rank((size_t)E);
+      for (int64_t e = 0; e < E; ++e) rank[(size_t)e] = (int32_t)e;
+      for (int64_t e = 0; e + 1 < E; ++e) {
+        before[(size_t)e] = (int32_t)e;
+        after[(size_t)e] = (int32_t)(e + 1);
+      }
+      hbp_graph_desc d{L.V, L.F, E, L.rowptr.data(), L.edge_var.data(), L.kind.data(),
+                       L.p1.data(), L.p2.data()};
+      hbp::Schedule canon;
+      int64_t cyc = -1;
+      if ((st = hbp::compile(d, (int64_t)before.size(), before.data(), after.data(), rank.data(),
+                             canon, &cyc)) != HBP_OK)
+        return st;
+      bool same = canon.s_off == p->s_off && canon.t_off == p->t_off;
+      if (same) {
+        std::vector<int32_t> mine((size_t)(p->ns + p->t_off.back()));
+        if (!mine.empty())
+          HBP_CUDA(cudaMemcpy(mine.data(), p->d_sched, mine.size() * 4, cudaMemcpyDeviceToHost));
+        same = std::equal(canon.s_edges.begin(), canon.s_edges.end(), mine.begin()) &&
+               std::equal(canon.t_edges.begin(), canon.t_edges.end(), mine.begin() + p->ns);
+      }
+      p->ev_ok = same ? 1 : 0;
+    }
+  }
+  *ok = p->ev_ok == 1;
+  return HBP_OK;
+}
+
 static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *res) {
   hbp_graph *g = p->g;
   if (!opt || !res) {
@@ -1335,16 +1509,28 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   }
   HBP_CUDA(cudaSetDevice(g->device));
   const size_t n = (size_t)opt->max_iterations + 2;
-  hbp_status st = ensure_ctrl(g, n);
-  if (st) return st;
-  if ((st = reset_ctrl(g, n))) return st;
-  double2 *hist = nullptr;
-  if (opt->record_history) {
-    size_t need = (size_t)opt->max_iterations * (size_t)std::max(1, g->L.V);
-    if (need * sizeof(double2) > ((size_t)16 << 30)) {
-      hbp::set_error("record_history buffer would exceed 16 GiB");
+  hbp_status st = HBP_OK;
+  if (g->has_ev) {
+    bool ok = false;
+    if ((st = evidence_eligible(p, &ok))) return st;
+    if (!ok) {
+      hbp::set_error("graph evidence needs a PARALL or canonical SEQFIX plan (the schedules "
+                     "clamp_evidence leaves unchanged); clamp the graph and compile instead");
       return HBP_EINVAL;
     }
+  }
+  st = ensure_ctrl(g, n);
+  if (st) return st;
+  if ((st = reset_ctrl(g, n))) return st;
+  // record_history: the device keeps the marginals of the first hist_iters
+  // iterations, a buffer sized by a budget rather than by max_iterations
+  // (the reference appends only the iterations that run, engine.py:574-575);
+  // a run that goes beyond it is re-run -- deterministically -- with a buffer
+  // of exactly its iteration count
+  double2 *hist = nullptr;
+  int hist_iters = 0;
+  auto ensure_hist = [&](int iters) -> hbp_status {
+    const size_t need = (size_t)iters * (size_t)std::max(1, g->L.V);
     if (g->hist_cap < need) {
       if (g->d_hist) cudaFree(g->d_hist);
       g->d_hist = nullptr;
@@ -1353,6 +1539,13 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
       g->hist_cap = need;
     }
     hist = g->d_hist;
+    hist_iters = iters;
+    return HBP_OK;
+  };
+  if (opt->record_history) {
+    const size_t per_it = (size_t)std::max(1, g->L.V) * sizeof(double2);
+    const int budget = (int)std::max<size_t>(32, ((size_t)256 << 20) / per_it);
+    if ((st = ensure_hist(std::min(opt->max_iterations, budget)))) return st;
   }
   CtrlView c = ctrl_view(g->d_ctrl, g->ctrl_cap);
   hbp::KParams P = base_params(g);
@@ -1367,6 +1560,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.uf_where = c.uf_where;
   P.tflag = c.tflag;
   P.hist = hist;
+  P.hist_iters = hist_iters;
   P.ev = g->has_ev ? g->d_ev : nullptr;
   P.trace = nullptr;
   if (getenv("HBP_TRACE")) {
@@ -1385,8 +1579,46 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.time_limit_ns = opt->time_limit > 0 ? (long long)(opt->time_limit * 1e9) : 0;
   if (opt->time_limit > 0 && P.time_limit_ns == 0) P.time_limit_ns = 1;
   P.csize = p->csize;
-  void *args[] = {&P};
+  P.halt_it = 0;
+  P.halt_phase = 0;
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
+  if ((st = launch_kernel(p, P))) return st;
+  HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
+  g_last_launches = 1;
+  hbp::Ctrl hc;
+  HBP_CUDA(cudaMemcpyAsync(&hc, c.ctrl, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
+  HBP_CUDA(cudaStreamSynchronize(g->stream));
+  if (hist && hc.stop != 4 && hc.iterations > hist_iters) {
+    if ((st = ensure_hist(hc.iterations))) return st;
+    P.hist = hist;
+    P.hist_iters = hist_iters;
+    if ((st = reset_ctrl(g, n))) return st;
+    HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
+    if ((st = launch_kernel(p, P))) return st;
+    HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
+    g_last_launches = 2;
+    HBP_CUDA(cudaMemcpyAsync(&hc, c.ctrl, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
+    HBP_CUDA(cudaStreamSynchronize(g->stream));
+  }
+  g->hist_valid = hist ? std::min(hc.iterations, hist_iters) : 0;
+  float ms = 0;
+  HBP_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+  std::memset(res, 0, sizeof(*res));
+  res->iterations = hc.iterations;
+  res->converged = hc.converged;
+  res->device_ms = ms;
+  std::memcpy(&res->last_delta, &hc.last_delta, 8);
+  if (hc.stop == 4) {
+    if ((st = attribute_underflow(p, P, hc.iterations, n, res))) return st;
+    hbp::set_error("underflow");
+    return HBP_EUNDERFLOW;
+  }
+  return HBP_OK;
+}
+
+static hbp_status launch_kernel(hbp_plan *p, hbp::KParams &P) {
+  hbp_graph *g = p->g;
+  void *args[] = {&P};
   if (p->csize > 1) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[2];
@@ -1406,41 +1638,135 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
     HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
                                          g->stream));
   }
-  HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
-  g_last_launches = 1;
-  hbp::Ctrl hc;
-  HBP_CUDA(cudaMemcpyAsync(&hc, c.ctrl, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
-  HBP_CUDA(cudaStreamSynchronize(g->stream));
-  float ms = 0;
-  HBP_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-  std::memset(res, 0, sizeof(*res));
-  res->iterations = hc.iterations;
-  res->converged = hc.converged;
-  res->device_ms = ms;
-  std::memcpy(&res->last_delta, &hc.last_delta, 8);
-  if (hc.stop == 4) {
-    int um = 0, ug = 0, mw = 0;
-    unsigned long long where = 0;
-    const int it = hc.iterations;
-    HBP_CUDA(cudaMemcpy(&um, c.uf_msg + it, 4, cudaMemcpyDeviceToHost));
-    HBP_CUDA(cudaMemcpy(&ug, c.uf_marg + it, 4, cudaMemcpyDeviceToHost));
-    HBP_CUDA(cudaMemcpy(&mw, c.uf_mwhere + it, 4, cudaMemcpyDeviceToHost));
-    HBP_CUDA(cudaMemcpy(&where, c.uf_where + it, 8, cudaMemcpyDeviceToHost));
-    res->underflow_iteration = it;
-    if (um) {
-      const int kind = (int)((where >> 32) & 1);
-      const int32_t pos = (int32_t)(where & 0xFFFFFFFFu);
-      res->underflow_kind = kind == 0 ? 1 : 2;
-      hbp_status hs = hbp::ensure_host_layout(g);
-      if (hs != HBP_OK) return hs;
-      res->underflow_index = kind == 0 ? g->L.vtof2canon[pos] : g->L.ftov2canon[pos];
+  return HBP_OK;
+}
+
+// Reference store position of canonical edge e's factor-to-variable message
+// in the (clamped) graph: storage.py:55-63's variable-major transpose, where
+// each clamp factor appends one slot at the END of its variable's row
+// (graph.py:189-200), shifting every later variable's row.
+static hbp_status ref_ftov_position(hbp_graph *g, int32_t e, int64_t *pos) {
+  hbp_status st = hbp::ensure_host_layout(g);
+  if (st != HBP_OK) return st;
+  const hbp::HostLayout &L = g->L;
+  int64_t q = -1;
+  for (int64_t i = 0; i < L.E && q < 0; ++i)
+    if (L.ref_ftov[i] == e) q = i;
+  const int32_t v = L.edge_var[e];
+  for (int32_t cv : g->ev_var) q += cv < v;
+  *pos = q;
+  return HBP_OK;
+}
+
+// The exact reference underflow report of a run that stopped on underflow at
+// iteration it (engine.py:155-165, :512-518; see uf_attr_kernel).
+static hbp_status attribute_underflow(hbp_plan *p, const hbp::KParams &P0, int it, size_t nctrl,
+                               hbp_result *res) {
+  hbp_graph *g = p->g;
+  cudaStream_t s = g->stream;
+  CtrlView c = ctrl_view(g->d_ctrl, g->ctrl_cap);
+  int um = 0;
+  unsigned long long where = ~0ull;
+  HBP_CUDA(cudaMemcpyAsync(&um, c.uf_msg + it, 4, cudaMemcpyDeviceToHost, s));
+  HBP_CUDA(cudaMemcpyAsync(&where, c.uf_where + it, 8, cudaMemcpyDeviceToHost, s));
+  HBP_CUDA(cudaStreamSynchronize(s));
+  // messages fail before the marginal of the same iteration; the earliest
+  // failing phase is the key's high part
+  const bool marg = um == 0;
+  const int phase = marg ? 0 : (int)(where >> 33);
+  hbp::KParams P = P0;
+  P.halt_it = marg ? it + 1 : it;
+  P.halt_phase = phase;
+  P.time_limit_ns = 0;
+  P.hist = nullptr;
+  P.trace = nullptr;
+  hbp_status st;
+  if ((st = reset_ctrl(g, nctrl))) return st;
+  if ((st = launch_kernel(p, P))) return st;
+  int mode = 2, n = P.V;
+  const int *list = nullptr;
+  if (!marg) {
+    const int b = p->host.phase_batch[phase];
+    if (p->host.phases[phase].type == 0) {
+      mode = 0;
+      list = p->d_sched + p->ns + p->t_off[b];
+      n = (int)(p->t_off[b + 1] - p->t_off[b]);
     } else {
-      res->underflow_kind = 3;
-      res->underflow_index = mw;
+      mode = 1;
+      list = p->d_sched + p->s_off[b];
+      n = (int)(p->s_off[b + 1] - p->s_off[b]);
     }
-    (void)ug;
-    hbp::set_error("underflow");
-    return HBP_EUNDERFLOW;
+  }
+  int kind = 0;
+  int64_t index = -1;
+  if ((st = attribute_pass(g, P, mode, list, n, it, &kind, &index))) return st;
+  if (kind == 0) {
+    hbp::set_error("internal: underflow flagged on the device but no reference pass fails");
+    return HBP_ECUDA;
+  }
+  res->underflow_kind = kind;
+  res->underflow_iteration = it;
+  res->underflow_index = index;
+  return HBP_OK;
+}
+
+// One attribution over a pass whose inputs are on the device (P's buffers):
+// kind 0 = no group of the pass raises, else 1 vtof / 2 ftov / 3 marginal with
+// the reference's index (vtof position = canonical edge, ftov store position,
+// variable id). The ftov passes report the first failing group in
+// _FTOV_RUNNERS order in *group_out (0..3) when non-null.
+static hbp_status attribute_pass(hbp_graph *g, const hbp::KParams &P, int mode, const int *list, int n,
+                          int it, int *kind, int64_t *index, int *group_out) {
+  cudaStream_t s = g->stream;
+  *kind = 0;
+  *index = -1;
+  if (group_out) *group_out = 4;
+  if (n <= 0) return HBP_OK;
+  CtrlView c = ctrl_view(g->d_ctrl, g->ctrl_cap);
+  unsigned long long *tk = (unsigned long long *)((char *)c.ctrl + 256), *sk = tk + 4;
+  HBP_CUDA(cudaMemsetAsync(tk, 0xFF, 64, s));
+  int *d_nclamp = nullptr;
+  if (g->has_ev && !g->ev_var.empty()) {
+    std::vector<int> cnt((size_t)g->L.V, 0);
+    for (int32_t v : g->ev_var) cnt[(size_t)v]++;
+    HBP_CUDA(cudaMalloc(&d_nclamp, cnt.size() * 4));
+    HBP_CUDA(cudaMemcpyAsync(d_nclamp, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice, s));
+  }
+  for (int second = 0; second < 2; ++second)
+    hbp::uf_attr_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, mode, list, n, it, d_nclamp,
+                                                                   tk, sk, second);
+  cudaError_t le = cudaGetLastError();
+  unsigned long long h[8];
+  cudaError_t ce = cudaMemcpyAsync(h, tk, 64, cudaMemcpyDeviceToHost, s);
+  cudaError_t se = cudaStreamSynchronize(s);
+  if (d_nclamp) cudaFree(d_nclamp);
+  HBP_CUDA(le);
+  HBP_CUDA(ce);
+  HBP_CUDA(se);
+  const int ngroups = mode == 1 ? 4 : 1;
+  for (int grp = 0; grp < ngroups; ++grp) {
+    if (h[grp] == ~0ull) continue;  // empty group (or only NaN totals)
+    const unsigned long long u = h[grp];
+    const unsigned long long bits = (u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
+    double t;
+    std::memcpy(&t, &bits, 8);
+    if (!(t < hbp::dev::kMinMessageSum)) continue;
+    const unsigned pos = (unsigned)(h[4 + grp] & 0xFFFFFFFFu);
+    if (group_out) *group_out = grp;
+    if (mode == 2) {
+      *kind = 3;
+      *index = pos;
+      return HBP_OK;
+    }
+    int32_t e = 0;
+    HBP_CUDA(cudaMemcpy(&e, list + pos, 4, cudaMemcpyDeviceToHost));
+    if (mode == 0) {
+      *kind = 1;
+      *index = e;
+      return HBP_OK;
+    }
+    *kind = 2;
+    return ref_ftov_position(g, e, index);
   }
   return HBP_OK;
 }
@@ -1469,6 +1795,20 @@ hbp_status hbp_run(hbp_plan *p, const hbp_options *opt, double *marginals_out, d
   HBP_CUDA(cudaStreamSynchronize(g->stream));
   res->total_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return HBP_OK;
+}
+
+hbp_status hbp_graph_history(hbp_graph *g, int32_t iterations, double *out) {
+  if (!g || iterations < 0 || (iterations > 0 && !out)) {
+    hbp::set_error("bad history arguments");
+    return HBP_EINVAL;
+  }
+  if (iterations > g->hist_valid) {
+    hbp::set_error("the last run recorded fewer iterations of history");
+    return HBP_EINVAL;
+  }
+  if (iterations)
+    HBP_CUDA(cudaMemcpy(out, g->d_hist, (size_t)iterations * g->L.V * 16, cudaMemcpyDeviceToHost));
   return HBP_OK;
 }
 
@@ -1515,7 +1855,7 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
   if (st) return st;
   if ((st = reset_ctrl(g, 4))) return st;
   int *d_items = nullptr;
-  HBP_CUDA(cudaMalloc(&d_items, items.size() * 4));
+  HBP_CUDA(cudaMalloc(&d_items, items.size() * 8));  // [slot items | canonical targets]
   cudaStream_t s = g->stream;
   HBP_CUDA(cudaMemcpyAsync(g->d_vtof, hv.data(), hv.size() * 16, cudaMemcpyHostToDevice, s));
   HBP_CUDA(cudaMemcpyAsync(g->d_ftov, hf.data(), hf.size() * 16, cudaMemcpyHostToDevice, s));
@@ -1538,16 +1878,38 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
   cudaMemcpyAsync(hv.data(), g->d_vtof, hv.size() * 16, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(hf.data(), g->d_ftov, hf.size() * 16, cudaMemcpyDeviceToHost, s);
   cudaError_t se = cudaStreamSynchronize(s);
-  cudaFree(d_items);
   if (le != cudaSuccess || se != cudaSuccess) {
+    cudaFree(d_items);
     hbp::set_error(std::string("pass kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : se));
     return HBP_ECUDA;
   }
+  // The reference raises in the first failing pass (engine.py:155-165): for
+  // the vtof direction before any scatter; for the ftov direction after the
+  // groups that precede the failing one (_FTOV_RUNNERS order) have scattered.
+  int fail_group = 4;
   if (uf) {
-    const int32_t pos = (int32_t)(where & 0xFFFFFFFFu);
-    if (underflow_index) *underflow_index = direction == 0 ? L.vtof2canon[pos] : L.ftov2canon[pos];
-    hbp::set_error("underflow");
-    return HBP_EUNDERFLOW;  // store left untouched, like the reference's raise-before-scatter
+    int kind = 0;
+    int64_t index = -1;
+    hbp_status ast = HBP_OK;
+    if (cudaMemcpy(d_items + n, targets, (size_t)n * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(d_items);
+      hbp::set_error("attribution upload failed");
+      return HBP_ECUDA;
+    }
+    ast = attribute_pass(g, P, direction ? 1 : 0, d_items + n, (int)n, 1, &kind, &index, &fail_group);
+    cudaFree(d_items);
+    if (ast != HBP_OK) return ast;
+    if (kind == 0) {
+      hbp::set_error("internal: underflow flagged on the device but no reference pass fails");
+      return HBP_ECUDA;
+    }
+    if (underflow_index) *underflow_index = index;
+    if (direction == 0) {
+      hbp::set_error("underflow");
+      return HBP_EUNDERFLOW;  // store untouched: the reference raises before its scatter
+    }
+  } else {
+    cudaFree(d_items);
   }
   if (direction == 0) {
     for (int64_t i = 0; i < n; ++i) {
@@ -1561,9 +1923,18 @@ hbp_status hbp_pass(hbp_graph *g, int32_t direction, int64_t n, const int32_t *t
     for (int64_t q = 0; q < L.E; ++q) ref_pos[L.ref_ftov[q]] = (int32_t)q;
     for (int64_t i = 0; i < n; ++i) {
       int32_t e = targets[i];
+      if (fail_group < 4) {  // (kind, head/body) group of e in _FTOV_RUNNERS order
+        const int32_t f = L.edge_factor[e];
+        const int grp = (L.kind[f] == 1 ? 2 : 0) + (e == L.rowptr[f] ? 1 : 0);
+        if (grp >= fail_group) continue;
+      }
       double2 m = hf[L.canon2f[e]];
       ftov0[ref_pos[e]] = m.x;
       ftov1[ref_pos[e]] = m.y;
+    }
+    if (fail_group < 4) {
+      hbp::set_error("underflow");
+      return HBP_EUNDERFLOW;
     }
   }
   return HBP_OK;
@@ -1610,8 +1981,16 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
   HBP_CUDA(cudaMemcpyAsync(&mw, c.uf_mwhere + 1, 4, cudaMemcpyDeviceToHost, s));
   HBP_CUDA(cudaMemcpyAsync(out, g->d_marg, (size_t)L.V * 16, cudaMemcpyDeviceToHost, s));
   HBP_CUDA(cudaStreamSynchronize(s));
-  if (uf) {
-    if (underflow_var) *underflow_var = mw;
+  (void)mw;
+  if (uf == 1) {  // bit1: a NaN total suppresses the raise (numpy min propagates NaN)
+    int kind = 0;
+    int64_t index = -1;
+    if ((st = attribute_pass(g, P, 2, nullptr, L.V, 2, &kind, &index))) return st;
+    if (kind != 3) {
+      hbp::set_error("internal: underflow flagged on the device but no reference pass fails");
+      return HBP_ECUDA;
+    }
+    if (underflow_var) *underflow_var = index;
     hbp::set_error("underflow");
     return HBP_EUNDERFLOW;
   }
@@ -1640,6 +2019,8 @@ hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var,
   if (!g->d_ev) HBP_CUDA(cudaMalloc(&g->d_ev, (size_t)L.V + 4));
   HBP_CUDA(cudaMemsetAsync(g->d_ev, 0, (size_t)L.V + 4, s));
   g->has_ev = n > 0;
+  g->ev_var.assign(var, var + n);
+  g->ev_val.assign(value, value + n);
   if (n > 0) {
     const size_t need = (size_t)n * 5 + 16;
     if (g->ev_list_cap < need) {

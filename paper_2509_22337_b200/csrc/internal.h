@@ -115,6 +115,7 @@ struct PlanHost {
   std::vector<int32_t> items;          // list-mode slot items (both sides)
   int64_t updates_per_iter = 0;        // sum |s_i| + |t_i|
   int32_t max_items = 0;               // largest phase (work items)
+  std::vector<int32_t> phase_batch;    // batch index of each phase (underflow attribution)
 };
 
 // the two whole-graph phases of a PARALL schedule (every edge once on the

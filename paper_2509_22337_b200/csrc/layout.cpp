@@ -233,6 +233,7 @@ void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
   f.grid = nf >= small_threshold;  // smaller phases run on cluster 0 only
   P.phases.push_back(v);
   P.phases.push_back(f);
+  P.phase_batch.assign(2, 0);
   P.max_items = std::max(nv, nf);
 }
 
@@ -265,6 +266,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
   P.updates_per_iter = ns + nt;
   P.phases.clear();
   P.items.clear();
+  P.phase_batch.clear();
   P.max_items = 0;
 
   std::vector<int64_t> stamp((size_t)E, -1);
@@ -274,10 +276,12 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
   int64_t nonunary_total = 0;
   for (int32_t v = 0; v < V; ++v) nonunary_total += L.nonunary[v];
 
+  int32_t cur_batch = 0;
   auto push_phase = [&](Phase ph, int32_t n) {
     ph.grid = n >= small_threshold;  // smaller phases run on cluster 0 only
     P.max_items = std::max(P.max_items, n);
     P.phases.push_back(ph);
+    P.phase_batch.push_back(cur_batch);
   };
 
   // PARALL fast path: one batch holding every edge once and every slot of a
@@ -305,6 +309,7 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
 
   const int64_t levels = std::max<int64_t>(k, 1);
   for (int64_t b = 0; b < levels; ++b) {
+    cur_batch = (int32_t)b;
     // ---------------- variable side: vtof(t_b) (+ marginals in phase 0)
     {
       slots.clear();

@@ -197,7 +197,8 @@ __device__ __forceinline__ void sw_marginal(const SweepParams &P, const SwLane &
                                            double q0, double q1, double prev_p0,
                                            unsigned long long &dmax) {
   const double t = add(q0, q1);
-  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], P.vorig[v]);
+  // NaN totals suppress the raise (numpy's min propagates NaN): they record -1
+  if (!(t >= kMinMessageSum)) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], t != t ? -1 : P.vorig[v]);
   const double p0 = div_rn(q0, t);
   const double p1 = sub(1.0, p0);
   const double prev = it == 2 ? 0.5 : sub(1.0, prev_p0);  // prev P1 starts at 0.5
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __gri
         const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
         const int um = ((const volatile int *)P.ufmarg)[i];
         const int tf = ((const volatile int *)P.tflag)[done];
-        if (uk != ~0ull || um != kNoVar) stop = 4;
+        if (uk != ~0ull || (um != kNoVar && um >= 0)) stop = 4;
         else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
         else if (done == P.max_it) stop = 2;
         else if (tf) stop = 3;
@@ -560,7 +561,8 @@ __device__ __forceinline__ void sw_marginal_d(const SweepParams &P, double *p0_s
                                              int it, double q0, double q1, double prev_p0,
                                              unsigned long long &dmax) {
   const double t = add(q0, q1);
-  if (t < kMinMessageSum) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + set], P.vorig[v]);
+  // NaN totals suppress the raise (numpy's min propagates NaN): they record -1
+  if (!(t >= kMinMessageSum)) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + set], t != t ? -1 : P.vorig[v]);
   const double p0 = div_rn(q0, t);
   const double p1 = sub(1.0, p0);
   const double prev = it == 2 ? 0.5 : sub(1.0, prev_p0);  // prev P1 starts at 0.5
@@ -1124,7 +1126,7 @@ __device__ __forceinline__ int sw_decide(const SweepParams &P, int s, int done) 
   const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
   const int um = ((const volatile int *)P.ufmarg)[i];
   const int tf = ((const volatile int *)P.tflag)[done];
-  if (uk != ~0ull || um != kNoVar) return 4;
+  if (uk != ~0ull || (um != kNoVar && um >= 0)) return 4;  // um -1: a NaN total
   if (__longlong_as_double((long long)db) < P.tol) return 1;
   if (done == P.max_it) return 2;
   if (tf) return 3;
@@ -1529,7 +1531,7 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *
       const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
       if ((par ? ev_alt : ev)[at] == 0) {
         const double p1 = sub(1.0, (double)(par ? p0_alt : p0)[at]);
-        k = ~(unsigned long long)__double_as_longlong(p1);
+        k = rank_key(p1);
       }
     }
     key[i] = k;
@@ -1591,8 +1593,10 @@ struct hbp_sweep {
   void *d_scratch = nullptr;  // evidence lists, selection, staging outputs
   size_t scratch_bytes = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, k0 = nullptr, k1 = nullptr;
+  hbp_plan *parall = nullptr;  // single-graph PARALL plan: exact underflow attribution
   ~hbp_sweep() {
     cudaSetDevice(g->device);
+    if (parall) hbp_plan_destroy(parall);
     for (void *p : {(void *)d_vinv, (void *)d_vtof, (void *)d_ftov, (void *)d_p0, (void *)d_ev,
                     (void *)d_p0_alt, (void *)d_ev_alt,
                     d_ctrl, d_scratch, (void *)d_vrow, (void *)d_frow, (void *)d_vtof_twin,
@@ -1617,6 +1621,56 @@ hbp_status ensure(void **p, size_t *cap, size_t need) {
   HBP_CUDA(cudaMalloc(p, need));
   *cap = need;
   return HBP_OK;
+}
+
+// The exact reference underflow report of sweep set j (engine.py:155-165,
+// :512-518): the set re-runs on the single-graph executor with its evidence
+// codes -- the same fp64 arithmetic, so the same stop -- which halts at the
+// failing pass and attributes it there (engine.cu attribute_underflow). The
+// re-run uses the graph's own single-run buffers and restores its evidence.
+// fp32 sets (no bitwise contract) keep the sweep's own report unless the fp64
+// re-run stops on underflow at the same iteration.
+hbp_status attribute_set(hbp_sweep *sw, const hbp_options *opt, const hbp_evidence *ev, int j,
+                         bool fp32, hbp_set_result *r) {
+  hbp_graph *g = sw->g;
+  const hbp::HostLayout &L = g->L;
+  if (!sw->parall) {
+    std::vector<int32_t> se((size_t)L.E), te;
+    te.reserve((size_t)L.E);
+    for (int64_t e = 0; e < L.E; ++e) {
+      se[(size_t)e] = (int32_t)e;
+      const int32_t f = L.edge_factor[(size_t)e];
+      if (L.rowptr[(size_t)f + 1] - L.rowptr[(size_t)f] > 1) te.push_back((int32_t)e);
+    }
+    const int64_t so[2] = {0, L.E}, to[2] = {0, (int64_t)te.size()};
+    hbp_status st = hbp_plan_create(g, 1, so, se.data(), to, te.data(), &sw->parall);
+    if (st != HBP_OK) return st;
+  }
+  const std::vector<int32_t> keep_var = g->ev_var;
+  const std::vector<int8_t> keep_val = g->ev_val;
+  const bool keep_has = g->has_ev;
+  const int64_t a = ev->offsets[j], b = ev->offsets[j + 1];
+  hbp_status st = hbp_graph_set_evidence(g, (int32_t)(b - a), ev->var + a, ev->value + a);
+  if (st != HBP_OK) return st;
+  hbp_options o = *opt;
+  o.precision = 0;
+  o.record_history = 0;
+  hbp_result res;
+  std::memset(&res, 0, sizeof(res));
+  const hbp_status rs = hbp_run_device(sw->parall, &o, &res, nullptr);
+  st = hbp_graph_set_evidence(g, keep_has ? (int32_t)keep_var.size() : 0, keep_var.data(),
+                              keep_val.data());
+  if (st != HBP_OK) return st;
+  if (rs == HBP_EUNDERFLOW && res.underflow_iteration == r->underflow_iteration) {
+    r->underflow_kind = res.underflow_kind;
+    r->underflow_index = res.underflow_index;
+    return HBP_OK;
+  }
+  if (rs != HBP_OK && rs != HBP_EUNDERFLOW) return rs;
+  if (fp32) return HBP_OK;
+  hbp::set_error("internal: sweep set " + std::to_string(j) +
+                 " underflowed but its single-graph re-run did not stop there");
+  return HBP_ECUDA;
 }
 
 }  // namespace
@@ -1931,6 +1985,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
   std::vector<signed char> h_ev_val;
   int64_t launches = 0;
   int passes = 0, compactions = 0;
+  std::vector<int> uf_sets;  // sets that stopped on underflow (exact attribution below)
   double dev_ms = 0, ker_ms = 0;
   for (int base = 0; base < n; base += cap) {
     const int ns = std::min(cap, n - base);
@@ -2072,18 +2127,23 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       if (h_rs[j] == 4) {
         r.underflow_iteration = it;
         const unsigned long long key = h_uk[(size_t)it * S + j];
-        if (key != ~0ull) {
+        if (key != ~0ull) {  // the sweep's own report (kept for fp32 sets only)
           const int kind = (int)(key >> 32);
           const int32_t pos = (int32_t)(key & 0xffffffffu);
           r.underflow_kind = kind == 0 ? 1 : 2;
-          r.underflow_index = kind == 0 ? L.vtof2canon[pos] : L.ftov2canon[pos];
+          r.underflow_index = kind == 0 ? L.vtof2canon[pos] : -1;
         } else {
           r.underflow_kind = 3;
           r.underflow_index = h_um[(size_t)it * S + j];
         }
+        uf_sets.push_back(base + j);
       }
     }
     ++passes;
+  }
+  for (int j : uf_sets) {
+    hbp_status st = attribute_set(sw, opt, ev, j, fp32, &out->sets[j]);
+    if (st != HBP_OK) return st;
   }
   out->device_ms = dev_ms;
   out->kernel_ms = ker_ms;

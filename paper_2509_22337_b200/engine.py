@@ -42,7 +42,31 @@ _native.lib()  # fail loudly at import if the engine library is missing
 
 class UnderflowError(RuntimeError):
     """A message or marginal degenerated to total mass zero
-    (usually contradictory evidence on connected variables)."""
+    (usually contradictory evidence on connected variables).
+
+    Beyond the reference's message, raised instances carry ``kind`` (1
+    variable-to-factor, 2 factor-to-variable, 3 marginal), ``iteration`` (0
+    for the single-pass API) and ``index``: the reference's own report --
+    the vtof store position, the ftov store position, or the variable id of
+    ``rows[argmin(total)]`` in the first failing pass (engine.py:155-165,
+    :512-518)."""
+
+    kind: int = 0
+    iteration: int = 0
+    index: int = -1
+
+
+def _underflow_error(kind: int, index: int, iteration: int = 0) -> UnderflowError:
+    """The reference's UnderflowError text (engine.py:159-164, :515-518)."""
+    if kind == 1:
+        msg = f"variable-to-factor message degenerated to zero mass at {index} (contradictory evidence?)"
+    elif kind == 2:
+        msg = f"factor-to-variable message degenerated to zero mass at {index} (contradictory evidence?)"
+    else:
+        msg = f"marginal of variable {index} degenerated to zero mass (contradictory evidence?)"
+    exc = UnderflowError(msg)
+    exc.kind, exc.index, exc.iteration = int(kind), int(index), int(iteration)
+    return exc
 
 
 class OpCounter:
@@ -115,22 +139,8 @@ def _raise_status(status: int, what: str, result: Optional[_native.Result] = Non
                   graph: Optional[FactorGraph] = None):
     msg = _native.last_error()
     if status == _native.HBP_EUNDERFLOW and result is not None:
-        kind = result.underflow_kind
-        idx = int(result.underflow_index)
-        if kind == 1:
-            raise UnderflowError(f"variable-to-factor message degenerated to zero mass at {idx} "
-                                 "(contradictory evidence?)")
-        if kind == 2:
-            pos = idx
-            if graph is not None:
-                rp, ved = graph._var_csr()
-                inv = np.empty(len(ved), dtype=np.int64)
-                inv[ved] = np.arange(len(ved))
-                pos = int(inv[idx])
-            raise UnderflowError(f"factor-to-variable message degenerated to zero mass at {pos} "
-                                 "(contradictory evidence?)")
-        raise UnderflowError(f"marginal of variable {idx} degenerated to zero mass "
-                             "(contradictory evidence?)")
+        raise _underflow_error(result.underflow_kind, int(result.underflow_index),
+                               result.underflow_iteration)
     if status in (_native.HBP_EINVAL, _native.HBP_ECYCLE):
         raise ValueError(f"{what}: {msg}")
     if status == _native.HBP_ENOMEM:
@@ -200,16 +210,18 @@ class _Plan:
         opt = self.options(options)
         marg = np.empty((V, 2), dtype=np.float64)
         deltas = np.empty(options.max_iterations, dtype=np.float64)
-        hist = (np.empty((options.max_iterations, V, 2), dtype=np.float64)
-                if options.record_history else None)
         res = _native.Result()
         st = _native.lib().hbp_run(self.handle, C.byref(opt), _native.ptr(marg, C.c_double),
-                                   _native.ptr(deltas, C.c_double),
-                                   None if hist is None else _native.ptr(hist, C.c_double),
-                                   C.byref(res))
+                                   _native.ptr(deltas, C.c_double), None, C.byref(res))
         if st != _native.HBP_OK:
             _raise_status(st, "hbp_run", res, graph)
         n = res.iterations
+        hist = None
+        if options.record_history:  # sized by the iterations run (engine.py:574-575)
+            hist = np.empty((n, V, 2), dtype=np.float64)
+            st = _native.lib().hbp_graph_history(self.dg.handle, n, _native.ptr(hist, C.c_double))
+            if st != _native.HBP_OK:
+                _raise_status(st, "hbp_graph_history")
         return InferenceResult(
             marginals=marg, converged=bool(res.converged), iterations=n,
             last_delta=float(res.last_delta), deltas=deltas[:n].tolist(),
@@ -392,11 +404,7 @@ def _store_pass(store: MessageStore, direction: int, targets: np.ndarray, normal
                                 _native.ptr(store.ftov0, C.c_double),
                                 _native.ptr(store.ftov1, C.c_double), C.byref(where))
     if st == _native.HBP_EUNDERFLOW:
-        if direction == 0:
-            raise UnderflowError(f"variable-to-factor message degenerated to zero mass at "
-                                 f"{int(where.value)} (contradictory evidence?)")
-        raise UnderflowError(f"factor-to-variable message degenerated to zero mass at "
-                             f"{int(store.vtof_to_ftov[where.value])} (contradictory evidence?)")
+        raise _underflow_error(1 if direction == 0 else 2, int(where.value))
     if st != _native.HBP_OK:
         _raise_status(st, "hbp_pass")
 
@@ -494,8 +502,7 @@ def compute_marginals(store: MessageStore) -> np.ndarray:
                                      _native.ptr(f1, C.c_double), _native.ptr(out, C.c_double),
                                      C.byref(bad))
     if st == _native.HBP_EUNDERFLOW:
-        raise UnderflowError(f"marginal of variable {int(bad.value)} degenerated to zero mass "
-                             "(contradictory evidence?)")
+        raise _underflow_error(3, int(bad.value))
     if st != _native.HBP_OK:
         _raise_status(st, "hbp_marginals")
     return out

@@ -26,7 +26,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from . import _native
-from .engine import EngineOptions, UnderflowError, device_graph, run
+from .engine import EngineOptions, UnderflowError, _underflow_error, device_graph, run
 from .graph import FactorGraph, GraphError, clamp_evidence
 from .schedule import Strategy
 
@@ -97,6 +97,24 @@ class EvidenceCSR:
     def __len__(self) -> int:
         return len(self.offsets) - 1
 
+    def __getitem__(self, key):
+        """A slice of sets is an EvidenceCSR (re-based offsets, views of the
+        arrays); an integer is set j as a list of (variable, observed) pairs."""
+        if isinstance(key, slice):
+            lo, hi, step = key.indices(len(self))
+            if step != 1:
+                raise ValueError("EvidenceCSR slices must be contiguous")
+            hi = max(lo, hi)
+            a, b = int(self.offsets[lo]), int(self.offsets[hi])
+            return EvidenceCSR(self.offsets[lo:hi + 1] - a, self.var[a:b], self.val[a:b])
+        j = int(key)
+        if j < 0:
+            j += len(self)
+        if not 0 <= j < len(self):
+            raise IndexError("evidence set index out of range")
+        a, b = int(self.offsets[j]), int(self.offsets[j + 1])
+        return [(int(v), bool(o)) for v, o in zip(self.var[a:b].tolist(), self.val[a:b].tolist())]
+
 
 def _normalise_sets(graph: FactorGraph, evidence_sets) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """Evidence sets -> (offsets, var, value). A set is an iterable of
@@ -132,18 +150,6 @@ def _normalise_sets(graph: FactorGraph, evidence_sets) -> tuple[np.ndarray, np.n
     return offsets, var.astype(np.int32), val.astype(np.int8)
 
 
-def _underflow(kind: int, idx: int, graph: FactorGraph) -> UnderflowError:
-    if kind == 1:
-        return UnderflowError(f"variable-to-factor message degenerated to zero mass at {idx} "
-                              "(contradictory evidence?)")
-    if kind == 2:
-        rp, ved = graph._var_csr()
-        inv = np.empty(len(ved), dtype=np.int64)
-        inv[ved] = np.arange(len(ved))
-        return UnderflowError(f"factor-to-variable message degenerated to zero mass at "
-                              f"{int(inv[idx])} (contradictory evidence?)")
-    return UnderflowError(f"marginal of variable {idx} degenerated to zero mass "
-                          "(contradictory evidence?)")
 
 
 def _is_parall(strategy) -> bool:
@@ -228,7 +234,8 @@ def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Str
     errors: list[Optional[UnderflowError]] = []
     for j in range(n):
         k = res[j].underflow_kind
-        errors.append(None if k == 0 else _underflow(k, int(res[j].underflow_index), graph))
+        errors.append(None if k == 0 else _underflow_error(k, int(res[j].underflow_index),
+                                                            res[j].underflow_iteration))
     base_upd = dg.parall_updates(graph)
     return SweepResult(
         iterations=its,

@@ -101,8 +101,9 @@ def test_random_graphs_bitwise_vs_oracle():
                              normalize_messages=bool(trial % 5 != 2))
         o = orc.run(g, sched.arrays(g), opts.max_iterations, opts.tolerance, opts.normalize_messages)
         if o["underflow"] is not None:
-            with pytest.raises(UnderflowError):
+            with pytest.raises(UnderflowError) as ei:
                 P.run(g, sched, opts)
+            assert (ei.value.kind, ei.value.iteration, ei.value.index) == o["underflow"], trial
             continue
         res = P.run(g, sched, opts)
         assert res.iterations == o["iterations"], trial
@@ -181,6 +182,24 @@ def test_history_matches_oracle_prefixes():
     for i, h in enumerate(r.history, start=1):
         o = orc.run(g, s.arrays(g), i, 0.0)
         assert h.tobytes() == o["marginals"].tobytes()
+
+
+def test_history_sized_by_iterations_run():
+    """record_history keeps only the iterations that run (engine.py:574-575):
+    a huge max_iterations at ftp scale must not allocate max_iterations x V;
+    a run longer than the device's history budget re-runs with an exact
+    buffer, and every recorded row is that iteration's marginals."""
+    w = W.build("C4-PARALL")
+    s = w.strategy.compile(w.graph)
+    r = P.run(w.graph, s, EngineOptions(max_iterations=10_000_000, tolerance=1e-9,
+                                        record_history=True))
+    assert r.converged and len(r.history) == r.iterations == 23
+    assert r.history[-1].tobytes() == r.marginals.tobytes()
+    r2 = P.run(w.graph, s, EngineOptions(max_iterations=90, tolerance=0.0, record_history=True))
+    assert len(r2.history) == 90  # beyond the 256 MiB budget (79 ftp iterations): re-run
+    r3 = P.run(w.graph, s, EngineOptions(max_iterations=40, tolerance=0.0))
+    assert r2.history[39].tobytes() == r3.marginals.tobytes()
+    assert r2.history[22].tobytes() == r.marginals.tobytes()
 
 
 def test_normalization_toggle_close():
@@ -420,3 +439,78 @@ def test_more_phases_than_the_shared_memory_phase_cache():
     assert res.iterations == o["iterations"] and res.converged == o["converged"]
     assert res.marginals.tobytes() == o["marginals"].tobytes()
     assert np.asarray(res.deltas).tobytes() == o["deltas"].tobytes()
+
+
+def _compile_any(rng, g, mode):
+    if mode == 0:
+        return Strategy.parall().compile(g)
+    if mode == 1:
+        return Strategy.seqfix().compile(g)
+    if mode == 2:
+        return Strategy.seqfix(g.edges_at(rng.permutation(g.num_edges))).compile(g)
+    return P.compile_schedule(g, random_poset(rng, g))
+
+
+def test_underflow_attribution_bitwise_vs_oracle():
+    """UnderflowError names the reference's message or variable: the first
+    failing pass of the first failing iteration, rows[argmin(total)] in the
+    reference's stable descending-row-length order (engine.py:155-165,
+    :512-518) -- (kind, iteration, index) equal to the oracle's, which
+    tests/test_oracle.py pins to hornbp itself."""
+    from builders import contradictory_graph
+
+    rng = np.random.default_rng(505)
+    raised, kinds = 0, set()
+    for trial in range(360):
+        g = contradictory_graph(rng)
+        sched = _compile_any(rng, g, trial % 4)
+        opts = EngineOptions(max_iterations=int(rng.integers(1, 25)), tolerance=1e-9,
+                             normalize_messages=trial % 7 != 3)
+        o = orc.run(g, sched.arrays(g), opts.max_iterations, opts.tolerance, opts.normalize_messages)
+        if o["underflow"] is None:
+            res = P.run(g, sched, opts)
+            assert res.iterations == o["iterations"], trial
+            assert res.marginals.tobytes() == o["marginals"].tobytes(), trial
+            continue
+        with pytest.raises(UnderflowError) as ei:
+            P.run(g, sched, opts)
+        got = (ei.value.kind, ei.value.iteration, ei.value.index)
+        assert got == o["underflow"], (trial, got, o["underflow"])
+        raised += 1
+        kinds.add(got[0])
+    assert raised >= 200 and kinds == {1, 2, 3}, (raised, kinds)
+
+
+def test_underflow_attribution_with_evidence_codes():
+    """interaction_loop's device evidence (hbp_graph_set_evidence) reports the
+    clamped graph's positions: the clamp slots lengthen their variables'
+    rows and shift later ftov rows (graph.py:189-200, storage.py:55-63)."""
+    from builders import contradictory_graph
+
+    rng = np.random.default_rng(606)
+    raised = 0
+    for trial in range(120):
+        g = contradictory_graph(rng, n_clamps=0)
+        pairs = [(int(rng.integers(0, g.num_variables)), bool(rng.integers(0, 2)))
+                 for _ in range(int(rng.integers(1, 6)))]
+        strategy = Strategy.parall() if trial % 2 == 0 else Strategy.seqfix()
+        cur = g
+        for v, o_ in pairs:
+            cur = clamp_evidence(cur, v, o_)
+        sched = strategy.compile(cur)
+        o = orc.run(cur, sched.arrays(cur), 30, 1e-9)
+        dg = P.engine.device_graph(g)
+        plan = dg.plan(strategy.compile(g), g)
+        dg.set_evidence([v for v, _ in pairs], [o_ for _, o_ in pairs])
+        try:
+            if o["underflow"] is None:
+                res = plan.run(EngineOptions(30, 1e-9), g)
+                assert res.marginals.tobytes() == o["marginals"].tobytes(), trial
+                continue
+            with pytest.raises(UnderflowError) as ei:
+                plan.run(EngineOptions(30, 1e-9), g)
+        finally:
+            dg.set_evidence([], [])
+        assert (ei.value.kind, ei.value.iteration, ei.value.index) == o["underflow"], trial
+        raised += 1
+    assert raised >= 40, raised

@@ -9,7 +9,8 @@ from builders import random_graph
 from conftest import sha
 from oracle import orc
 import paper_2509_22337_b200 as P
-from paper_2509_22337_b200 import EngineOptions, Strategy, clamp_evidence, rank_alarms
+from paper_2509_22337_b200 import (EngineOptions, Factor, FactorGraph, FactorKind, Strategy,
+                                   clamp_evidence, rank_alarms)
 from paper_2509_22337_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -41,7 +42,9 @@ def check_against_oracle(g, sets, opts, res):
     for j, pairs in enumerate(sets):
         o, sched = oracle_set(g, pairs, opts)
         if o["underflow"] is not None:
-            assert res.errors[j] is not None, j
+            e = res.errors[j]
+            assert e is not None, j
+            assert (e.kind, e.iteration, e.index) == o["underflow"], (j, e, o["underflow"])
             continue
         assert res.errors[j] is None, (j, res.errors[j])
         assert res.iterations[j] == o["iterations"], j
@@ -86,6 +89,26 @@ def test_sweep_contradictory_evidence_is_a_per_set_underflow():
     assert isinstance(res.errors[1], P.UnderflowError)
     o, _ = oracle_set(g, sets[1], EngineOptions())
     assert o["underflow"] is not None and o["underflow"][0] == 3  # marginal, like the reference
+    e = res.errors[1]
+    assert (e.kind, e.iteration, e.index) == o["underflow"]
+
+
+def test_sweep_underflow_attribution_vs_oracle():
+    """Per-set UnderflowError of the sweep == the reference's report for
+    run(clamp_evidence(G, set j), PARALL), on contradictory random graphs."""
+    from builders import contradictory_graph
+
+    rng = np.random.default_rng(707)
+    raised = 0
+    for trial in range(25):
+        g = contradictory_graph(rng, n_clamps=0)
+        sets = random_sets(rng, g.num_variables, 40, max_size=5, allow_dup=True)
+        opts = EngineOptions(max_iterations=30, tolerance=1e-9,
+                             normalize_messages=trial % 5 != 2)
+        res = P.run_many(g, sets, None, opts)
+        check_against_oracle(g, sets, opts, res)
+        raised += sum(e is not None for e in res.errors)
+    assert raised >= 200, raised
 
 
 def test_sweep_passes_equal_single_pass():
@@ -268,3 +291,37 @@ def test_sweep_empty_and_csr_inputs():
     b = P.run_many(g, [[], [(5, True), (5, True)]])
     assert a.marginals.tobytes() == b.marginals.tobytes()
     assert list(a.iterations) == list(b.iterations) and a.errors == b.errors == [None, None]
+
+
+def test_ranking_keeps_alarms_with_p1_exactly_zero():
+    """An unlabeled alarm whose P1 is exactly 0.0 (derived only through a
+    false-clamped tuple by a deterministic OR, synth.py's p1=1, p2=0) is still
+    ranked -- last, by id -- like rank_alarms (ranking.py:83-91)."""
+    from paper_2509_22337_b200 import AlarmSet
+
+    g = FactorGraph(4, [Factor(FactorKind.AND, 0, (), 0.5, 0.5),
+                        Factor(FactorKind.OR, 1, (0,), 1.0, 0.0),
+                        Factor(FactorKind.OR, 3, (0,), 1.0, 0.0),
+                        Factor(FactorKind.AND, 2, (), 0.3, 0.3)])
+    alarms = AlarmSet((0, 1, 2, 3), (False, False, True, False))
+    sets = [[(0, False)], [(0, False), (2, True)], []]
+    sel = np.arange(4)
+    res = P.run_many(g, sets, select=sel, topk=4)
+    for j, pairs in enumerate(sets):
+        assert res.marginals[j].shape == (4, 2)
+        want = rank_alarms(res.marginals[j], alarms, [v for v, _ in pairs])
+        got = [v for v in res.ranked[j].tolist() if v >= 0]
+        assert got == want, (j, got, want)
+    assert res.marginals[0][1, 1] == 0.0 and 1 in res.ranked[0].tolist()
+    # the single-graph device ranking (interaction_loop's argmax) as well
+    dg = P.engine.device_graph(g)
+    plan = dg.plan(Strategy.parall().compile(g), g)
+    dg.set_evidence([0, 2], [0, 1])
+    try:
+        plan.run(EngineOptions(), g)
+        top, p1 = dg.rank(np.array([1, 2, 3], dtype=np.int32), 1)
+        assert top[0] == 1 and p1[0] == 0.0
+        top, _ = dg.rank(np.array([1, 2, 3], dtype=np.int32), 3)
+        assert top.tolist() == [1, 3, -1]
+    finally:
+        dg.set_evidence([], [])

@@ -77,3 +77,25 @@ def test_evidence_csr_equals_the_list_form():
         EvidenceCSR([0, 3], [1, 2], [1, 0])
     with pytest.raises(GraphError):
         _normalise_sets(g, EvidenceCSR([0, 1], [g.num_variables], [1]))
+
+
+def test_evidence_csr_slicing_and_indexing():
+    g, _ = W.graph("weblech")
+    sets = [[(1, True), (2, False)], [], [(3, False)], [(4, True), (5, True), (6, False)]]
+    csr = P.EvidenceCSR.from_sets(g, sets)
+    assert [csr[j] for j in range(len(csr))] == sets
+    assert csr[-1] == sets[-1]
+    part = csr[1:4]
+    assert isinstance(part, P.EvidenceCSR) and len(part) == 3
+    assert [part[j] for j in range(3)] == sets[1:4]
+    assert part.offsets[0] == 0
+    assert len(csr[3:1]) == 0
+    with pytest.raises(IndexError):
+        csr[4]
+
+
+def test_alarms_to_text_matches_reference_format():
+    from paper_2509_22337_b200.ranking import AlarmSet, alarms_to_text
+
+    assert alarms_to_text(AlarmSet((), ())) == "\n"
+    assert alarms_to_text(AlarmSet((3, 7), (True, False))) == "alarm 3 1\nalarm 7 0\n"
