@@ -203,6 +203,20 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def loaded_repo_libs() -> list:
+    """Shared objects of this repo mapped into the process (/proc/self/maps)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1] if len(line.split()) >= 6 else ""
+                if path.endswith(".so") and os.path.realpath(path).startswith(os.path.realpath(ROOT)):
+                    out.add(os.path.relpath(os.path.realpath(path), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(out)
+
+
 def import_reference():
     """hornbp from baseline/_ref (installed from /root/reference with pip
     --target; it travels to the GPU box with the snapshot)."""
@@ -365,6 +379,7 @@ def run_reference(args) -> None:
     # the arm must not have touched the product (its native library included)
     assert not any(m.split(".")[0] == "paper_2509_22337_b200" for m in sys.modules), \
         "reference arm imported the product package"
+    line["native_libs_loaded"] = loaded_repo_libs()
     print(json.dumps(line), flush=True)
 
 
