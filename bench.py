@@ -569,7 +569,10 @@ def run_ours_sweep(args) -> None:
                                 "sample": f"sets 0..{len(sample) - 1}, one per core, C oracle "
                                           "single-threaded runs (clamp + PARALL compile + run)"}
         line["fp32_mode"] = measure_fp32(P, g, sets, sel, p1.cpu().numpy(), rk.cpu().numpy())
-        line["single_graph"] = measure_single(torch, "c4", steps=20, warmup=5)
+        line["single_graph"] = measure_single(torch, "C4-PARALL", steps=20, warmup=5)
+        # every other BASELINE configuration on the same line (configs[0..3])
+        line["configs"] = {k: measure_single(torch, k, steps=10, warmup=3)
+                           for k in SINGLE_KEYS if k != "C4-PARALL"}
         line["interaction_loop"] = measure_loop(g, alarms, cores)
     print(json.dumps(line), flush=True)
     if multi:
@@ -634,16 +637,53 @@ def measure_loop(g, alarms, cores: int) -> dict:
             "path": "paper_2509_22337_b200.interaction_loop (evidence codes + device ranking)"}
 
 
-# ---- single graph (configs[3]) -------------------------------------------------------------
+# ---- single graphs (configs[0..3]) ---------------------------------------------------------
 
-def measure_single(torch, workload: str, steps: int, warmup: int) -> dict:
+SINGLE_KEYS = ("C1", "C2", "C3", "C4-PARALL", "C4-SEQFIX")
+WORKLOAD_TEXT = {
+    "C1": "C1: weblech SynthSpec(313,383,8,0) (696 V / 1,655 E), PARALL, fixed 100 iterations",
+    "C2": "C2: hedc SynthSpec(1657,3690,8,25) (5,347 V / 14,231 E), user-defined sequential sweep "
+          "(SEQFIX over default_rng(1234).permutation(E), 224 levels), tol 1e-9",
+    "C3": "C3: avrora SynthSpec(9424,26667,8,3) (36,091 V / 100,789 E), static residual-priority "
+          "order (SEQFIX, 303 levels), tol 1e-6",
+    "C4-PARALL": "C4-PARALL: ftp SynthSpec(101583,109592,8,0) (211,175 V / 476,915 E), PARALL, tol 1e-9",
+    "C4-SEQFIX": "C4-SEQFIX: ftp SynthSpec(101583,109592,8,0), canonical SEQFIX (476 levels), tol 1e-9",
+}
+
+
+def plan_info(lib, plan) -> tuple[int, int, int, int]:
+    import ctypes as C
+    f = lib.hbp_debug_plan_info
+    f.restype = None
+    f.argtypes = [C.c_void_p] + [C.POINTER(C.c_int32)] * 4
+    v = [C.c_int32() for _ in range(4)]
+    f(plan.handle, *[C.byref(x) for x in v])
+    return tuple(x.value for x in v)  # phases, grid, threads, fused levels
+
+
+def l2_traffic(key: str) -> Optional[dict]:
+    """lts__t_sectors of one launch of this config's kernel, from this round's
+    ncu capture (profiles/l2_traffic.json, written by tools/collect_l2.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_traffic.json")) as fh:
+            return json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def measure_single(torch, key: str, steps: int, warmup: int, e2e: bool = True,
+                   cpu: bool = True) -> dict:
+    """One single-graph config: device time to convergence (CUDA events
+    around the one persistent launch, L2 flushed before each run), updates/s,
+    roofline, parity against the reference's golden run, the public run()
+    end to end, and the C port on one host core."""
     import ctypes as C
 
     import paper_2509_22337_b200 as P
+    from oracle import orc
     from paper_2509_22337_b200 import _native
     from paper_2509_22337_b200 import workloads as W
 
-    key = "C4-SEQFIX" if workload == "c4-seqfix" else "C4-PARALL"
     w = W.build(key)
     g = w.graph
     sched = w.strategy.compile(g)
@@ -654,6 +694,7 @@ def measure_single(torch, workload: str, steps: int, warmup: int) -> dict:
     dg = P.engine.device_graph(g)
     plan = dg.plan(sched, g)
     copt = plan.options(opts)
+    nphases, grid, threads, nfused = plan_info(lib, plan)
 
     def step():
         res = _native.Result()
@@ -682,55 +723,84 @@ def measure_single(torch, workload: str, steps: int, warmup: int) -> dict:
         with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
             gold = json.load(fh)["runs"][key]
         parity = (hashlib.sha256(res_check.marginals.tobytes()).hexdigest() == gold["marginals_sha"]
-                  and res_check.iterations == gold["iterations"])
+                  and res_check.iterations == gold["iterations"]
+                  and [float(d).hex() for d in res_check.deltas] == gold["deltas"])
     except (OSError, KeyError):
         pass
-    # end to end through run(): fresh device layout + plan every step. The
-    # graphs and sweeps of the earlier legs are released (and collected)
-    # first, so their multi-GB frees do not land inside a timed step.
-    import gc
-    P.engine.clear_device_cache()
-    gc.collect()
-    torch.cuda.synchronize()
-    e2e_s, e2e_iters = [], []
-    for i in range(max(5, warmup) + steps):
-        P.engine.clear_device_cache()
-        t0 = time.perf_counter()
-        r = P.run(g, sched, opts)
-        dt = time.perf_counter() - t0
-        if i >= max(5, warmup):
-            e2e_s.append(dt)
-            e2e_iters.append(r.iterations)
     E, V, F = g.num_edges, g.num_variables, g.num_factors
-    s_off, s_e, t_off, t_e = sched.arrays(g)
-    # canonical graph (rowptr, vars, kind, p1, p2) -> device layout build, then
-    # the schedule's batches -> device PARALL shape test
-    h2d = 8 * (F + 1) + 4 * E + 17 * F + 4 * (len(s_e) + len(t_e))
-    d2h = 16 * V + 8 * e2e_iters[-1]
     peak, peak_kind = load_peaks()
     bpi = single_bytes_per_iteration(g, upd)
+    mean_ms = statistics.mean(dev_ms)
     bytes_per_launch = bpi * statistics.mean(iters) + 32 * E
-    achieved = bytes_per_launch / (statistics.mean(dev_ms) * 1e-3) / 1e9
-    return {
-        "workload": f"{key}: ftp SynthSpec(101583,109592,8,0), {w.strategy.kind}, "
-                    f"tol {w.tolerance}, to convergence, L2 flushed (256 MiB write) between runs",
+    achieved = bytes_per_launch / (mean_ms * 1e-3) / 1e9
+    l2 = l2_roofline(achieved)
+    levelled = sched.num_batches > 1
+    out = {
+        "workload": WORKLOAD_TEXT[key] + ", to convergence, L2 flushed (256 MiB write) between runs",
         "value": value, "unit": UNIT, "time_to_convergence_ms": total_ms / steps,
         "iterations": iters[-1], "updates_per_iteration": upd, "k_batches": sched.num_batches,
+        "phases_per_iteration": nphases, "fused_levels": nfused, "grid": [grid, threads],
         "parity_vs_reference_golden": parity, "gpu_launches": launches,
-        "e2e": {"value": upd * sum(e2e_iters) / sum(e2e_s), "unit": UNIT,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": 1e3 * statistics.mean(e2e_s),
-                "path": "paper_2509_22337_b200.run() with a fresh graph every step (device layout build + plan + run + marginals to host)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "kernel": "hbp::lbp_persistent (whole run in one launch)",
-                     "bytes_per_launch": bytes_per_launch,
-                     "note": "working set (~28 MB) is L2-resident within a run",
-                     "l2": l2_roofline(achieved),
-                     "l2_traffic_per_launch": 2044344768.0,
-                     "l2_traffic_source": "ncu lts__t_sectors.sum x 32 B of one launch (profiles/r1_c4_parall_ncu.md v2)"},
     }
+    if levelled or key == "C1":
+        # dependent-chain latency, not bandwidth: each phase is a barrier-
+        # separated dependent step (a level on CTA 0, or a whole-graph pass)
+        out["roofline"] = {
+            "bound": "latency", "us_per_phase": 1e3 * mean_ms / (iters[-1] * nphases),
+            "phases": iters[-1] * nphases, "achieved_gbs": achieved,
+            "hbm_frac": achieved / peak, "l2_frac": l2["frac"] if l2 else None,
+            "kernel": "hbp::lbp_persistent (whole run in one launch)",
+            "bytes_per_launch": bytes_per_launch}
+    else:
+        tr = l2_traffic(key)
+        out["roofline"] = {
+            "bound": "l2", "achieved": achieved, "peak": l2["peak"] if l2 else None,
+            "unit": "GB/s", "frac": l2["frac"] if l2 else None,
+            "traffic": tr["l2_bytes_per_launch"] if tr else None,
+            "traffic_source": tr["source"] if tr else None,
+            "peak_source": l2["peak_source"] if l2 else None,
+            "hbm": {"peak": peak, "frac": achieved / peak,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+            "kernel": "hbp::lbp_persistent (whole run in one launch)",
+            "bytes_per_launch": bytes_per_launch,
+            "note": "working set (~28 MB) is L2-resident within a run"}
+    if e2e:
+        # end to end through run(): fresh device layout + plan every step. The
+        # graphs and sweeps of the earlier legs are released (and collected)
+        # first, so their multi-GB frees do not land inside a timed step.
+        import gc
+        P.engine.clear_device_cache()
+        gc.collect()
+        torch.cuda.synchronize()
+        e2e_s, e2e_iters = [], []
+        for i in range(max(5, warmup) + steps):
+            P.engine.clear_device_cache()
+            t0 = time.perf_counter()
+            r = P.run(g, sched, opts)
+            dt = time.perf_counter() - t0
+            if i >= max(5, warmup):
+                e2e_s.append(dt)
+                e2e_iters.append(r.iterations)
+        s_off, s_e, t_off, t_e = sched.arrays(g)
+        # canonical graph (rowptr, vars, kind, p1, p2) -> device layout build, then
+        # the schedule's batches -> device PARALL shape test / host level plan
+        h2d = 8 * (F + 1) + 4 * E + 17 * F + 4 * (len(s_e) + len(t_e))
+        d2h = 16 * V + 8 * e2e_iters[-1]
+        out["e2e"] = {"value": upd * sum(e2e_iters) / sum(e2e_s), "unit": UNIT,
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "ms_per_step": 1e3 * statistics.mean(e2e_s),
+                      "path": "paper_2509_22337_b200.run() with a fresh graph every step "
+                              "(device layout build + plan + run + marginals to host)"}
+    if cpu:
+        t0 = time.perf_counter()
+        o = orc.run(g, sched.arrays(g), w.max_iterations, w.tolerance, threads=1)
+        cpu_s = time.perf_counter() - t0
+        assert o["marginals"].tobytes() == res_check.marginals.tobytes()
+        out["cpu_baseline"] = {"value": upd * o["iterations"] / cpu_s, "unit": UNIT, "cores": 1,
+                               "kind": "port", "seconds": cpu_s,
+                               "sample": f"one full {key} run, C oracle single-threaded "
+                                         "(bit-identical marginals checked)"}
+    return out
 
 
 def l2_roofline(achieved: float) -> Optional[dict]:
@@ -753,17 +823,10 @@ def run_ours_single(args) -> None:
     import paper_2509_22337_b200 as P
 
     P.engine.set_device(0)
+    key = {"c4": "C4-PARALL", "c4-seqfix": "C4-SEQFIX", "c1": "C1", "c2": "C2",
+           "c3": "C3"}[args.workload]
     with ClockSampler(0) as clk:
-        sg = measure_single(torch, args.workload, args.steps, args.warmup)
-    from oracle import orc
-    from paper_2509_22337_b200 import workloads as W
-
-    key = "C4-SEQFIX" if args.workload == "c4-seqfix" else "C4-PARALL"
-    w = W.build(key)
-    sched = w.strategy.compile(w.graph)
-    t0 = time.perf_counter()
-    o = orc.run(w.graph, sched.arrays(w.graph), w.max_iterations, w.tolerance, threads=1)
-    cpu_s = time.perf_counter() - t0
+        sg = measure_single(torch, key, args.steps, args.warmup)
     line = {
         "metric": METRIC, "value": sg["value"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sg["time_to_convergence_ms"],
@@ -774,10 +837,7 @@ def run_ours_single(args) -> None:
                    "k_batches": sg["k_batches"], "parallelism": "single graph, 1 GPU"},
         "time_to_convergence_ms": sg["time_to_convergence_ms"],
         "parity_vs_reference_golden": sg["parity_vs_reference_golden"],
-        "e2e": sg["e2e"], "roofline": sg["roofline"],
-        "cpu_baseline": {"value": sched.updates_per_iteration() * o["iterations"] / cpu_s,
-                         "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"one full {key} run, C oracle single-threaded"},
+        "e2e": sg["e2e"], "roofline": sg["roofline"], "cpu_baseline": sg["cpu_baseline"],
         "clocks": clk.summary(), "gpu_launches": sg["gpu_launches"],
     }
     print(json.dumps(line), flush=True)
@@ -789,7 +849,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["sweep", "c4", "c4-seqfix"], default="sweep")
+    ap.add_argument("--workload", choices=["sweep", "c1", "c2", "c3", "c4", "c4-seqfix"],
+                    default="sweep")
     ap.add_argument("--sets", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -40,10 +40,9 @@ struct hbp_graph {
   cudaStream_t stream = nullptr;      // stream all work of this graph runs on
   cudaStream_t own_stream = nullptr;  // created with the graph
   int num_sms = 0, coop_blocks = 0, threads = 1024;
-  // cluster 0 runs the small levels: csize CTAs (1 = CTA 0 alone), and a
-  // cooperative cluster launch fits cluster_grid CTAs
-  int csize = 1, cluster_grid = 0;
-  const void *kernel = nullptr;
+  const void *kernel = nullptr;         // the single-graph executor
+  const void *kernel_fused = nullptr;   // its instance for plans with fused levels
+  int coop_blocks_fused = 0;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
   int2 *d_vslot = nullptr, *d_fslot = nullptr;
@@ -106,8 +105,11 @@ struct hbp_plan {
   hbp::PlanHost host;
   hbp::Phase *d_phases = nullptr;
   int *d_items = nullptr;
+  int32_t *d_fitems = nullptr;  // fused levels (int4 lane records)
+  hbp_plan *unfused = nullptr;  // the same schedule without fused levels (underflow attribution)
   int grid = 1;
-  int csize = 1;  // CTAs of cluster 0 (small levels); 1 = no cluster launch
+  const void *kernel = nullptr;  // executor instance (fused levels or not)
+  int threads = 0;
   // the schedule as given (reference batch order), for the exact underflow
   // attribution: device [s_edges | t_edges] (stream-ordered pool) + host offsets
   int *d_sched = nullptr;
@@ -119,8 +121,9 @@ struct hbp_plan {
   int ev_ok = -1;
   ~hbp_plan() {
     cudaSetDevice(g->device);
-    for (void *p : {(void *)d_phases, (void *)d_items})
+    for (void *p : {(void *)d_phases, (void *)d_items, (void *)d_fitems})
       if (p) cudaFree(p);
+    delete unfused;
     if (d_sched) cudaFreeAsync(d_sched, g->stream);
   }
 };

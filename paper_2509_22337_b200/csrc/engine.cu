@@ -39,6 +39,10 @@ namespace hbp {
 using namespace dev;
 
 constexpr int kThreads = 768;  // default block size: 80 registers, fewest spills (measured best)
+#ifndef HBP_FUSED_THREADS
+#define HBP_FUSED_THREADS 768
+#endif
+constexpr int kFusedThreads = HBP_FUSED_THREADS;  // plans with fused levels
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 constexpr int kPhaseCache = 1024;  // phase descriptors staged in shared memory (32 KB)
 constexpr int kChunkTrace = 16384;  // HBP_TRACE=1: per-chunk ns of iteration 3, PARALL phases 0/1
@@ -80,6 +84,7 @@ struct KParams {
   const Phase *phases;
   int nphases;
   const int *items;
+  const int4 *fitems;  // fused levels: two int4 per lane (layout.cpp emit_fused)
   // control
   Ctrl *ctrl;
   unsigned long long *delta_bits;  // [max_it + 2]
@@ -91,7 +96,7 @@ struct KParams {
   double2 *hist;                   // [hist_iters][V] or null
   int hist_iters;                  // iterations the history buffer holds
   unsigned long long *trace;       // debug: [kTraceIters][nphases][grid][2] or null
-  int csize;                       // CTAs of cluster 0, which runs the small levels
+  int csize;                       // CTAs that run the small levels (1: CTA 0 alone)
   int max_it;
   int normalize;
   double tol;
@@ -139,9 +144,9 @@ __device__ __forceinline__ void sync_point(Ctrl *c, Sync &s, unsigned arrivals, 
 // Underflow is recorded in a per-thread key (min over the phase) and
 // published once per phase by flush_underflow, so the common path issues no
 // atomics. key = phase << 33 | kind << 32 | slot.
-__device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
-                                            int phase, int kind, int slot,
-                                            unsigned long long &ufkey) {
+__device__ __forceinline__ void put_message_ref(const KParams &P, double2 *dst, double &a0,
+                                                double &a1, int phase, int kind, int slot,
+                                                unsigned long long &ufkey) {
   if (P.normalize) {
     const double t = add(a0, a1);
     if (__builtin_expect(t < kMinMessageSum, 0)) {
@@ -152,6 +157,12 @@ __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, doub
     div2_rn(a0, a1, t, a0, a1);
   }
   *dst = make_double2(a0, a1);
+}
+
+__device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
+                                            int phase, int kind, int slot,
+                                            unsigned long long &ufkey) {
+  put_message_ref(P, dst, a0, a1, phase, kind, slot, ufkey);
 }
 
 __device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsigned long long ufkey) {
@@ -541,6 +552,100 @@ __device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool f
   }
 }
 
+
+// --------------------------------------------------------------------------------------
+// fused level (layout.cpp emit_fused): one lane per row slot of the level's
+// factors, a factor's lanes inside one warp. Lane k of factor f computes the
+// vtof message of slot k (t_b) from its variable's row, the factor's lanes
+// exchange their row by warp shuffles, and lane k then computes the ftov
+// message of slot k (s_b) from the row. The plan admits a level only when no
+// other factor of the level writes into a row a lane reads, so the values of
+// the two-phase order are read (engine.py:566-570).
+
+// The lanes of a warp belong to different variables (rows of mixed length),
+// so the row is loaded branch-free: kFuseRow predicated loads issued
+// together, one memory round trip for every lane (a switch on the length
+// would serialise one round trip per distinct length). Longer rows finish
+// in a loop.
+constexpr int kFuseRow = 6;
+
+// one lane: h = {factor, row start, d | slot << 8 | group lane << 16,
+// tmask | smask << 12}, rc = the slot's record {variable row start,
+// (variable degree << 16) | own index, internal variable, ftov slot}.
+// Called by all 32 lanes of a warp.
+__device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, int it, int phase,
+                                           unsigned long long &ufkey) {
+  const int d = h.z & 0xff, k = (h.z >> 8) & 0xff, base = h.z >> 16;
+  const int tmask = h.w & 0xfff, smask = (h.w >> 12) & 0xfff;
+  const bool tgt = d && ((tmask >> k) & 1);
+  const int dv = tgt ? rc.y >> 16 : 0, j = rc.y & 0xffff;
+  // every load of the lane in one round trip: its variable's row (t_b
+  // target) or its current vtof message, the evidence code, the parameters
+  double2 x[kFuseRow];
+#pragma unroll
+  for (int i = 0; i < kFuseRow; ++i)
+    x[i] = i < dv ? P.ftov[rc.x + i] : make_double2(1.0, 1.0);
+  const double2 cur = (d && !tgt) ? P.vtof[h.y + k] : make_double2(1.0, 1.0);
+  const unsigned code = (tgt && P.ev) ? P.ev[rc.z] : 0u;
+  const bool out = d && ((smask >> k) & 1);
+  const double2 pp = out ? __ldg(P.fpar + h.x) : make_double2(0.0, 0.0);
+  double2 m = cur;
+  if (tgt) {  // vtof (engine.py:186-195): the row without slot j, left to right
+    double a0 = 1.0, a1 = 1.0;
+#pragma unroll
+    for (int i = 0; i < kFuseRow; ++i)
+      if (i < dv && i != j) {
+        a0 = mul(a0, x[i].x);
+        a1 = mul(a1, x[i].y);
+      }
+    for (int i = kFuseRow; i < dv; ++i)
+      if (i != j) {
+        const double2 y = P.ftov[rc.x + i];
+        a0 = mul(a0, y.x);
+        a1 = mul(a1, y.y);
+      }
+    if (code && it > 1) apply_clamp(code, a0, a1);
+    put_message_ref(P, P.vtof + h.y + k, a0, a1, phase, 0, h.y + k, ufkey);
+    m = make_double2(a0, a1);
+  }
+  const bool is_or = factor_is_or(P, h.x);
+  const int dmax = __reduce_max_sync(0xffffffffu, d);
+  double b1 = 1.0, b2 = 1.0;
+  for (int i = 0; i < dmax; ++i) {
+    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
+    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
+    if (out && i < d && i != k) {  // left to right, the own slot skipped
+      double f1, f2;
+      if (i == 0) {
+        if (is_or)
+          head_slot_terms<1>(pp.x, pp.y, x0, x1, f1, f2);
+        else
+          head_slot_terms<0>(pp.x, pp.y, x0, x1, f1, f2);
+      } else {
+        f1 = add(x0, x1);
+        f2 = is_or ? x0 : x1;
+      }
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
+    }
+  }
+  if (out) {
+    double o0, o1;
+    if (k == 0) {
+      if (is_or)
+        head_message<1>(pp.x, pp.y, b1, b2, o0, o1);
+      else
+        head_message<0>(pp.x, pp.y, b1, b2, o0, o1);
+    } else {
+      if (is_or)
+        body_message<1>(pp.x, pp.y, b1, b2, o0, o1);
+      else
+        body_message<0>(pp.x, pp.y, b1, b2, o0, o1);
+    }
+    put_message(P, P.ftov + rc.w, o0, o1, phase, 1, rc.w, ufkey);
+  }
+}
+
 // --------------------------------------------------------------------------------------
 // one phase over its slots, grid- or CTA-strided
 
@@ -550,6 +655,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+template <bool FUSED>
 __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, int pidx, int it,
                                            bool do_marg, bool do_vtof,
                                            unsigned long long &dmax) {
@@ -564,6 +670,15 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
   }
   const int n = ph.end - ph.begin;
   unsigned long long ufkey = ~0ull;
+  if (FUSED && ph.type == 2) {  // n is a multiple of 32: whole warps
+    for (int i = start; i < n; i += stride) {
+      const int4 *lr = P.fitems + 2 * (size_t)(ph.begin + i);
+      const int4 h = __ldg(lr), rc = __ldg(lr + 1);
+      fused_lane(P, h, rc, it, pidx, ufkey);
+    }
+    flush_underflow(P, it, ufkey);
+    return;
+  }
   if (ph.list == 2) {
     // whole light nodes [begin, end), then the slots of the heavy nodes
     // [sbegin, send); grid-strided so a warp's 32 items are neighbouring rows
@@ -721,16 +836,6 @@ __device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int 
   }
 }
 
-// barrier of cluster 0 between two small levels (release/acquire at cluster
-// scope orders the global-memory messages too); csize 1: CTA 0 alone
-__device__ __forceinline__ void cluster0_sync(int csize) {
-  if (csize > 1) {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  } else {
-    __syncthreads();
-  }
-}
-
 // marginals of the stopping iteration in the reference's variable order
 __device__ __forceinline__ void write_marginals(const KParams &P) {
   const int gs = gridDim.x * blockDim.x;
@@ -740,8 +845,10 @@ __device__ __forceinline__ void write_marginals(const KParams &P) {
   }
 }
 
-template <int THREADS, int MINB = 1>
-__global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_constant__ KParams P) {
+// FUSED: the instance for plans with fused levels (a separate instance keeps
+// the PARALL kernel's register allocation untouched)
+template <int THREADS, bool FUSED>
+__global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
   const bool multi = gridDim.x > 1;
   const unsigned G = gridDim.x;
@@ -786,7 +893,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
     if (it == P.halt_it && P.halt_phase == 0) return;  // attribution re-run
     if (!(parall && it == 1)) {
       trace_mark(P, it, 0, 0);
-      exec_phase(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
+      exec_phase<FUSED>(P, phase_at(0), 0, it, it > 1, !final_pass, dmax);
       trace_mark(P, it, 0, 1);
       if (it > 1) {
         unsigned long long m = block_max(dmax);
@@ -851,8 +958,8 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
         } else if (prev_grid && !ph.grid) {
           sync_point(C, sy, G, true, in0);
         } else if (!prev_grid && !ph.grid) {
-          if (in0) cluster0_sync(P.csize);
-        } else {  // cluster 0 -> grid
+          if (in0) __syncthreads();
+        } else {  // CTA 0 -> grid
           sync_point(C, sy, P.csize, in0, true);
         }
       }
@@ -866,7 +973,17 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       if (p + 1 < P.nphases) {
         const Phase &np = phase_at(p + 1);
         const int i = blockIdx.x * blockDim.x + threadIdx.x;
-        look = np.list == 1 && (np.grid || (int)blockIdx.x < P.csize) && i < np.end - np.begin;
+        const bool mine = (np.grid || (int)blockIdx.x < P.csize) && i < np.end - np.begin;
+        if (FUSED && np.list == 3 && mine) {
+          // fused level: the item lines (read-only) of this thread's first
+          // two lanes into L1
+          const int stride = (np.grid ? (int)gridDim.x : P.csize) * (int)blockDim.x;
+          const int4 *lr = P.fitems + 2 * (size_t)(np.begin + i);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(lr));
+          if (i + stride < np.end - np.begin)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(lr + 2 * (size_t)stride));
+        }
+        look = np.list == 1 && mine;
         if (look) {
           const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_nx[threadIdx.x]);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" ::"r"(dst),
@@ -876,7 +993,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lbp_persistent(const __grid_con
       }
       unsigned long long unused = 0;
       trace_mark(P, it, p, 0);
-      exec_phase(P, ph, p, it, false, true, unused);
+      exec_phase<FUSED>(P, ph, p, it, false, true, unused);
       trace_mark(P, it, p, 1);
       if (look) {
         asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1271,52 +1388,17 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   HBP_CUDA(cudaEventCreate(&g->ev1));
   HBP_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
   int per_sm = 0;
-  {
-    // HBP_THREADS (A/B): 768 (default: one CTA/SM, 80 registers), 1024 (64
-    // registers, spills), 512 (108 registers), 5122 (512 threads, two CTAs/SM).
-    // Measured on B200: 768 is best for PARALL and levelled schedules alike.
-    const char *env = getenv("HBP_THREADS");
-    const int sel = env ? atoi(env) : hbp::kThreads;
-    g->threads = sel == 1024 ? 1024 : (sel == 512 || sel == 5122 ? 512 : hbp::kThreads);
-    g->kernel = sel == 512    ? (const void *)hbp::lbp_persistent<512>
-                : sel == 1024 ? (const void *)hbp::lbp_persistent<1024>
-                : sel == 5122 ? (const void *)hbp::lbp_persistent<512, 2>
-                              : (const void *)hbp::lbp_persistent<hbp::kThreads>;
-  }
+  // one CTA of 768 threads per SM (80 registers). Measured on B200 against
+  // 512 (108 registers), 1024 (64 registers, spills) and 2 x 512 per SM: 768
+  // is best for PARALL and levelled schedules alike.
+  g->threads = hbp::kThreads;
+  g->kernel = (const void *)hbp::lbp_persistent<hbp::kThreads, false>;
+  g->kernel_fused = (const void *)hbp::lbp_persistent<hbp::kFusedThreads, true>;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
-  // HBP_CLUSTER=1 (opt-in): small levels run on one thread-block cluster --
-  // the largest cluster size whose cooperative cluster launch still covers
-  // >= 90 % of the SMs -- with barrier.cluster between levels. Measured on
-  // B200 it is slower than CTA 0 alone (C4 SEQFIX 48.7 vs 41.5 ms): a small
-  // level is bound by its dependent-load chain, not by one SM's issue rate,
-  // and the cluster barrier costs more than __syncthreads.
-  g->csize = 1;
-  g->cluster_grid = g->coop_blocks;
-  if (getenv("HBP_CLUSTER")) {
-    for (int c : {8, 4, 2}) {
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = c;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(g->coop_blocks / c * c);
-      cfg.blockDim = dim3(g->threads);
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, g->kernel, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        continue;
-      }
-      if (nclusters * c * 10 >= g->coop_blocks * 9) {
-        g->csize = c;
-        g->cluster_grid = nclusters * c;
-        break;
-      }
-    }
-  }
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_fused,
+                                                         hbp::kFusedThreads, 0));
+  g->coop_blocks_fused = std::max(1, per_sm) * g->num_sms;
   // the layout is built on the device (layout_dev.cu); the host copy of it
   // only when a host-side consumer needs it (hbp::ensure_host_layout)
   hbp::set_last_launches(0);
@@ -1355,20 +1437,31 @@ hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to
   return HBP_OK;
 }
 
+static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const int32_t *s_edges,
+                              const int64_t *t_off, const int32_t *t_edges, bool fuse,
+                              hbp_plan **out);
+
 hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const int32_t *s_edges,
                            const int64_t *t_off, const int32_t *t_edges, hbp_plan **out) {
   if (!g || !out) {
     hbp::set_error("null argument");
     return HBP_EINVAL;
   }
+  // HBP_FUSE=0 (A/B): every level as two phases
+  const char *fe = getenv("HBP_FUSE");
+  return plan_create(g, k, s_off, s_edges, t_off, t_edges, !(fe && atoi(fe) == 0), out);
+}
+
+static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const int32_t *s_edges,
+                              const int64_t *t_off, const int32_t *t_edges, bool fuse,
+                              hbp_plan **out) {
   *out = nullptr;
   std::unique_ptr<hbp_plan> p(new (std::nothrow) hbp_plan());
   if (!p) return HBP_ENOMEM;
   p->g = g;
-  // levels smaller than two items per thread of cluster 0 run on cluster 0 only
-  // levels below this many items run on cluster 0 alone (HBP_SMALL: A/B)
+  // levels below this many items run on CTA 0 alone (HBP_SMALL: A/B)
   const char *se = getenv("HBP_SMALL");
-  const int32_t small = se ? atoi(se) : (g->csize > 1 ? 2 * g->csize * g->threads : 3072);
+  const int32_t small = se ? atoi(se) : 3072;
   HBP_CUDA(cudaSetDevice(g->device));
   hbp_status st;
   bool parall = false;
@@ -1386,11 +1479,12 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
   } else {
     if ((st = hbp::ensure_host_layout(g)) != HBP_OK) return st;
     if ((st = hbp::build_plan(g->L, k, s_off, s_edges, t_off, t_edges, p->host, small,
-                              grouping)) != HBP_OK)
+                              grouping, fuse)) != HBP_OK)
       return st;
   }
   cudaStream_t s = g->stream;
-  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)))
+  if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)) ||
+      (st = upload(&p->d_fitems, p->host.fitems, s)))
     return st;
   // keep the schedule in its reference order for the underflow attribution
   // (a PARALL-shape batch is already on the device: the shape test's copy)
@@ -1411,25 +1505,21 @@ hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const 
         HBP_CUDA(cudaMemcpyAsync(p->d_sched + ns, t_edges, (size_t)nt * 4, cudaMemcpyHostToDevice, s));
     }
   }
+  // kernel instance: plans with fused levels run the FUSED instance
+  const bool fused = p->host.n_fused > 0;
+  p->kernel = fused ? g->kernel_fused : g->kernel;
+  p->threads = fused ? hbp::kFusedThreads : g->threads;
+  const int coop = fused ? g->coop_blocks_fused : g->coop_blocks;
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
   for (const auto &ph : p->host.phases)
     if (ph.grid)
       big = std::max<int64_t>(big, (ph.end - ph.begin) + (ph.list == 2 ? ph.send - ph.sbegin : 0));
-  int64_t want = (big + g->threads - 1) / g->threads;
-  if (big < 2 * g->threads) want = 1;
-  bool has_small = false;
-  for (const auto &ph : p->host.phases) has_small |= !ph.grid;
-  p->csize = (has_small && want > 1) ? g->csize : 1;
-  if (p->csize > 1) {
-    want = std::max<int64_t>(want, p->csize);
-    want = (want + p->csize - 1) / p->csize * p->csize;
-    p->grid = (int)std::min<int64_t>(want, g->cluster_grid);
-  } else {
-    p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, g->coop_blocks));
-    if (const char *ge = getenv("HBP_GRID"))  // A/B: force the CTA count
-      p->grid = std::max(1, std::min(atoi(ge), g->coop_blocks));
-  }
+  int64_t want = (big + p->threads - 1) / p->threads;
+  if (big < 2 * p->threads) want = 1;
+  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, coop));
+  if (const char *ge = getenv("HBP_GRID"))  // A/B: force the CTA count
+    p->grid = std::max(1, std::min(atoi(ge), coop));
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();
   return HBP_OK;
@@ -1552,6 +1642,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.phases = p->d_phases;
   P.nphases = (int)p->host.phases.size();
   P.items = p->d_items;
+  P.fitems = (const int4 *)p->d_fitems;
   P.ctrl = c.ctrl;
   P.delta_bits = c.delta_bits;
   P.uf_msg = c.uf_msg;
@@ -1578,7 +1669,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.tol = opt->tolerance;
   P.time_limit_ns = opt->time_limit > 0 ? (long long)(opt->time_limit * 1e9) : 0;
   if (opt->time_limit > 0 && P.time_limit_ns == 0) P.time_limit_ns = 1;
-  P.csize = p->csize;
+  P.csize = 1;
   P.halt_it = 0;
   P.halt_phase = 0;
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
@@ -1609,6 +1700,24 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   res->device_ms = ms;
   std::memcpy(&res->last_delta, &hc.last_delta, 8);
   if (hc.stop == 4) {
+    if (p->host.n_fused > 0) {
+      // the attribution replays the failing pass group by group (engine.py:
+      // 566-570), which needs the two-phase form of every level: re-run the
+      // same schedule unfused -- bitwise the same run -- and attribute there
+      if (!p->unfused) {
+        const int64_t kb = (int64_t)p->s_off.size() - 1;
+        std::vector<int32_t> edges((size_t)(p->ns + (kb > 0 ? p->t_off[kb] : 0)));
+        if (!edges.empty())
+          HBP_CUDA(cudaMemcpy(edges.data(), p->d_sched, edges.size() * 4, cudaMemcpyDeviceToHost));
+        hbp_plan *u = nullptr;
+        if ((st = plan_create(g, kb, p->s_off.data(), edges.data(), p->t_off.data(),
+                              edges.data() + p->ns, false, &u)))
+          return st;
+        p->unfused = u;
+      }
+      p->unfused->ev_ok = p->ev_ok;
+      return launch_run(p->unfused, opt, res);
+    }
     if ((st = attribute_underflow(p, P, hc.iterations, n, res))) return st;
     hbp::set_error("underflow");
     return HBP_EUNDERFLOW;
@@ -1617,27 +1726,9 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
 }
 
 static hbp_status launch_kernel(hbp_plan *p, hbp::KParams &P) {
-  hbp_graph *g = p->g;
   void *args[] = {&P};
-  if (p->csize > 1) {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = p->csize;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(p->grid);
-    cfg.blockDim = dim3(g->threads);
-    cfg.stream = g->stream;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    HBP_CUDA(cudaLaunchKernelExC(&cfg, g->kernel, args));
-  } else {
-    HBP_CUDA(cudaLaunchCooperativeKernel(g->kernel, dim3(p->grid), dim3(g->threads), args, 0,
-                                         g->stream));
-  }
+  HBP_CUDA(cudaLaunchCooperativeKernel(p->kernel, dim3(p->grid), dim3(p->threads), args, 0,
+                                       p->g->stream));
   return HBP_OK;
 }
 
@@ -2091,17 +2182,19 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
 int64_t hbp_last_launch_count(void) { return g_last_launches; }
 
 // Debug: phase count and grid size of a plan (not part of the public header).
-void hbp_debug_plan_info(hbp_plan *p, int32_t *nphases, int32_t *grid, int32_t *threads) {
+void hbp_debug_plan_info(hbp_plan *p, int32_t *nphases, int32_t *grid, int32_t *threads,
+                         int32_t *nfused) {
   *nphases = (int32_t)p->host.phases.size();
+  if (nfused) *nfused = p->host.n_fused;
   *grid = p->grid;
-  *threads = p->g->threads;
+  *threads = p->threads;
 }
 
 // Debug timeline of the last run with HBP_TRACE=1 (not part of the public header).
 int64_t hbp_debug_trace(hbp_plan *p, unsigned long long *out, int64_t cap) {
   hbp_graph *g = p->g;
   const int64_t n = (int64_t)hbp::kTraceIters * (int64_t)p->host.phases.size() * p->grid * 2 +
-                    (p->host.phases.size() == 2 ? 2 * hbp::kChunkTrace : 0);
+                    2 * hbp::kChunkTrace;
   if (!g->d_trace || cap < n) return -n;
   cudaMemcpy(out, g->d_trace, (size_t)n * 8, cudaMemcpyDeviceToHost);
   return n;

@@ -34,11 +34,12 @@ hbp_status compile(const hbp_graph_desc &g, int64_t m, const int32_t *before,
 // cover every slot [begin, end); list-mode phases read slot ids from the
 // item array (levelled schedules).
 struct Phase {
-  int32_t type;   // 0 variable side, 1 factor side
+  int32_t type;   // 0 variable side, 1 factor side, 2 fused level (list == 3)
   int32_t grid;   // 1: whole grid; 0: cluster 0 only (small level)
   int32_t list;   // 0: slots [begin, end); 1: slot ids from the item list;
                   // 2: whole nodes [begin, end) (variables for type 0, factors for
-                  //    type 1), every outgoing message of a node from one row read
+                  //    type 1), every outgoing message of a node from one row read;
+                  // 3: fused level items [begin, end) of PlanHost::fitems (type 2)
   int32_t marg;   // 1: row-start slots also produce the marginal (phase 0)
   int32_t begin, end;     // nodes (list == 2) or slots / items
   int32_t sbegin, send;   // list == 2: slots of the heavy nodes, one thread per slot
@@ -116,7 +117,20 @@ struct PlanHost {
   int64_t updates_per_iter = 0;        // sum |s_i| + |t_i|
   int32_t max_items = 0;               // largest phase (work items)
   std::vector<int32_t> phase_batch;    // batch index of each phase (underflow attribution)
+  // fused levels (type 2): one lane per row slot of every factor of the level,
+  // a factor's lanes contiguous inside one warp (padding lanes have d = 0).
+  // Per lane two int4: {internal factor, vtof row start,
+  // d | slot << 8 | first lane of the factor << 16, tmask | smask << 12}
+  // (tmask / smask: the row slots whose vtof (t_b) / ftov (s_b) message the
+  // level computes) and the slot's record {variable's ftov row start,
+  // (variable degree << 16) | index in that row, internal variable, ftov slot}
+  std::vector<int32_t> fitems;
+  int32_t n_fused = 0;                 // fused levels in the plan
 };
+
+// factors up to this degree can be part of a fused level (12-bit slot masks,
+// at most one warp per factor)
+constexpr int32_t kFuseMaxDeg = 12;
 
 // the two whole-graph phases of a PARALL schedule (every edge once on the
 // factor side, every non-unary slot once on the variable side), from the
@@ -130,6 +144,7 @@ void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
 // 0 = one slot per thread in the schedule's own (EdgeId) order.
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P, int32_t small_threshold, int grouping = 2);
+                      PlanHost &P, int32_t small_threshold, int grouping = 2,
+                      bool fuse = true);
 
 }  // namespace hbp

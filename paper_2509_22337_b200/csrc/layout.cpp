@@ -239,7 +239,7 @@ void parall_plan(const HostLayout &L, int64_t ns, int64_t nt, PlanHost &P,
 
 hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
                       const int32_t *s_edges, const int64_t *t_off, const int32_t *t_edges,
-                      PlanHost &P, int32_t small_threshold, int grouping) {
+                      PlanHost &P, int32_t small_threshold, int grouping, bool fuse) {
   const int32_t V = L.V;
   const int64_t E = L.E;
   if (k < 0 || (k > 0 && (s_off[0] != 0 || t_off[0] != 0))) {
@@ -268,6 +268,8 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
   P.items.clear();
   P.phase_batch.clear();
   P.max_items = 0;
+  P.fitems.clear();
+  P.n_fused = 0;
 
   std::vector<int64_t> stamp((size_t)E, -1);
   std::vector<int32_t> slots;
@@ -307,9 +309,109 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
     }
   }
 
+  // Level fusion. A level b >= 1 whose factor-side writes are never read by
+  // its own variable side -- no ftov message s_b writes into variable u's row
+  // is read by a t_b target (a', u) of ANOTHER factor a' -- runs as ONE
+  // phase: a thread owns a factor of the level, computes its t_b
+  // vtof messages (reading the variables' rows), then its s_b ftov messages
+  // from its own row. Every read then sees exactly the state the two-phase
+  // order gives it (engine.py:566-570), so the results are the same bits.
+  // (Level 0 is never fused: its variable side carries the marginals, which
+  // read every variable's full row.)
+  std::vector<int64_t> wstamp, istamp;
+  std::vector<int32_t> writer, item_of;
+  if (fuse && grouping == 2) {
+    wstamp.assign((size_t)V, -1);
+    writer.assign((size_t)V, 0);
+    istamp.assign((size_t)L.F, -1);
+    item_of.assign((size_t)L.F, 0);
+  }
+  auto fusable = [&](int64_t b) -> bool {
+    if (!fuse || grouping != 2 || b == 0 || b >= k) return false;
+    for (int64_t i = s_off[b]; i < s_off[b + 1]; ++i) {
+      const int32_t e = s_edges[i];
+      const int32_t u = L.edge_var[e], a = L.edge_factor[e];
+      if (L.rowptr[a + 1] - L.rowptr[a] > kFuseMaxDeg) return false;
+      if (wstamp[u] != b) {
+        wstamp[u] = b;
+        writer[u] = a;
+      } else if (writer[u] != a) {
+        writer[u] = -1;  // two writers: any reader of u conflicts
+      }
+    }
+    for (int64_t i = t_off[b]; i < t_off[b + 1]; ++i) {
+      const int32_t e = t_edges[i];
+      const int32_t u = L.edge_var[e], a = L.edge_factor[e];
+      if (L.rowptr[a + 1] - L.rowptr[a] > kFuseMaxDeg) return false;
+      if (wstamp[u] == b && writer[u] != a) return false;
+    }
+    return true;
+  };
+  auto emit_fused = [&](int64_t b) {
+    std::vector<int32_t> order;  // internal factors of the level
+    std::vector<int32_t> tm, sm;
+    auto touch = [&](int32_t e, bool is_s) {
+      const int32_t p = L.canon2v[e];
+      const int32_t fi = L.fslot[2 * (size_t)p], kk = L.fslot[2 * (size_t)p + 1] & 0xffff;
+      if (istamp[fi] != b) {
+        istamp[fi] = b;
+        item_of[fi] = (int32_t)order.size();
+        order.push_back(fi);
+        tm.push_back(0);
+        sm.push_back(0);
+      }
+      (is_s ? sm : tm)[item_of[fi]] |= 1 << kk;
+    };
+    for (int64_t i = t_off[b]; i < t_off[b + 1]; ++i) touch(t_edges[i], false);
+    for (int64_t i = s_off[b]; i < s_off[b + 1]; ++i) touch(s_edges[i], true);
+    std::vector<int32_t> idx(order.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int32_t)i;
+    // ascending internal factor == (kind, degree) order: warp-uniform role
+    std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return order[x] < order[y]; });
+    Phase ph{};
+    ph.type = 2;
+    ph.list = 3;
+    ph.begin = (int32_t)(P.fitems.size() / 8);
+    // one lane per row slot; a factor's lanes never straddle a warp
+    int32_t lane = 0;
+    auto pad_to = [&](int32_t upto) {
+      for (; lane < upto; ++lane)
+        for (int c = 0; c < 8; ++c) P.fitems.push_back(c == 2 ? (lane << 16) : 0);
+    };
+    for (int32_t i : idx) {
+      const int32_t fi = order[i], r = L.frow[fi], d = L.frow[fi + 1] - r;
+      if (lane + d > 32) {
+        pad_to(32);
+        lane = 0;
+      }
+      const int32_t base = lane;
+      for (int32_t kk = 0; kk < d; ++kk, ++lane) {
+        const int32_t q = L.vtof_twin[r + kk];
+        const int32_t w = L.vslot[2 * (size_t)q + 1];
+        P.fitems.push_back(fi);
+        P.fitems.push_back(r);
+        P.fitems.push_back(d | kk << 8 | base << 16);
+        P.fitems.push_back(tm[i] | sm[i] << 12);
+        P.fitems.push_back(q - (w & 0xffff));
+        P.fitems.push_back(w);
+        P.fitems.push_back(L.vslot[2 * (size_t)q]);
+        P.fitems.push_back(q);
+      }
+      if (lane == 32) lane = 0;
+    }
+    if (lane) pad_to(32);
+    ph.end = (int32_t)(P.fitems.size() / 8);
+    push_phase(ph, ph.end - ph.begin);
+    ++P.n_fused;
+  };
+
   const int64_t levels = std::max<int64_t>(k, 1);
   for (int64_t b = 0; b < levels; ++b) {
     cur_batch = (int32_t)b;
+    if (fusable(b)) {
+      emit_fused(b);
+      continue;
+    }
     // ---------------- variable side: vtof(t_b) (+ marginals in phase 0)
     {
       slots.clear();

@@ -514,3 +514,50 @@ def test_underflow_attribution_with_evidence_codes():
         assert (ei.value.kind, ei.value.iteration, ei.value.index) == o["underflow"], trial
         raised += 1
     assert raised >= 40, raised
+
+
+def _plan_info(g, sched):
+    import ctypes as C
+    lib = P._native.lib()
+    f = lib.hbp_debug_plan_info
+    f.restype = None
+    f.argtypes = [C.c_void_p] + [C.POINTER(C.c_int32)] * 4
+    plan = P.engine.device_graph(g).plan(sched, g)
+    nph, grid, thr, nfused = (C.c_int32() for _ in range(4))
+    f(plan.handle, C.byref(nph), C.byref(grid), C.byref(thr), C.byref(nfused))
+    return nph.value, nfused.value
+
+
+def test_level_fusion_plans():
+    """Levels whose factor-side writes no other factor of the level reads
+    run as one phase (layout.cpp emit_fused): every level >= 1 of ftp's
+    canonical SEQFIX (475 of 476), about half of hedc's random order."""
+    w = W.build("C4-SEQFIX")
+    sched = w.strategy.compile(w.graph)
+    nph, nfused = _plan_info(w.graph, sched)
+    assert sched.num_batches == 476 and nfused == 475 and nph == 2 + 475, (nph, nfused)
+    w = W.build("C2")
+    nph, nfused = _plan_info(w.graph, w.strategy.compile(w.graph))
+    assert 90 <= nfused < 224 and nph == 2 * 224 - nfused, (nph, nfused)
+
+
+def test_level_fusion_bitwise_identical_to_two_phase(monkeypatch):
+    """HBP_FUSE=0 runs every level as two phases: same bits, iterations and
+    deltas as the fused plan, on every schedule family."""
+    rng = np.random.default_rng(4242)
+    graphs = [W.graph("hedc")[0]] + [random_graph(rng, max_vars=40, max_factors=40, max_body=6)
+                                     for _ in range(12)]
+    for i, g in enumerate(graphs):
+        for mode in (1, 2, 3):
+            sched = _compile_any(rng, g, mode)
+            opts = EngineOptions(60, 1e-9)
+            monkeypatch.delenv("HBP_FUSE", raising=False)
+            P.engine.clear_device_cache()
+            ref = P.run(g, sched, opts)
+            monkeypatch.setenv("HBP_FUSE", "0")
+            P.engine.clear_device_cache()
+            got = P.run(g, sched, opts)
+            assert got.iterations == ref.iterations, (i, mode)
+            assert got.marginals.tobytes() == ref.marginals.tobytes(), (i, mode)
+            assert np.asarray(got.deltas).tobytes() == np.asarray(ref.deltas).tobytes()
+    P.engine.clear_device_cache()

@@ -53,8 +53,9 @@ def test_binding_bitwise_vs_hornbp_run(R):
     g, _ = R.generate(R.SynthSpec(313, 383, 8, 0))  # C1 weblech, the reference's generator
     for strat, opts in ((R.Strategy.parall(), R.EngineOptions(max_iterations=100, tolerance=0.0)),
                         (R.Strategy.seqfix(), R.EngineOptions(max_iterations=1000, tolerance=1e-9)),
-                        (R.Strategy.topo(), R.EngineOptions(max_iterations=50, tolerance=1e-9,
-                                                            record_history=True))):
+                        # explicit-order SEQFIX (TOPO needs a forest; weblech is loopy)
+                        (R.Strategy.seqfix(list(reversed(list(g.edges())))),
+                         R.EngineOptions(max_iterations=50, tolerance=1e-9, record_history=True))):
         sched = strat.compile(g)
         want = R.run(g, sched, opts)
         got = hornbp_gpu.run(g, sched, opts)

@@ -79,6 +79,15 @@ int main() {
   run("dependent DFMA", dep_dfma);
   run("normalise pair (DADD + div2_rn)", dep_div2);
   run("normalise pair (DADD + 2x __ddiv_rn)", dep_ddiv);
+  // one SM, 768 threads: the same dependent chains (a fused level's shape)
+  auto run768 = [&](const char *name, void (*k)(double, int, double *, long long *)) {
+    k<<<1, 768>>>(0.3, n, out, cyc);
+    k<<<1, 768>>>(0.3, n, out, cyc);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-40s %lld cycles per step (768 threads, 1 SM)\n", name, h);
+  };
+  run768("dependent DMUL", dep_dmul);
+  run768("normalise pair (DADD + div2_rn)", dep_div2);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);

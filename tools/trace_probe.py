@@ -18,9 +18,9 @@ lib = _native.lib()
 lib.hbp_debug_trace.restype = C.c_int64
 lib.hbp_debug_trace.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_int64]
 nph, grid, thr = C.c_int32(), C.c_int32(), C.c_int32()
-lib.hbp_debug_plan_info(plan.handle, C.byref(nph), C.byref(grid), C.byref(thr))
+lib.hbp_debug_plan_info(plan.handle, C.byref(nph), C.byref(grid), C.byref(thr), None)
 nph, G = nph.value, grid.value
-n = 4 * nph * G * 2 + (2 * 16384 if nph == 2 else 0)
+n = 4 * nph * G * 2 + 2 * 16384
 buf = (C.c_ulonglong * n)()
 lib.hbp_debug_trace(plan.handle, buf, n)
 allb = np.frombuffer(buf, dtype=np.uint64)
