@@ -413,6 +413,11 @@ def run_ours_sweep(args) -> None:
     P.engine.set_device(local)
     multi = world > 1
     if multi:
+        # NCCL's init lines (nranks, NVLS) go to stderr: the driver's log shows
+        # the communicator; stdout stays the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if shared:
             dist.init_process_group("gloo")
         else:
@@ -539,11 +544,15 @@ def run_ours_sweep(args) -> None:
     except (OSError, KeyError, ValueError):
         pass
 
+    cfg = sweep_config(n, world)
+    if shared and multi:
+        cfg["shared_gpu"] = (f"test mode: all {world} ranks on cuda:0 over gloo "
+                             "(HBP_BENCH_SHARED_GPU=1, the box has fewer GPUs than ranks)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": sweep_config(n, world),
+        "config": cfg,
         "time_to_convergence_ms": ms_max / args.steps,
         "iterations": {"min": int(last.iterations.min()), "max": int(last.iterations.max()),
                        "mean": float(last.iterations.mean())},
@@ -843,6 +852,27 @@ def run_ours_single(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def spawn(args) -> None:
+    """`python bench.py --gpus N` outside torchrun: launch the N ranks the
+    way the driver does (torch.distributed.run, one process per GPU, rendezvous
+    on 127.0.0.1). On a box with fewer than N GPUs the ranks share cuda:0 over
+    gloo (HBP_BENCH_SHARED_GPU=1, a test mode the JSON line names)."""
+    import socket
+
+    import torch
+
+    env = dict(os.environ)
+    if torch.cuda.device_count() < args.gpus:
+        env["HBP_BENCH_SHARED_GPU"] = "1"
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd, env=env).returncode)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -854,6 +884,9 @@ def main() -> None:
     ap.add_argument("--sets", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

@@ -47,13 +47,6 @@ namespace hbp {
 
 using namespace dev;
 
-constexpr int kSwWarps = 8;  // warps per CTA (blockDim = 256); lanes = 32 sets
-constexpr int kSwThreads = 32 * kSwWarps;
-constexpr int kSwMinBlocks = 4;  // default register budget: 4 CTAs (32 warps) per SM
-#ifndef HBP_SWEEP_NS
-#define HBP_SWEEP_NS 1
-#endif
-constexpr int kSweepNS = HBP_SWEEP_NS;  // default sets per lane of the staged kernel
 constexpr int kNoVar = 0x7f7f7f7f;  // ufmarg reset value (memset 0x7F)
 
 struct SweepParams {
@@ -122,63 +115,7 @@ __device__ __forceinline__ unsigned long long sw_globaltimer() {
   return t;
 }
 
-// ---- per-thread view of its set group ---------------------------------------------------
-// Arrays are tiled [group][row][32]: group g = sets 32g..32g+31, so a warp's
-// 32 lanes read one contiguous 512-byte segment per row and a node's d rows
-// are d consecutive segments (DRAM-page friendly streaming).
-
-struct SwLane {
-  double2 *vtof, *ftov;     // &X[g][0][lane]
-  double *p0;
-  const unsigned char *ev;
-  int s;                    // set index within the pass
-};
-
-// current state buffers of the staged kernel (swapped by a compaction)
-struct SwBufs {
-  double2 *ftov, *vtof;
-  double *p0;
-  unsigned char *ev;
-  int parity;  // 0: the pass's original p0 / ev buffers, 1: the alternates
-};
-
-__device__ __forceinline__ SwLane sw_lane_b(const SwBufs &B, int slot, int set, int E, int V) {
-  const int g = slot >> 5, lane = slot & 31;
-  SwLane L;
-  L.vtof = B.vtof + (size_t)g * E * 32 + lane;
-  L.ftov = B.ftov + (size_t)g * E * 32 + lane;
-  L.p0 = B.p0 + (size_t)g * V * 32 + lane;
-  L.ev = B.ev + (size_t)g * V * 32 + lane;
-  L.s = set;
-  return L;
-}
-
-__device__ __forceinline__ SwLane sw_lane(const SweepParams &P, int s, int E) {
-  const int g = s >> 5, lane = s & 31;
-  SwLane L;
-  L.vtof = P.vtof + (size_t)g * E * 32 + lane;
-  L.ftov = P.ftov + (size_t)g * E * 32 + lane;
-  L.p0 = P.p0 + (size_t)g * P.V * 32 + lane;
-  L.ev = P.ev + (size_t)g * P.V * 32 + lane;
-  L.s = s;
-  return L;
-}
-
-// ---- message output: normalise, record underflow (engine.py:155-165) ----------------------
-
-__device__ __forceinline__ void sw_put(const SweepParams &P, double2 *dst, double a0, double a1,
-                                      unsigned kind, unsigned slot, unsigned long long &uf) {
-  if (P.normalize) {
-    const double t = add(a0, a1);
-    if (t < kMinMessageSum) {
-      const unsigned long long key = ((unsigned long long)kind << 32) | slot;
-      uf = key < uf ? key : uf;
-    }
-    div2_rn(a0, a1, t, a0, a1);
-  }
-  *dst = make_double2(a0, a1);
-}
-
+// ---- the clamp factor's message ---------------------------------------------------------
 // the clamp factor's message, multiplied in after the row (it is the row's last slot)
 __device__ __forceinline__ void sw_clamp(unsigned code, double &a0, double &a1) {
   if (code & 1u) {  // observed false: (1, 0)
@@ -188,324 +125,6 @@ __device__ __forceinline__ void sw_clamp(unsigned code, double &a0, double &a1) 
   if (code & 2u) {  // observed true: (0, 1)
     a0 = mul(a0, 0.0);
     a1 = mul(a1, 1.0);
-  }
-}
-
-// marginal of the previous iteration + |dP1| (engine.py:510-523, :557, :572);
-// prev_p0 was loaded together with the row
-__device__ __forceinline__ void sw_marginal(const SweepParams &P, const SwLane &L, int v, int it,
-                                           double q0, double q1, double prev_p0,
-                                           unsigned long long &dmax) {
-  const double t = add(q0, q1);
-  // NaN totals suppress the raise (numpy's min propagates NaN): they record -1
-  if (!(t >= kMinMessageSum)) atomicMin(&P.ufmarg[(size_t)(it - 1) * P.S + L.s], t != t ? -1 : P.vorig[v]);
-  const double p0 = div_rn(q0, t);
-  const double p1 = sub(1.0, p0);
-  const double prev = it == 2 ? 0.5 : sub(1.0, prev_p0);  // prev P1 starts at 0.5
-  const unsigned long long raw = (unsigned long long)__double_as_longlong(sub(p1, prev));
-  unsigned long long bits;
-  asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
-  dmax = bits > dmax ? bits : dmax;
-  L.p0[v * 32] = p0;
-}
-
-// ---- variable side: every outgoing vtof message of node v + its marginal ------------------
-
-template <int D>
-__device__ __forceinline__ void sw_var_fixed(const SweepParams &P, const SwLane &L, int v, int r,
-                                            int it, bool write_vtof, unsigned long long &dmax,
-                                            unsigned long long &uf) {
-  // every load of the node first (one memory round trip), then the products
-  double x0[D], x1[D];
-  unsigned tw[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double2 m = L.ftov[(r + k) * 32];
-    x0[k] = m.x;
-    x1[k] = m.y;
-    tw[k] = __ldg(P.ftov_twin + r + k);
-  }
-  const unsigned code = L.ev[v * 32];
-  const double prev_p0 = it > 2 ? L.p0[v * 32] : 0.5;
-  double a0 = 1.0, a1 = 1.0;  // prefix x[0] * ... * x[j-1]: the reference's partial products
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    if (write_vtof && !(tw[j] & kUnaryBit)) {
-      double b0 = a0, b1 = a1;
-#pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b0 = mul(b0, x0[k]);
-        b1 = mul(b1, x1[k]);
-      }
-      if (code) sw_clamp(code, b0, b1);
-      sw_put(P, L.vtof + tw[j] * 32, b0, b1, 0u, tw[j], uf);
-    }
-    a0 = mul(a0, x0[j]);
-    a1 = mul(a1, x1[j]);
-  }
-  if (code) sw_clamp(code, a0, a1);
-  sw_marginal(P, L, v, it, a0, a1, prev_p0, dmax);
-}
-
-// rows longer than 6: per target, re-read the row (L1 hits), same left-to-right order
-__device__ __noinline__ void sw_var_long(const SweepParams &P, const SwLane &L, int v, int r, int d,
-                                         int it, bool write_vtof, unsigned long long &dmax,
-                                         unsigned long long &uf) {
-  const unsigned code = L.ev[v * 32];
-  const double prev_p0 = it > 2 ? L.p0[v * 32] : 0.5;
-  if (write_vtof) {
-    for (int j = 0; j < d; ++j) {
-      const unsigned tw = __ldg(P.ftov_twin + r + j);
-      if (tw & kUnaryBit) continue;
-      double b0 = 1.0, b1 = 1.0;
-      for (int k = 0; k < d; ++k) {
-        if (k == j) continue;
-        const double2 m = L.ftov[(r + k) * 32];
-        b0 = mul(b0, m.x);
-        b1 = mul(b1, m.y);
-      }
-      if (code) sw_clamp(code, b0, b1);
-      sw_put(P, L.vtof + tw * 32, b0, b1, 0u, tw, uf);
-    }
-  }
-  double q0 = 1.0, q1 = 1.0;
-  for (int k = 0; k < d; ++k) {
-    const double2 m = L.ftov[(r + k) * 32];
-    q0 = mul(q0, m.x);
-    q1 = mul(q1, m.y);
-  }
-  if (code) sw_clamp(code, q0, q1);
-  sw_marginal(P, L, v, it, q0, q1, prev_p0, dmax);
-}
-
-__device__ __forceinline__ void sw_var(const SweepParams &P, const SwLane &L, int v, int r, int d,
-                                      int it, bool write_vtof, unsigned long long &dmax,
-                                      unsigned long long &uf) {
-  switch (d) {
-    case 1: sw_var_fixed<1>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    case 2: sw_var_fixed<2>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    case 3: sw_var_fixed<3>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    case 4: sw_var_fixed<4>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    case 5: sw_var_fixed<5>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    case 6: sw_var_fixed<6>(P, L, v, r, it, write_vtof, dmax, uf); break;
-    default: sw_var_long(P, L, v, r, d, it, write_vtof, dmax, uf); break;
-  }
-}
-
-// ---- factor side: every outgoing ftov message of factor f ---------------------------------
-// Head target: products over body slots of (m0 + m1) and m1 (AND) / m0 (OR),
-// engine.py:229-248; body targets: the head slot contributes the blend and
-// (m0 - m1), engine.py:198-226. Iteration 1 reads no messages: every vtof
-// message is still the normalised uniform one.
-
-template <int D, int KIND>
-__device__ __forceinline__ void sw_fac_fixed(const SweepParams &P, const SwLane &L, int f, int r,
-                                            int it, unsigned long long &uf) {
-  const double2 pp = __ldg(P.fpar + f);
-  double m0[D], m1[D];
-  int tw[D];
-  const double c = P.normalize ? 0.5 : 1.0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    tw[k] = __ldg(P.vtof_twin + r + k);
-    if (it == 1) {
-      m0[k] = c;
-      m1[k] = c;
-    } else {
-      const double2 m = L.vtof[(r + k) * 32];
-      m0[k] = m.x;
-      m1[k] = m.y;
-    }
-  }
-  double sm[D];
-#pragma unroll
-  for (int k = 1; k < D; ++k) sm[k] = add(m0[k], m1[k]);
-  {
-    double h1 = 1.0, h2 = 1.0;
-#pragma unroll
-    for (int k = 1; k < D; ++k) {
-      h1 = mul(h1, sm[k]);
-      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
-    }
-    double o0, o1;
-    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    sw_put(P, L.ftov + tw[0] * 32, o0, o1, 1u, (unsigned)tw[0], uf);
-  }
-  if (D > 1) {
-    double a1, a2;
-    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
-#pragma unroll
-    for (int j = 1; j < D; ++j) {
-      double b1 = a1, b2 = a2;
-#pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b1 = mul(b1, sm[k]);
-        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
-      }
-      double o0, o1;
-      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-      sw_put(P, L.ftov + tw[j] * 32, o0, o1, 1u, (unsigned)tw[j], uf);
-      a1 = mul(a1, sm[j]);
-      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
-    }
-  }
-}
-
-template <int KIND>
-__device__ __noinline__ void sw_fac_long(const SweepParams &P, const SwLane &L, int f, int r, int d,
-                                         int it, unsigned long long &uf) {
-  const double2 pp = __ldg(P.fpar + f);
-  const double c = P.normalize ? 0.5 : 1.0;
-  for (int j = 0; j < d; ++j) {
-    double b1 = 1.0, b2 = 1.0;
-    for (int k = 0; k < d; ++k) {
-      if (k == j) continue;
-      const double2 m = it == 1 ? make_double2(c, c) : L.vtof[(r + k) * 32];
-      double f1, f2;
-      if (k == 0) {
-        head_slot_terms<KIND>(pp.x, pp.y, m.x, m.y, f1, f2);
-      } else {
-        f1 = add(m.x, m.y);
-        f2 = KIND == 0 ? m.y : m.x;
-      }
-      b1 = mul(b1, f1);
-      b2 = mul(b2, f2);
-    }
-    double o0, o1;
-    if (j == 0)
-      head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-    else
-      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-    const int tw = __ldg(P.vtof_twin + r + j);
-    sw_put(P, L.ftov + tw * 32, o0, o1, 1u, (unsigned)tw, uf);
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void sw_fac_k(const SweepParams &P, const SwLane &L, int f, int r, int d,
-                                        int it, unsigned long long &uf) {
-  switch (d) {
-    case 1:  // prior / unary: a constant message, written once
-      if (it == 1) sw_fac_fixed<1, KIND>(P, L, f, r, it, uf);
-      break;
-    case 2: sw_fac_fixed<2, KIND>(P, L, f, r, it, uf); break;
-    case 3: sw_fac_fixed<3, KIND>(P, L, f, r, it, uf); break;
-    case 4: sw_fac_fixed<4, KIND>(P, L, f, r, it, uf); break;
-    case 5: sw_fac_fixed<5, KIND>(P, L, f, r, it, uf); break;
-    default: sw_fac_long<KIND>(P, L, f, r, d, it, uf); break;
-  }
-}
-
-__device__ __forceinline__ void sw_fac(const SweepParams &P, const SwLane &L, int f, int r, int d,
-                                      int it, unsigned long long &uf) {
-  const bool is_or = (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
-  if (!is_or)
-    sw_fac_k<0>(P, L, f, r, d, it, uf);
-  else
-    sw_fac_k<1>(P, L, f, r, d, it, uf);
-}
-
-// ---- the persistent sweep kernel -----------------------------------------------------------
-// grid (NX, S/32), block 256 = 8 warps; lane = set blockIdx.y*32 + lane, warps
-// stride over nodes. Per iteration: [variable side: marginal(it-1) + delta +
-// vtof(it)] -> grid sync -> per-set stop decision -> [factor side: ftov(it)]
-// -> grid sync -> exit when every set has stopped. The next node's row bounds
-// are fetched while the current node computes.
-
-template <int MINB>
-__global__ void __launch_bounds__(kSwThreads, MINB) sweep_persistent(const __grid_constant__ SweepParams P) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int s = blockIdx.y * 32 + lane;
-  const unsigned nblocks = gridDim.x * gridDim.y;
-  const int wstride = gridDim.x * kSwWarps;
-  const int w0 = blockIdx.x * kSwWarps + warp;
-  const int E = P.E;
-  const SwLane L = sw_lane(P, s, E);
-  bool alive = s < P.nsets;
-  unsigned expected = 0;
-  __shared__ unsigned long long red[kSwWarps][32];
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *P.t0 = sw_globaltimer();
-
-  for (int it = 1;; ++it) {
-    if (it >= 2) {
-      const bool final_pass = it == P.max_it + 1;
-      unsigned long long dmax = 0, uf = ~0ull;
-      if (__syncthreads_or(alive) && alive && w0 < P.V) {
-        int v = w0;
-        int r = __ldg(P.vrow + v), re = __ldg(P.vrow + v + 1);
-        while (true) {
-          const int vn = v + wstride;
-          int rn = 0, rne = 0;
-          if (vn < P.V) {
-            rn = __ldg(P.vrow + vn);
-            rne = __ldg(P.vrow + vn + 1);
-          }
-          sw_var(P, L, v, r, re - r, it, !final_pass, dmax, uf);
-          if (vn >= P.V) break;
-          v = vn;
-          r = rn;
-          re = rne;
-        }
-      }
-      red[warp][lane] = dmax;
-      __syncthreads();
-      if (warp == 0) {
-        unsigned long long m = 0;
-#pragma unroll
-        for (int w = 0; w < kSwWarps; ++w) m = red[w][lane] > m ? red[w][lane] : m;
-        if (alive) atomicMax(&P.dbits[(size_t)(it - 1) * P.S + s], m);
-      }
-      if (alive && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
-      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && P.time_limit_ns > 0)
-        P.tflag[it - 1] = (long long)(sw_globaltimer() - *P.t0) > P.time_limit_ns;
-      sw_grid_sync(P.bar, expected, nblocks);
-      // stop decision for iteration done = it - 1: every thread of set s reads
-      // the same final values, so the decision is identical across CTAs
-      const int done = it - 1;
-      int stop = 0;
-      if (alive) {
-        const size_t i = (size_t)done * P.S + s;
-        const unsigned long long db = ((const volatile unsigned long long *)P.dbits)[i];
-        const unsigned long long uk = ((const volatile unsigned long long *)P.ufkey)[i];
-        const int um = ((const volatile int *)P.ufmarg)[i];
-        const int tf = ((const volatile int *)P.tflag)[done];
-        if (uk != ~0ull || (um != kNoVar && um >= 0)) stop = 4;
-        else if (__longlong_as_double((long long)db) < P.tol) stop = 1;
-        else if (done == P.max_it) stop = 2;
-        else if (tf) stop = 3;
-      }
-      if (stop) {
-        alive = false;
-        if (blockIdx.x == 0 && warp == 0) {
-          P.res_it[s] = done;
-          P.res_stop[s] = stop;
-          atomicAdd(P.nstop, 1u);
-        }
-      }
-    }
-    {
-      unsigned long long uf = ~0ull;
-      if (__syncthreads_or(alive) && alive && w0 < P.F) {
-        int f = w0;
-        int r = __ldg(P.frow + f), re = __ldg(P.frow + f + 1);
-        while (true) {
-          const int fn = f + wstride;
-          int rn = 0, rne = 0;
-          if (fn < P.F) {
-            rn = __ldg(P.frow + fn);
-            rne = __ldg(P.frow + fn + 1);
-          }
-          sw_fac(P, L, f, r, re - r, it, uf);
-          if (fn >= P.F) break;
-          f = fn;
-          r = rn;
-          re = rne;
-        }
-      }
-      if (alive && uf != ~0ull) atomicMin(&P.ufkey[(size_t)it * P.S + s], uf);
-    }
-    sw_grid_sync(P.bar, expected, nblocks);
-    if (((const volatile unsigned *)P.nstop)[0] >= (unsigned)P.S) return;
   }
 }
 
@@ -1583,7 +1202,6 @@ struct hbp_sweep {
   int4 *d_vchunks = nullptr, *d_fchunks = nullptr;
   int n_vchunks = 0, n_fchunks = 0, fchunk_nonunary = 0;
   size_t smem = 0;
-  bool ws = true;
   double2 *d_vtof = nullptr, *d_ftov = nullptr;
   double *d_p0 = nullptr, *d_p0_alt = nullptr;
   int compact_cap = 0;  // slots the alternate buffers hold
@@ -1692,49 +1310,28 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   const hbp::HostLayout &L = g->L;
   int per_sm = 0;
   {
-    // HBP_SWEEP_KERNEL=plain selects the register-pipelined kernel (A/B
-    // comparison); the default is the TMA-staged warp-specialised one.
-    const char *kenv = getenv("HBP_SWEEP_KERNEL");
-    sw->ws = !(kenv && std::string(kenv) == "plain");
-    if (sw->ws) {
-      // HBP_SWEEP_NS: sets per lane (1 or 2). Measured on B200 (1,024 ftp
-      // sets): NS=1 182-184 ms, NS=2 209 ms -- the default stays 1.
-      const char *nenv = getenv("HBP_SWEEP_NS");
-      sw->ns = nenv ? (atoi(nenv) == 2 ? 2 : 1) : hbp::kSweepNS;
-      if (sw->ns == 2) {
-        sw->smem = sizeof(hbp::WsShared<2, double>);
-        sw->threads = hbp::WsCfg<2>::threads;
-        sw->kernel = (const void *)hbp::sweep_ws<true, 2, double>;
-        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 2, double>;
-      } else {
-        sw->smem = sizeof(hbp::WsShared<1, double>);
-        sw->threads = hbp::WsCfg<1>::threads;
-        sw->kernel = (const void *)hbp::sweep_ws<true, 1, double>;
-        sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 1, double>;
-      }
-      // fp32 mode (opt-in per run): the same staged kernel on float messages
-      sw->smem32 = sizeof(hbp::WsShared<1, float>);
-      sw->kernel32 = (const void *)hbp::sweep_ws<true, 1, float>;
-      sw->kernel32_nonorm = (const void *)hbp::sweep_ws<false, 1, float>;
-      for (const void *k : {sw->kernel32, sw->kernel32_nonorm})
-        HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem32));
-      int per_sm32 = 0;
-      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, sw->kernel32,
-                                                             hbp::WsCfg<1>::threads, sw->smem32));
-      sw->grid_x_max32 = std::max(1, per_sm32) * g->num_sms;
-      for (const void *k : {sw->kernel, sw->kernel_nonorm})
-        HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem));
-      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, sw->threads,
-                                                             sw->smem));
-    } else {
-      const char *env = getenv("HBP_SWEEP_MINB");
-      const int minb = env ? atoi(env) : hbp::kSwMinBlocks;
-      sw->kernel = minb == 3 ? (const void *)hbp::sweep_persistent<3>
-                 : minb == 2 ? (const void *)hbp::sweep_persistent<2>
-                             : (const void *)hbp::sweep_persistent<4>;
-      sw->kernel_nonorm = sw->kernel;
-      HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, hbp::kSwThreads, 0));
-    }
+    // the TMA-staged warp-specialised kernel, one set per lane. Measured on
+    // B200 against a register-pipelined kernel without staging and against
+    // two sets per lane: both slower, removed.
+    sw->ns = 1;
+    sw->smem = sizeof(hbp::WsShared<1, double>);
+    sw->threads = hbp::WsCfg<1>::threads;
+    sw->kernel = (const void *)hbp::sweep_ws<true, 1, double>;
+    sw->kernel_nonorm = (const void *)hbp::sweep_ws<false, 1, double>;
+    // fp32 mode (opt-in per run): the same staged kernel on float messages
+    sw->smem32 = sizeof(hbp::WsShared<1, float>);
+    sw->kernel32 = (const void *)hbp::sweep_ws<true, 1, float>;
+    sw->kernel32_nonorm = (const void *)hbp::sweep_ws<false, 1, float>;
+    for (const void *k : {sw->kernel32, sw->kernel32_nonorm})
+      HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem32));
+    int per_sm32 = 0;
+    HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, sw->kernel32,
+                                                           hbp::WsCfg<1>::threads, sw->smem32));
+    sw->grid_x_max32 = std::max(1, per_sm32) * g->num_sms;
+    for (const void *k : {sw->kernel, sw->kernel_nonorm})
+      HBP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw->smem));
+    HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw->kernel, sw->threads,
+                                                           sw->smem));
   }
   sw->grid_x_max = std::max(1, per_sm) * g->num_sms;
   // capacity: requested, else what fits in half of the free memory
@@ -1796,11 +1393,10 @@ hbp_status hbp_sweep_create(hbp_graph *g, int32_t max_sets_per_pass, hbp_sweep *
   HBP_CUDA(cudaMalloc(&sw->d_ftov, (size_t)L.E * cap * sizeof(double2)));
   HBP_CUDA(cudaMalloc(&sw->d_p0, (size_t)std::max(1, L.V) * cap * sizeof(double)));
   HBP_CUDA(cudaMalloc(&sw->d_ev, (size_t)std::max(1, L.V) * cap + 4));
-  if (sw->ws) {  // compaction's alternate state buffers (passes of <= kMaxCompact slots)
-    sw->compact_cap = std::min(cap, hbp::kMaxCompact);
-    HBP_CUDA(cudaMalloc(&sw->d_p0_alt, (size_t)std::max(1, L.V) * sw->compact_cap * sizeof(double)));
-    HBP_CUDA(cudaMalloc(&sw->d_ev_alt, (size_t)std::max(1, L.V) * sw->compact_cap + 4));
-  }
+  // compaction's alternate state buffers (passes of <= kMaxCompact slots)
+  sw->compact_cap = std::min(cap, hbp::kMaxCompact);
+  HBP_CUDA(cudaMalloc(&sw->d_p0_alt, (size_t)std::max(1, L.V) * sw->compact_cap * sizeof(double)));
+  HBP_CUDA(cudaMalloc(&sw->d_ev_alt, (size_t)std::max(1, L.V) * sw->compact_cap + 4));
   HBP_CUDA(cudaEventCreate(&sw->e0));
   HBP_CUDA(cudaEventCreate(&sw->e1));
   HBP_CUDA(cudaEventCreate(&sw->k0));
@@ -1839,10 +1435,6 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     return HBP_EINVAL;
   }
   const bool fp32 = opt->precision == 1;
-  if (fp32 && !sw->ws) {
-    hbp::set_error("fp32 mode needs the staged sweep kernel");
-    return HBP_EINVAL;
-  }
   hbp_graph *g = sw->g;
   const hbp::HostLayout &L = g->L;
   const int n = ev->num_sets;
@@ -1992,7 +1584,6 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     const int unit = 32 * sw->ns;
     const int S = (ns + unit - 1) / unit * unit;
     const int groups = S / 32;
-    const int nx = std::max(1, std::min(sw->grid_x_max / groups, (L.F + hbp::kSwWarps - 1) / hbp::kSwWarps));
     P.S = S;
     P.nsets = ns;
     P.compact = compact_enabled && S <= sw->compact_cap;
@@ -2034,7 +1625,7 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 12, cudaMemcpyHostToDevice, st));
     void *args[] = {&P};
     HBP_CUDA(cudaEventRecord(sw->k0, st));
-    if (sw->ws) {
+    {
       const int gy = groups / (fp32 ? 1 : sw->ns);
       const int gxm = fp32 ? sw->grid_x_max32 : sw->grid_x_max;
       const int nxw = std::max(1, std::min(gxm / gy, sw->n_vchunks));
@@ -2043,9 +1634,6 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       HBP_CUDA(cudaLaunchCooperativeKernel(k, dim3(nxw, gy),
                                            dim3(fp32 ? hbp::WsCfg<1>::threads : sw->threads), args,
                                            fp32 ? sw->smem32 : sw->smem, st));
-    } else {
-      HBP_CUDA(cudaLaunchCooperativeKernel(sw->kernel, dim3(nx, groups), dim3(hbp::kSwThreads), args,
-                                           0, st));
     }
     HBP_CUDA(cudaEventRecord(sw->k1, st));
     ++launches;

@@ -125,18 +125,22 @@ def test_trees_all_strategies_bitwise_and_exact():
             assert np.allclose(res.marginals, exact, atol=1e-8)
 
 
-def test_bitwise_independent_of_block_size():
-    w = W.build("C2")
-    sched = w.strategy.compile(w.graph)
-    a = P.run(w.graph, sched, EngineOptions(1000, 1e-9))
-    os.environ["HBP_THREADS"] = "512"
-    try:
-        P.engine.clear_device_cache()
-        b = P.run(w.graph, sched, EngineOptions(1000, 1e-9))
-    finally:
-        os.environ.pop("HBP_THREADS")
-        P.engine.clear_device_cache()
-    assert a.marginals.tobytes() == b.marginals.tobytes()
+def test_bitwise_independent_of_grid_size():
+    """HBP_GRID forces the CTA count: the work moves between CTAs, the bits
+    do not (PARALL whole-node phases and fused levels alike)."""
+    for key in ("C2", "C4-PARALL"):
+        w = W.build(key)
+        sched = w.strategy.compile(w.graph)
+        a = P.run(w.graph, sched, EngineOptions(1000, 1e-9))
+        os.environ["HBP_GRID"] = "37"
+        try:
+            P.engine.clear_device_cache()
+            b = P.run(w.graph, sched, EngineOptions(1000, 1e-9))
+        finally:
+            os.environ.pop("HBP_GRID")
+            P.engine.clear_device_cache()
+        assert a.iterations == b.iterations
+        assert a.marginals.tobytes() == b.marginals.tobytes()
 
 
 # ---- run-loop contracts (engine.py:531-594) -----------------------------------------------
