@@ -43,6 +43,10 @@ constexpr int kThreads = 768;  // default block size: 80 registers, fewest spill
 #define HBP_FUSED_THREADS 768
 #endif
 constexpr int kFusedThreads = HBP_FUSED_THREADS;  // plans with fused levels
+#ifndef HBP_GROUP_MIN
+#define HBP_GROUP_MIN (HBP_NODE_MAX + 1)
+#endif
+static_assert(HBP_GROUP_MIN >= 2 && HBP_GROUP_MIN <= HBP_NODE_MAX + 1, "lane-group threshold");
 constexpr int kTraceIters = 4;  // HBP_TRACE=1: timestamps for iterations 2..5
 constexpr int kPhaseCache = 1024;  // phase descriptors staged in shared memory (32 KB)
 constexpr int kChunkTrace = 16384;  // HBP_TRACE=1: per-chunk ns of iteration 3, PARALL phases 0/1
@@ -55,6 +59,20 @@ struct Ctrl {
   unsigned long long t0;
   unsigned long long last_delta;  // delta bits of the stopping iteration
 };
+
+// A chunk class of a whole-node phase: chunks [chunk_begin, next class's)
+// cover the class's nodes [node_begin, node_end) (rows from row_begin) --
+// style 0: one node per lane (degree <= kNodeMax), style 1: lane groups (one
+// lane per row slot, 32 / d nodes per chunk, degree <= kClassMax), style 2:
+// one slot per lane over [row_begin, node_end) (huge nodes; node_end holds
+// the slot end there).
+struct ChunkClass {
+  int chunk_begin, node_begin, node_end, row_begin;
+  int info;  // degree | kind << 16 | style << 20
+  int grp;   // lane groups: nodes per chunk | ceil(2^16 / degree) << 8 (lane / d as a multiply)
+};
+constexpr int kMaxVarClasses = kClassMax + 2;
+constexpr int kMaxFacClasses = 2 * (kClassMax + 2);
 
 struct KParams {
   // layout
@@ -80,6 +98,12 @@ struct KParams {
   int vc_node[kNodeMax + 2], vc_row[kNodeMax + 2];
   int fa_node[kNodeMax + 2], fa_row[kNodeMax + 2];  // light AND factors
   int fo_node[kNodeMax + 2], fo_row[kNodeMax + 2];  // light OR factors
+  // whole-node phases: the chunk classes of each side (base_params), in
+  // processing order (dearest first); a class's chunks are warp-uniform in
+  // role, degree and style
+  ChunkClass vcc[kMaxVarClasses], fcc[kMaxFacClasses];
+  int nvcc, nfcc;
+  int vchunks, fchunks, fchunks_nounary;  // factor chunks without the unary classes (last)
   // plan
   const Phase *phases;
   int nphases;
@@ -141,19 +165,18 @@ __device__ __forceinline__ void sync_point(Ctrl *c, Sync &s, unsigned arrivals, 
 // --------------------------------------------------------------------------------------
 // message output with normalisation + underflow flag (engine.py:155-165)
 
-// Underflow is recorded in a per-thread key (min over the phase) and
-// published once per phase by flush_underflow, so the common path issues no
-// atomics. key = phase << 33 | kind << 32 | slot.
+// Underflow is recorded in per-thread flag bits (bit 0 a vtof, bit 1 an ftov
+// message) and published once per phase by flush_underflow -- uf_msg gets the
+// bits, uf_where the earliest failing phase (<< 33) -- so the common path
+// issues no atomics; the failing message itself is named by the attribution
+// re-run (attribute_underflow).
 __device__ __forceinline__ void put_message_ref(const KParams &P, double2 *dst, double &a0,
                                                 double &a1, int phase, int kind, int slot,
                                                 unsigned long long &ufkey) {
   if (P.normalize) {
     const double t = add(a0, a1);
-    if (__builtin_expect(t < kMinMessageSum, 0)) {
-      const unsigned long long key = ((unsigned long long)phase << 33) |
-                                     ((unsigned long long)kind << 32) | (unsigned)slot;
-      ufkey = key < ufkey ? key : ufkey;
-    }
+    // bit `kind` of the phase's underflow flags (flush_underflow)
+    ufkey |= (unsigned long long)(t < kMinMessageSum) << kind;
     div2_rn(a0, a1, t, a0, a1);
   }
   *dst = make_double2(a0, a1);
@@ -165,10 +188,11 @@ __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, doub
   put_message_ref(P, dst, a0, a1, phase, kind, slot, ufkey);
 }
 
-__device__ __forceinline__ void flush_underflow(const KParams &P, int it, unsigned long long ufkey) {
-  if (ufkey != ~0ull) {
-    atomicOr(&P.uf_msg[it], 1 << (int)((ufkey >> 32) & 1));
-    atomicMin(&P.uf_where[it], ufkey);
+__device__ __forceinline__ void flush_underflow(const KParams &P, int it, int phase,
+                                                unsigned long long ufkey) {
+  if (ufkey) {
+    atomicOr(&P.uf_msg[it], (int)ufkey);
+    atomicMin(&P.uf_where[it], (unsigned long long)phase << 33 | (unsigned long long)(~ufkey & 1) << 32);
   }
 }
 
@@ -539,6 +563,162 @@ __device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, i
   }
 }
 
+// --------------------------------------------------------------------------------------
+// lane groups (whole-node phases, kNodeMax < degree <= kClassMax): lane k of a
+// group owns row slot k of its node and loads that one message (a warp's loads
+// are one contiguous run of rows); the node's row reaches every lane of the
+// group by warp shuffles, and each lane forms its own slot's outgoing message
+// left to right over the row without its slot (engine.py:173-180) -- the
+// reference's order, so the same bits as the per-node kernels. d is
+// warp-uniform (one class per chunk); every lane of the warp calls these.
+
+__device__ __forceinline__ void vgroup(const KParams &P, int v, int q, int k, int d, int base,
+                                       bool active, bool marg, bool vt, int it, int phase,
+                                       unsigned long long &dmax, unsigned long long &ufkey,
+                                       bool uniform) {
+  double2 m = make_double2(1.0, 1.0);
+  unsigned tw = kUnaryBit, code = 0u;
+  double prev_p0 = 0.0;
+  int orig = 0;
+  const bool mk = marg && k == 0;
+  if (active) {
+    if (!uniform) m = P.ftov[q];
+    tw = __ldg(P.ftov_twin + q);
+    code = P.ev ? P.ev[v] : 0u;
+    if (mk) {
+      prev_p0 = P.p0[v];
+      orig = __ldg(P.vorig + v);
+    }
+  }
+  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
+  for (int i = 0; i < d; ++i) {
+    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
+    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
+    if (i != k) {
+      a0 = mul(a0, x0);
+      a1 = mul(a1, x1);
+    }
+    if (mk) {
+      q0 = mul(q0, x0);
+      q1 = mul(q1, x1);
+    }
+  }
+  if (!active) return;
+  if (vt && !(tw & kUnaryBit)) {
+    if (code && it > 1) apply_clamp(code, a0, a1);
+    put_message(P, P.vtof + tw, a0, a1, phase, 0, (int)tw, ufkey);
+  }
+  if (mk) {
+    if (code) apply_clamp(code, q0, q1);
+    put_marginal(P, v, q0, q1, it, dmax, prev_p0, orig);
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void fgroup(const KParams &P, int f, int p, int k, int d, int base,
+                                       bool active, int phase, unsigned long long &ufkey) {
+  double2 m = make_double2(1.0, 1.0), pp = make_double2(0.0, 0.0);
+  int tw = 0;
+  if (active) {
+    m = P.vtof[p];
+    tw = __ldg(P.vtof_twin + p);
+    pp = __ldg(P.fpar + f);
+  }
+  double b1 = 1.0, b2 = 1.0;
+  for (int i = 0; i < d; ++i) {
+    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
+    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
+    if (i != k) {
+      double f1, f2;
+      if (i == 0) {
+        head_slot_terms<KIND>(pp.x, pp.y, x0, x1, f1, f2);
+      } else {
+        f1 = add(x0, x1);
+        f2 = KIND == 0 ? x1 : x0;
+      }
+      b1 = mul(b1, f1);
+      b2 = mul(b2, f2);
+    }
+  }
+  if (!active) return;
+  double o0, o1;
+  if (k == 0)
+    head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+  else
+    body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
+  put_message(P, P.ftov + tw, o0, o1, phase, 1, tw, ufkey);
+}
+
+// one chunk of a whole-node phase: class cc, chunk j of the class
+__device__ __forceinline__ void var_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
+                                          bool marg, bool vt, int it, int phase,
+                                          unsigned long long &dmax, unsigned long long &ufkey,
+                                          bool uniform) {
+  const int d = cc.info & 0xffff, style = cc.info >> 20;
+  if (style == 0) {
+    const int v = cc.node_begin + j * 32 + lane;
+    if (v >= cc.node_end) return;
+    const int r = cc.row_begin + (v - cc.node_begin) * d;
+    switch (d) {
+      case 1: vnode_fixed<1>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+      case 2: vnode_fixed<2>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+      case 3: vnode_fixed<3>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+      default: vnode_fixed<kNodeMax>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+    }
+  } else if (style == 1) {
+    const int g = cc.grp & 0xff, ln = (lane * (cc.grp >> 8)) >> 16, k = lane - ln * d;
+    const int node = j * g + ln;
+    const int v = cc.node_begin + node;
+    vgroup(P, v, cc.row_begin + node * d + k, k, d, ln * d, ln < g && v < cc.node_end, marg, vt,
+           it, phase, dmax, ufkey, uniform);
+  } else {
+    const int q = cc.row_begin + j * 32 + lane;
+    if (q >= cc.node_end) return;
+    v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), vt ? -1 : 0, marg, it, phase, dmax,
+           ufkey, uniform);
+  }
+}
+
+__device__ __forceinline__ void fac_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
+                                          int phase, unsigned long long &ufkey) {
+  const int d = cc.info & 0xffff, kind = (cc.info >> 16) & 0xf, style = cc.info >> 20;
+  if (style == 0) {
+    const int f = cc.node_begin + j * 32 + lane;
+    if (f >= cc.node_end) return;
+    const int r = cc.row_begin + (f - cc.node_begin) * d;
+    if (kind == 0)
+      fnode_k<0>(P, f, r, d, phase, ufkey);
+    else
+      fnode_k<1>(P, f, r, d, phase, ufkey);
+  } else if (style == 1) {
+    const int g = cc.grp & 0xff, ln = (lane * (cc.grp >> 8)) >> 16, k = lane - ln * d;
+    const int node = j * g + ln;
+    const int f = cc.node_begin + node;
+    const bool active = ln < g && f < cc.node_end;
+    if (kind == 0)
+      fgroup<0>(P, f, cc.row_begin + node * d + k, k, d, ln * d, active, phase, ufkey);
+    else
+      fgroup<1>(P, f, cc.row_begin + node * d + k, k, d, ln * d, active, phase, ufkey);
+  } else {
+    const int p = cc.row_begin + j * 32 + lane;
+    if (p >= cc.node_end) return;
+    f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), phase, ufkey);
+  }
+}
+
+// class of chunk k: the last class whose chunk_begin <= k -- the classes'
+// chunk_begin values ascend, so the lanes that pass the test are a prefix of
+// the warp (one shared-memory compare per lane and a ballot per 32 classes)
+__device__ __forceinline__ int chunk_class(const ChunkClass *cc, int n, int k, int lane) {
+  int c = 0;
+  for (int b = 0; b < n; b += 32) {
+    const unsigned m = __ballot_sync(0xffffffffu, b + lane < n && cc[b + lane].chunk_begin <= k);
+    c += __popc(m);
+    if (m != 0xffffffffu) break;
+  }
+  return c - 1;
+}
+
 // first: iteration 1 -- afterwards the unary factors' messages are constants
 __device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool first,
                                       unsigned long long &ufkey) {
@@ -653,6 +833,8 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
 // sequence number: each phase resets the one the next phase uses (phases are
 // separated by __syncthreads; both are zeroed in the kernel prologue)
 __shared__ int s_claim[2];
+// the chunk classes of the two whole-node phases, staged from KParams at launch
+__shared__ ChunkClass s_vcc[kMaxVarClasses], s_fcc[kMaxFacClasses];
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -676,38 +858,29 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     stride = P.csize * blockDim.x;
   }
   const int n = ph.end - ph.begin;
-  unsigned long long ufkey = ~0ull;
+  unsigned long long ufkey = 0;
   if (FUSED && ph.type == 2) {  // n is a multiple of 32: whole warps
     for (int i = start; i < n; i += stride) {
       const int4 *lr = P.fitems + 2 * (size_t)(ph.begin + i);
       const int4 h = __ldg(lr), rc = __ldg(lr + 1);
       fused_lane(P, h, rc, it, pidx, ufkey);
     }
-    flush_underflow(P, it, ufkey);
+    flush_underflow(P, it, pidx, ufkey);
     return;
   }
   if (ph.list == 2) {
-    // whole light nodes [begin, end), then the slots of the heavy nodes
-    // [sbegin, send); grid-strided so a warp's 32 items are neighbouring rows
-    // (coalesced row loads, uniform degree).
-    // the heavy nodes' slot items come first (longest work first: the
-    // phase's tail is made of cheap light nodes, which balances the warps)
-    const int nn = ph.end - ph.begin;
-    const int hn = ph.send - ph.sbegin;
-    const int total = nn + hn;
-    // warp chunks of 32 consecutive items (coalesced rows, uniform degree)
+    // every node of the phase's side, in warp chunks of one chunk class each
+    // (base_params: dearest classes first, so the phase's tail is cheap
+    // chunks, which balances the warps); the unary factors' constant
+    // messages only in iteration 1
     const int lane = threadIdx.x & 31;
     const bool marg = do_marg && ph.marg;
     if (ph.type == 0 && !(marg || do_vtof)) return;
+    const int nchunks = ph.type == 0 ? P.vchunks : (it == 1 ? P.fchunks : P.fchunks_nounary);
     // Chunk map: round r (G consecutive chunks, G = the CTAs of the phase)
-    // goes to warp r % (warps per CTA) of every CTA, dealt boustrophedon --
-    // CTA b takes position b on even rounds and G-1-b on odd ones. Chunk
-    // cost grows with the row length along the degree-sorted order, so a
-    // plain deal (position b every round) hands the high CTA ids the dearer
-    // chunk of every round; per-CTA phase times then differ by up to 25 %,
-    // stably across iterations (measured at ftp: rotating the map per
-    // iteration decorrelates them -- the imbalance is data, not the SM).
-    const int nchunks = (total + 31) / 32;
+    // is dealt boustrophedon -- CTA b takes position b on even rounds and
+    // G-1-b on odd ones. Chunk cost falls along the class order, so a plain
+    // deal would hand the low CTA ids the dearer chunk of every round.
     const int G = ph.grid ? (int)gridDim.x : P.csize;
     unsigned long long *ctr = (P.trace && it == 3 && P.nphases == 2 && nchunks <= kChunkTrace)
                                   ? P.trace + (size_t)kTraceIters * 2 * gridDim.x * 2 + pidx * kChunkTrace
@@ -717,48 +890,28 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     // CTA's phase ends near its mean warp load instead of its max (measured
     // at ftp: max-warp 4.8 us against a 3.5 us mean with a static deal).
     int *claim = &s_claim[seq & 1];
-    auto run_chunks = [&](auto &&chunk) {
-      for (;;) {
-        int r = 0;
-        if (lane == 0) r = atomicAdd(claim, 1);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        if (r * G >= nchunks) break;
-        const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-        if (k >= nchunks) continue;
-        const unsigned long long t0 = ctr ? globaltimer() : 0;
-        chunk(k);
-        if (ctr) {
-          __syncwarp();
-          if (lane == 0) ctr[k] = globaltimer() - t0;
-        }
+    const bool uniform = it == 1 && pidx == 0;
+    for (;;) {
+      int r = 0;
+      if (lane == 0) r = atomicAdd(claim, 1);
+      r = __shfl_sync(0xffffffffu, r, 0);
+      if (r * G >= nchunks) break;
+      const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+      if (k >= nchunks) continue;
+      const unsigned long long t0 = ctr ? globaltimer() : 0;
+      if (ph.type == 0) {
+        const ChunkClass &cc = s_vcc[chunk_class(s_vcc, P.nvcc, k, lane)];
+        var_chunk(P, cc, k - cc.chunk_begin, lane, marg, do_vtof, it, pidx, dmax, ufkey, uniform);
+      } else {
+        const ChunkClass &cc = s_fcc[chunk_class(s_fcc, P.nfcc, k, lane)];
+        fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
       }
-    };
-    if (ph.type == 0) {
-      run_chunks([&](int c) {
-        const int i = c * 32 + lane;
-        if (i >= total) return;
-        if (i >= hn) {
-          vnode(P, ph.begin + (i - hn), marg, do_vtof, it, pidx, dmax, ufkey,
-                it == 1 && pidx == 0);
-        } else {
-          const int q = ph.sbegin + i;
-          v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), do_vtof ? -1 : 0, marg, it,
-                 pidx, dmax, ufkey, it == 1 && pidx == 0);
-        }
-      });
-    } else {
-      run_chunks([&](int c) {
-        const int i = c * 32 + lane;
-        if (i >= total) return;
-        if (i >= hn) {
-          fnode(P, ph.begin + (i - hn), pidx, it == 1, ufkey);
-        } else {
-          const int p = ph.sbegin + i;
-          f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), pidx, ufkey);
-        }
-      });
+      if (ctr) {
+        __syncwarp();
+        if (lane == 0) ctr[k] = globaltimer() - t0;
+      }
     }
-    flush_underflow(P, it, ufkey);
+    flush_underflow(P, it, pidx, ufkey);
     return;
   }
   // Slot words, twins and item lists are read-only for the whole launch
@@ -812,7 +965,7 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
       tw = twn;
     }
   }
-  flush_underflow(P, it, ufkey);
+  flush_underflow(P, it, pidx, ufkey);
 }
 
 __device__ __forceinline__ unsigned long long block_max(unsigned long long v) {
@@ -877,6 +1030,8 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
   __shared__ int s_nx[THREADS];  // look-ahead items (levelled schedules)
   for (int i = threadIdx.x; i < P.nphases && i < kPhaseCache; i += blockDim.x) s_ph[i] = P.phases[i];
   if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
+  for (int i = threadIdx.x; i < P.nvcc; i += blockDim.x) s_vcc[i] = P.vcc[i];
+  for (int i = threadIdx.x; i < P.nfcc; i += blockDim.x) s_fcc[i] = P.fcc[i];
   __syncthreads();
   auto phase_at = [&](int i) -> const Phase & { return i < kPhaseCache ? s_ph[i] : P.phases[i]; };
   const bool parall = P.nphases == 2 && s_ph[0].list == 2 && s_ph[1].list == 2;
@@ -1062,7 +1217,7 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int item = items[i];
-  unsigned long long unused = 0, ufkey = ~0ull;
+  unsigned long long unused = 0, ufkey = 0;
   if (type == 0) {
     const int q = item & (kWriteBit - 1);
     v_item(P, q, P.vslot[q], P.ftov_twin[q], (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1,
@@ -1070,7 +1225,7 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   } else {
     f_item(P, item, P.fslot[item], P.vtof_twin[item], 0, ufkey);
   }
-  flush_underflow(P, 1, ufkey);
+  flush_underflow(P, 1, 0, ufkey);
 }
 
 // ---- exact underflow attribution (engine.py:155-165, :512-518) ------------------------
@@ -1348,6 +1503,50 @@ hbp::KParams base_params(hbp_graph *g) {
   P.p0 = g->d_prev;
   P.normalize = 1;
   P.csize = 1;
+  // chunk classes of the whole-node phases (exec_phase list == 2), dearest
+  // first: huge-node slots, light nodes of degree kNodeMax..2, lane groups
+  // of degree kClassMax..kNodeMax+1, degree 1 last (for the factors: the
+  // unary ones, whose constant messages are only computed in iteration 1)
+  {
+    using hbp::ChunkClass;
+    const hbp::HostLayout &L = g->L;
+    // HBP_GROUP_MIN (A/B): the smallest degree processed as lane groups
+    const int KC = hbp::kClassMax, KN = HBP_GROUP_MIN - 1;
+    auto push = [](ChunkClass *cc, int &n, int &chunks, int d, int kind, int style, int node,
+                   int cnt, int row) {
+      if (cnt <= 0) return;
+      ChunkClass c;
+      c.chunk_begin = chunks;
+      c.node_begin = node;
+      c.node_end = style == 2 ? row + cnt : node + cnt;
+      c.row_begin = row;
+      c.info = (style == 2 ? 0 : d) | kind << 16 | style << 20;
+      const int per = style == 1 ? 32 / d : 32;
+      c.grp = style == 1 ? per | ((65536 + d - 1) / d) << 8 : 0;
+      chunks += (cnt + per - 1) / per;
+      cc[n++] = c;
+    };
+    P.nvcc = P.vchunks = 0;
+    push(P.vcc, P.nvcc, P.vchunks, 0, 0, 2, L.vcls_node[KC + 1], L.vcls_cnt[KC + 1], L.vcls_row[KC + 1]);
+    for (int d = KN; d >= 2; --d)
+      push(P.vcc, P.nvcc, P.vchunks, d, 0, 0, L.vcls_node[d], L.vcls_cnt[d], L.vcls_row[d]);
+    for (int d = KC; d > KN; --d)
+      push(P.vcc, P.nvcc, P.vchunks, d, 0, 1, L.vcls_node[d], L.vcls_cnt[d], L.vcls_row[d]);
+    push(P.vcc, P.nvcc, P.vchunks, 1, 0, 0, L.vcls_node[1], L.vcls_cnt[1], L.vcls_row[1]);
+    P.nfcc = P.fchunks = 0;
+    for (int k = 0; k < 2; ++k)
+      push(P.fcc, P.nfcc, P.fchunks, 0, k, 2, L.fcls_node[k][KC + 1], L.fcls_cnt[k][KC + 1],
+           L.fcls_row[k][KC + 1]);
+    for (int d = KN; d >= 2; --d)
+      for (int k = 0; k < 2; ++k)
+        push(P.fcc, P.nfcc, P.fchunks, d, k, 0, L.fcls_node[k][d], L.fcls_cnt[k][d], L.fcls_row[k][d]);
+    for (int d = KC; d > KN; --d)
+      for (int k = 0; k < 2; ++k)
+        push(P.fcc, P.nfcc, P.fchunks, d, k, 1, L.fcls_node[k][d], L.fcls_cnt[k][d], L.fcls_row[k][d]);
+    P.fchunks_nounary = P.fchunks;
+    for (int k = 0; k < 2; ++k)
+      push(P.fcc, P.nfcc, P.fchunks, 1, k, 0, L.fcls_node[k][1], L.fcls_cnt[k][1], L.fcls_row[k][1]);
+  }
   for (int k = 0; k <= hbp::kNodeMax + 1; ++k) {
     P.vc_node[k] = g->L.vc_node[k];
     P.vc_row[k] = g->L.vc_row[k];

@@ -51,6 +51,10 @@ struct Phase {
 #define HBP_NODE_MAX 4
 #endif
 constexpr int32_t kNodeMax = HBP_NODE_MAX;
+// Whole-node phases process nodes of degree kNodeMax < d <= kClassMax as lane
+// groups (one lane per row slot, a node's lanes in one warp) and larger ones
+// one slot per thread.
+constexpr int32_t kClassMax = 32;
 
 // List items: slot id | kWriteBit (type 0 only: also write the vtof message;
 // items without it exist only to produce a marginal).
@@ -107,7 +111,21 @@ struct HostLayout {
   int32_t vc_node[kNodeMax + 2] = {}, vc_row[kNodeMax + 2] = {};
   int32_t fa_node[kNodeMax + 2] = {}, fa_row[kNodeMax + 2] = {};  // light AND factors
   int32_t fo_node[kNodeMax + 2] = {}, fo_row[kNodeMax + 2] = {};  // light OR factors
+  // every degree class d = 1..kClassMax of the variables and of the AND / OR
+  // factors: first node, first row, node count (the nodes of a class are
+  // contiguous in internal order); index kClassMax + 1 is the "huge" rest
+  // (degree > kClassMax): first node, first row, SLOT count
+  int32_t vcls_node[kClassMax + 2] = {}, vcls_row[kClassMax + 2] = {}, vcls_cnt[kClassMax + 2] = {};
+  int32_t fcls_node[2][kClassMax + 2] = {}, fcls_row[2][kClassMax + 2] = {},
+          fcls_cnt[2][kClassMax + 2] = {};
 };
+
+// class tables from the per-class counts: vcnt[d] variables and fcnt[k][d]
+// kind-k factors of degree d (d <= kClassMax), and the slots of the huge
+// nodes (vhuge, fhuge[k]) -- the internal order is the sort order of
+// build_layout / the device layout build
+void class_tables(HostLayout &L, const int64_t *vcnt, int64_t vhuge, const int64_t (*fcnt)[kClassMax + 2],
+                  const int64_t *fhuge);
 
 hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L);
 

@@ -9,7 +9,45 @@
 
 namespace hbp {
 
-namespace {
+void class_tables(HostLayout &L, const int64_t *vcnt, int64_t vhuge, const int64_t (*fcnt)[kClassMax + 2],
+                  const int64_t *fhuge) {
+  // variables: ascending degree
+  int64_t n = 0, r = 0;
+  for (int32_t d = 1; d <= kClassMax; ++d) {
+    L.vcls_node[d] = (int32_t)n;
+    L.vcls_row[d] = (int32_t)r;
+    L.vcls_cnt[d] = (int32_t)vcnt[d];
+    n += vcnt[d];
+    r += d * vcnt[d];
+  }
+  L.vcls_node[kClassMax + 1] = (int32_t)n;
+  L.vcls_row[kClassMax + 1] = (int32_t)r;
+  L.vcls_cnt[kClassMax + 1] = (int32_t)vhuge;
+  // factors: [light AND | light OR | heavy AND | heavy OR], ascending degree
+  // inside each section, the huge ones ending the heavy sections
+  n = r = 0;
+  auto run = [&](int k, int32_t lo, int32_t hi) {
+    for (int32_t d = lo; d <= hi; ++d) {
+      L.fcls_node[k][d] = (int32_t)n;
+      L.fcls_row[k][d] = (int32_t)r;
+      L.fcls_cnt[k][d] = (int32_t)fcnt[k][d];
+      n += fcnt[k][d];
+      r += d * fcnt[k][d];
+    }
+  };
+  auto huge = [&](int k) {
+    L.fcls_node[k][kClassMax + 1] = (int32_t)n;
+    L.fcls_row[k][kClassMax + 1] = (int32_t)r;
+    L.fcls_cnt[k][kClassMax + 1] = (int32_t)fhuge[k];
+    n += fcnt[k][kClassMax + 1];
+    r += fhuge[k];
+  };
+  run(HBP_AND, 1, kNodeMax);
+  run(HBP_OR, 1, kNodeMax);
+  run(HBP_AND, kNodeMax + 1, kClassMax);
+  huge(HBP_AND);
+  run(HBP_OR, kNodeMax + 1, kClassMax);
+  huge(HBP_OR);
 }
 
 hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
@@ -165,6 +203,28 @@ hbp_status build_layout(const hbp_graph_desc &g, HostLayout &L) {
   classes(L.vrow, 0, L.v_heavy, L.vc_node, L.vc_row);
   classes(L.frow, 0, L.f_or_light, L.fa_node, L.fa_row);
   classes(L.frow, L.f_or_light, L.f_heavy, L.fo_node, L.fo_row);
+  {
+    int64_t vcnt[kClassMax + 2] = {}, fcnt[2][kClassMax + 2] = {}, vhuge = 0, fhuge[2] = {0, 0};
+    for (int32_t v = 0; v < V; ++v) {
+      const int32_t d = vdeg[v];
+      if (d > kClassMax) {
+        vcnt[kClassMax + 1]++;
+        vhuge += d;
+      } else {
+        vcnt[d]++;
+      }
+    }
+    for (int32_t f = 0; f < F; ++f) {
+      const int32_t d = (int32_t)(L.rowptr[f + 1] - L.rowptr[f]), k = L.kind[f];
+      if (d > kClassMax) {
+        fcnt[k][kClassMax + 1]++;
+        fhuge[k] += d;
+      } else {
+        fcnt[k][d]++;
+      }
+    }
+    class_tables(L, vcnt, vhuge, fcnt, fhuge);
+  }
 
   // the reference's own ftov order: variables by id, rows in canonical order
   // (a stable counting sort, storage.py:61)

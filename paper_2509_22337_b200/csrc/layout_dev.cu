@@ -41,6 +41,10 @@ struct DevInfo {
   int v_light;     // variables of degree <= kNodeMax
   int vhist[kNodeMax + 2];   // light variables per degree
   int fhist[2][kNodeMax + 2];  // light AND / OR factors per degree
+  // every class (layout.cpp class_tables): per degree up to kClassMax, the
+  // huge nodes' count at kClassMax + 1 and their slots
+  int vcls[kClassMax + 2], vhuge;
+  int fcls[2][kClassMax + 2], fhuge[2];
 };
 
 __global__ void k_iota(int *a, int64_t n) {
@@ -52,9 +56,11 @@ __global__ void k_iota(int *a, int64_t n) {
 // per factor: degree/kind checks, sort key (heavy, kind, degree) -- layout.cpp fkey
 __global__ void k_factors(const int64_t *rp, const int8_t *kind, int F, DevInfo *info,
                           unsigned *fkey) {
-  __shared__ int s_cls[4], s_unary, s_max, s_hist[2][kNodeMax + 2];
+  __shared__ int s_cls[4], s_unary, s_max, s_hist[2][kNodeMax + 2], s_all[2][kClassMax + 2], s_huge[2];
   if (threadIdx.x < 4) s_cls[threadIdx.x] = 0;
   if (threadIdx.x < 2 * (kNodeMax + 2)) (&s_hist[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x < 2 * (kClassMax + 2)) (&s_all[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x < 2) s_huge[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_unary = 0, s_max = 0;
   __syncthreads();
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
@@ -69,6 +75,12 @@ __global__ void k_factors(const int64_t *rp, const int8_t *kind, int F, DevInfo 
     fkey[f] = (unsigned)((heavy * 2 + k) << 16) | (unsigned)d;
     atomicAdd(&s_cls[heavy * 2 + k], 1);
     if (!heavy) atomicAdd(&s_hist[k][d], 1);
+    if (d > kClassMax) {
+      atomicAdd(&s_all[k][kClassMax + 1], 1);
+      atomicAdd(&s_huge[k], (int)d);
+    } else {
+      atomicAdd(&s_all[k][d], 1);
+    }
     if (d == 1) atomicAdd(&s_unary, 1);
     atomicMax(&s_max, (int)d);
   }
@@ -76,6 +88,9 @@ __global__ void k_factors(const int64_t *rp, const int8_t *kind, int F, DevInfo 
   if (threadIdx.x < 4) atomicAdd(&info->fclass[threadIdx.x], s_cls[threadIdx.x]);
   if (threadIdx.x < 2 * (kNodeMax + 2))
     atomicAdd(&(&info->fhist[0][0])[threadIdx.x], (&s_hist[0][0])[threadIdx.x]);
+  if (threadIdx.x < 2 * (kClassMax + 2))
+    atomicAdd(&(&info->fcls[0][0])[threadIdx.x], (&s_all[0][0])[threadIdx.x]);
+  if (threadIdx.x < 2) atomicAdd(&info->fhuge[threadIdx.x], s_huge[threadIdx.x]);
   if (threadIdx.x == 0) {
     atomicAdd(&info->n_unary, s_unary);
     atomicMax(&info->max_fdeg, s_max);
@@ -96,9 +111,10 @@ __global__ void k_edges(const int *evar, int64_t E, int V, DevInfo *info, int *v
 
 // per variable: no-factor check, degree maximum and light histogram
 __global__ void k_vars(const int *vdeg, int V, DevInfo *info) {
-  __shared__ int s_max, s_light, s_hist[kNodeMax + 2];
+  __shared__ int s_max, s_light, s_hist[kNodeMax + 2], s_all[kClassMax + 2], s_huge;
   if (threadIdx.x < kNodeMax + 2) s_hist[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_max = 0, s_light = 0;
+  if (threadIdx.x < kClassMax + 2) s_all[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_max = 0, s_light = 0, s_huge = 0;
   __syncthreads();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     const int d = vdeg[v];
@@ -108,9 +124,17 @@ __global__ void k_vars(const int *vdeg, int V, DevInfo *info) {
       atomicAdd(&s_light, 1);
       atomicAdd(&s_hist[d], 1);
     }
+    if (d > kClassMax) {
+      atomicAdd(&s_all[kClassMax + 1], 1);
+      atomicAdd(&s_huge, d);
+    } else {
+      atomicAdd(&s_all[d], 1);
+    }
   }
   __syncthreads();
   if (threadIdx.x < kNodeMax + 2) atomicAdd(&info->vhist[threadIdx.x], s_hist[threadIdx.x]);
+  if (threadIdx.x < kClassMax + 2) atomicAdd(&info->vcls[threadIdx.x], s_all[threadIdx.x]);
+  if (threadIdx.x == 0) atomicAdd(&info->vhuge, s_huge);
   if (threadIdx.x == 0) {
     atomicMax(&info->max_vdeg, s_max);
     atomicAdd(&info->v_light, s_light);
@@ -458,6 +482,15 @@ hbp_status build_layout_device(const hbp_graph_desc &desc, hbp_graph *g) {
   }
   L.vrow_heavy = rows[3 * K];
   L.frow_heavy = rows[3 * K + 1];
+  {
+    int64_t vcnt[kClassMax + 2], fcnt[2][kClassMax + 2], fhuge[2] = {h.fhuge[0], h.fhuge[1]};
+    for (int d = 0; d < kClassMax + 2; ++d) {
+      vcnt[d] = h.vcls[d];
+      fcnt[0][d] = h.fcls[0][d];
+      fcnt[1][d] = h.fcls[1][d];
+    }
+    class_tables(L, vcnt, h.vhuge, fcnt, fhuge);
+  }
   L.host_ready = false;
   clk.mark("tables");
   add_last_launches(17);
@@ -492,6 +525,13 @@ hbp_status ensure_host_layout(hbp_graph *g) {
     same = same && H.vc_node[d] == D.vc_node[d] && H.vc_row[d] == D.vc_row[d] &&
            H.fa_node[d] == D.fa_node[d] && H.fa_row[d] == D.fa_row[d] &&
            H.fo_node[d] == D.fo_node[d] && H.fo_row[d] == D.fo_row[d];
+  for (int d = 0; d < kClassMax + 2; ++d) {
+    same = same && H.vcls_node[d] == D.vcls_node[d] && H.vcls_row[d] == D.vcls_row[d] &&
+           H.vcls_cnt[d] == D.vcls_cnt[d];
+    for (int k = 0; k < 2; ++k)
+      same = same && H.fcls_node[k][d] == D.fcls_node[k][d] && H.fcls_row[k][d] == D.fcls_row[k][d] &&
+             H.fcls_cnt[k][d] == D.fcls_cnt[k][d];
+  }
   if (!same) {
     set_error("internal: device and host layouts disagree");
     return HBP_ECUDA;
