@@ -1382,32 +1382,9 @@ __global__ void __launch_bounds__(1024) rank_kernel(const double2 *marg, const u
     }
     return;
   }
-  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-    key[i] = key_of(i);
-    pos[i] = i;
-  }
-  __syncthreads();
-  for (int size = 2; size <= npow2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < npow2 / 2; t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long ka = key[lo], kb = key[hi];
-        const int pa = pos[lo], pb = pos[hi];
-        const bool gt = ka > kb || (ka == kb && pa > pb);
-        if (gt == up) {
-          key[lo] = kb;
-          key[hi] = ka;
-          pos[lo] = pb;
-          pos[hi] = pa;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  topk_stream(key_of, nsel, topk, npow2, key, pos);
   for (int i = threadIdx.x; i < topk; i += blockDim.x) {
-    const bool ok = i < nsel && key[i] != ~0ull;
+    const bool ok = i < nsel && i < npow2 && key[i] != ~0ull;
     ranked[i] = ok ? sel[pos[i]] : -1;
     if (p1_out) p1_out[i] = ok ? marg[sel[pos[i]]].y : 0.0;
   }
@@ -2359,10 +2336,11 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
       hbp::set_error("selection must be ascending variable ids");
       return HBP_EINVAL;
     }
+  // the shared-memory window of the streaming top-k (lbp_kernels.cuh)
   int npow2 = 2;
-  while (npow2 < num_select) npow2 <<= 1;
-  if (topk > 1 && (size_t)npow2 * 12 > 200 * 1024) {
-    hbp::set_error("device ranking supports at most 16384 selected variables");
+  while (npow2 < num_select && npow2 < hbp::dev::kRankCap) npow2 <<= 1;
+  if (topk > 1 && topk >= hbp::dev::kRankCap) {
+    hbp::set_error("device ranking returns at most 16383 alarms per call");
     return HBP_EINVAL;
   }
   HBP_CUDA(cudaSetDevice(g->device));

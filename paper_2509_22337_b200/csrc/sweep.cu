@@ -1143,41 +1143,16 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *
   unsigned long long *key = (unsigned long long *)smem;
   int *pos = (int *)(key + npow2);
   const int s = blockIdx.x;
-  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-    unsigned long long k = ~0ull;
-    if (i < nsel) {
-      int par;
-      const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
-      if ((par ? ev_alt : ev)[at] == 0) {
-        const double p1 = sub(1.0, (double)(par ? p0_alt : p0)[at]);
-        k = rank_key(p1);
-      }
-    }
-    key[i] = k;
-    pos[i] = i;
-  }
-  __syncthreads();
-  for (int size = 2; size <= npow2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < npow2 / 2; t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long ka = key[lo], kb = key[hi];
-        const int pa = pos[lo], pb = pos[hi];
-        const bool gt = ka > kb || (ka == kb && pa > pb);
-        if (gt == up) {
-          key[lo] = kb;
-          key[hi] = ka;
-          pos[lo] = pb;
-          pos[hi] = pa;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  auto key_of = [&](int i) -> unsigned long long {
+    int par;
+    const size_t at = final_pos(res_pos, s, vinv[sel[i]], V, par);
+    if ((par ? ev_alt : ev)[at] != 0) return ~0ull;
+    return rank_key(sub(1.0, (double)(par ? p0_alt : p0)[at]));
+  };
+  topk_stream(key_of, nsel, topk, npow2, key, pos);
   for (int i = threadIdx.x; i < topk; i += blockDim.x)
-    ranked[(size_t)(set_base + s) * topk + i] = (i < nsel && key[i] != ~0ull) ? sel[pos[i]] : -1;
+    ranked[(size_t)(set_base + s) * topk + i] =
+        (i < nsel && i < npow2 && key[i] != ~0ull) ? sel[pos[i]] : -1;
 }
 
 }  // namespace hbp
@@ -1468,10 +1443,11 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       hbp::set_error("selection must be ascending variable ids");
       return HBP_EINVAL;
     }
+  // the shared-memory window of the streaming top-k (lbp_kernels.cuh)
   int npow2 = 1;
-  while (npow2 < nsel) npow2 <<= 1;
-  if (out->ranked && (out->topk < 0 || (size_t)npow2 * 12 > 200 * 1024)) {
-    hbp::set_error("device ranking supports at most 16384 selected variables");
+  while (npow2 < nsel && npow2 < hbp::dev::kRankCap) npow2 <<= 1;
+  if (out->ranked && (out->topk < 0 || out->topk >= hbp::dev::kRankCap)) {
+    hbp::set_error("device ranking returns at most 16383 alarms per set");
     return HBP_EINVAL;
   }
   HBP_CUDA(cudaSetDevice(g->device));

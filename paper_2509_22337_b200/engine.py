@@ -381,11 +381,38 @@ def run(graph: FactorGraph, schedule: Schedule, options: Optional[EngineOptions]
     max |dP1| < tolerance after an iteration."""
     options = options or EngineOptions()
     options.validate()
-    if options.precision != "fp64":
-        raise ValueError("run() is fp64 only (bitwise with the reference); fp32 mode: run_many")
     _resolve_workers(workers)
+    if options.precision != "fp64":
+        return _run_fp32(graph, schedule, options)
     dg = device_graph(graph)
     return dg.plan(schedule, graph).run(options, graph)
+
+
+def _run_fp32(graph: FactorGraph, schedule: Schedule, options: EngineOptions) -> InferenceResult:
+    """The optional fp32 mode for a single graph: message
+    storage in fp32, arithmetic and marginals in fp64, through the sweep
+    kernel's fp32 instance with one (empty) evidence set. PARALL schedules
+    only -- the fp32 storage lives in the sweep kernel, which runs the
+    synchronous schedule. Marginals are within 1e-5 of the fp64 run
+    (north star), not bitwise."""
+    from .sweep import run_many
+
+    s_off, s_e, t_off, t_e = schedule.arrays(graph)
+    rp = np.asarray(graph.rowptr, dtype=np.int64)
+    nonunary = int((np.diff(rp)[np.diff(rp) > 1]).sum())
+    if len(s_off) != 2 or len(s_e) != graph.num_edges or len(t_e) != nonunary:
+        raise ValueError("fp32 mode runs PARALL schedules only (the fp32 message storage is the "
+                         "sweep kernel's)")
+    if options.record_history:
+        raise ValueError("record_history is not supported in fp32 mode")
+    r = run_many(graph, [[]], None, options,
+                 marginals=True, deltas=True)
+    if r.errors and r.errors[0] is not None:
+        raise r.errors[0]
+    return InferenceResult(marginals=r.marginals[0], converged=bool(r.converged[0]),
+                           iterations=int(r.iterations[0]), last_delta=float(r.last_delta[0]),
+                           deltas=list(r.deltas[0]), history=None, device_ms=r.kernel_ms,
+                           updates_per_iteration=int(r.updates_per_iteration[0]))
 
 
 # ---- single-pass API on a host store ------------------------------------------------------
@@ -410,20 +437,23 @@ def _store_pass(store: MessageStore, direction: int, targets: np.ndarray, normal
 
 
 def _count_vtof(store: MessageStore, idx: np.ndarray, counter: Optional[OpCounter]) -> None:
+    """The reference's count (engine.py:181-182): 2 multiplies per lane of the
+    product scan, whose lanes cover every slot of the target's row (the own
+    slot multiplies by 1.0) -- 2 x row length per target."""
     if counter is not None:
         d = store.av_end[idx] - store.av_start[idx]
-        counter.add(int((2 * np.maximum(d - 1, 0)).sum()))
+        counter.add(int((2 * d).sum()))
 
 
 def _count_ftov(store: MessageStore, idx: np.ndarray, counter: Optional[OpCounter]) -> None:
-    """Multiplies the device kernel performs per target (ft_one in engine.cu):
-    head target 2(d-1) + 3, body target 2 (blend) + 2(d-2) + 1."""
+    """The reference's count per factor-to-variable target with factor row
+    length d: body targets 4d (engine.py:224-225) + 1 (:258-259, :292-293),
+    head targets 2d (:246-247) + 3 (:277-278, :311-312)."""
     if counter is not None:
-        f = idx  # canonical
-        ft = store.vtof_to_ftov[f]
+        ft = store.vtof_to_ftov[idx]
         d = store.af_end[ft] - store.af_start[ft]
         head = store.af_head[ft]
-        n = np.where(head, 2 * (d - 1) + 3, 2 + 2 * (d - 2) + 1)
+        n = np.where(head, 2 * d + 3, 4 * d + 1)
         counter.add(int(n.sum()))
 
 

@@ -565,3 +565,49 @@ def test_level_fusion_bitwise_identical_to_two_phase(monkeypatch):
             assert got.marginals.tobytes() == ref.marginals.tobytes(), (i, mode)
             assert np.asarray(got.deltas).tobytes() == np.asarray(ref.deltas).tobytes()
     P.engine.clear_device_cache()
+
+
+def test_fp32_run_within_1e5_of_fp64():
+    """run(..., EngineOptions(precision="fp32")): fp32
+    message storage, fp64 arithmetic -- marginals within the north star's
+    1e-5 of the fp64 run; PARALL only."""
+    cases = [(W.build("C4-PARALL").graph, 1e-9), (W.build("C1").graph, 1e-9)]
+    rng = np.random.default_rng(77)
+    cases += [(random_graph(rng, max_vars=30, max_factors=30, max_body=5), 1e-9) for _ in range(10)]
+    for g, tol in cases:
+        sched = Strategy.parall().compile(g)
+        a = P.run(g, sched, EngineOptions(500, tol))
+        b = P.run(g, sched, EngineOptions(500, tol, precision="fp32"))
+        assert np.abs(a.marginals - b.marginals).max() <= 1e-5
+        # iteration counts may differ: fp32-stored messages can settle into
+        # ~1e-8 oscillations that never meet a 1e-9 tolerance
+        assert len(b.deltas) == b.iterations
+    g = W.build("C2").graph
+    with pytest.raises(ValueError):
+        P.run(g, Strategy.seqfix().compile(g), EngineOptions(50, 1e-9, precision="fp32"))
+
+
+def test_device_ranking_beyond_one_window():
+    """The device top-k streams candidates through a 16,384-entry window
+    (lbp_kernels.cuh topk_stream): a selection of every ftp variable
+    (211,175) ranks exactly like the host (-P1, id) order, ties included, for
+    the single graph and for sweep sets."""
+    g = W.build("C4-PARALL").graph
+    sched = Strategy.parall().compile(g)
+    res = P.run(g, sched, EngineOptions(1000, 1e-9))
+    sel = np.arange(g.num_variables, dtype=np.int32)
+    order = np.lexsort((sel, -res.marginals[:, 1]))
+    for k in (1, 100, 5000):
+        got, p1 = P.engine.device_graph(g).rank(sel, k)
+        assert got.tolist() == order[:k].tolist(), k
+        assert p1.tobytes() == res.marginals[order[:k], 1].tobytes()
+    _, alarms = W.graph("ftp")
+    sets = [W.evidence_set(alarms, j) for j in range(2)]
+    r = P.run_many(g, sets, None, EngineOptions(1000, 1e-9), marginals=True, deltas=False,
+                   select=sel, topk=300)
+    for j in range(2):
+        lab = set(int(v) for v in sets[j][0])
+        keep = np.array([v not in lab for v in sel])
+        o = np.lexsort((sel, -r.marginals[j][:, 1]))
+        want = [int(v) for v in o if keep[v]][:300]
+        assert r.ranked[j].tolist() == want

@@ -247,10 +247,10 @@ def test_sweep_fp32_mode_within_1e5_of_fp64(name, n):
         assert np.abs(r32.marginals[j] - o["marginals"]).max() < 1e-5
 
 
-def test_fp32_is_sweep_only():
+def test_fp32_is_parall_only():
     g, _ = W.graph("weblech")
     with pytest.raises(ValueError):
-        P.run(g, Strategy.parall().compile(g), EngineOptions(precision="fp32"))
+        P.run(g, Strategy.seqfix().compile(g), EngineOptions(precision="fp32"))
     with pytest.raises(ValueError):
         P.run_many(g, [[]], Strategy.seqfix(), EngineOptions(precision="fp32"))
 
