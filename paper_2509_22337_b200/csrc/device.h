@@ -110,6 +110,7 @@ struct hbp_plan {
   int grid = 1;
   const void *kernel = nullptr;  // executor instance (fused levels or not)
   int threads = 0;
+  int csize = 1;  // CTAs (one cluster) that run the small levels
   // the schedule as given (reference batch order), for the exact underflow
   // attribution: device [s_edges | t_edges] (stream-ordered pool) + host offsets
   int *d_sched = nullptr;

@@ -1003,6 +1003,54 @@ __device__ __forceinline__ void trace_mark(const KParams &P, int it, int p, int 
   }
 }
 
+// barrier of the CTAs that run the small levels: __syncthreads for CTA 0
+// alone, else the thread-block cluster barrier of cluster 0 (release /
+// acquire at cluster scope orders the global-memory messages too)
+__device__ __forceinline__ void cluster0_sync(int csize) {
+  if (csize > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+// A run of consecutive small fused levels [p0, p1) on the small-level CTAs:
+// a tight loop -- the level's lanes, the barrier, the next level -- instead
+// of the generic phase loop, whose per-phase prologue (descriptor copies,
+// transition logic, look-ahead) measured about 1 us per level on B200.
+// Each level prefetches the next level's lane records into L1 first.
+__device__ __forceinline__ void run_small_fused(const KParams &P, const Phase *cache, int p0,
+                                                int p1, int it) {
+  const int stride = P.csize * (int)blockDim.x;
+  const int start = (int)blockIdx.x * (int)blockDim.x + (int)threadIdx.x;
+  auto span = [&](int p, int &b, int &n) {
+    const Phase &ph = p < kPhaseCache ? cache[p] : P.phases[p];
+    b = ph.begin;
+    n = ph.end - ph.begin;
+  };
+  unsigned long long ufkey = 0;
+  int b, n;
+  span(p0, b, n);
+  for (int p = p0; p < p1; ++p) {
+    if (p > p0) cluster0_sync(P.csize);
+    int nb = 0, nn = 0;
+    if (p + 1 < p1) {
+      span(p + 1, nb, nn);
+      if (start < nn) {
+        const int4 *nx = P.fitems + 2 * (size_t)(nb + start);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
+      }
+    }
+    for (int i = start; i < n; i += stride) {
+      const int4 *lr = P.fitems + 2 * (size_t)(b + i);
+      fused_lane(P, __ldg(lr), __ldg(lr + 1), it, p, ufkey);
+    }
+    b = nb;
+    n = nn;
+  }
+  flush_underflow(P, it, p0, ufkey);
+}
+
 // marginals of the stopping iteration in the reference's variable order
 __device__ __forceinline__ void write_marginals(const KParams &P) {
   const int gs = gridDim.x * blockDim.x;
@@ -1128,12 +1176,19 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         } else if (prev_grid && !ph.grid) {
           sync_point(C, sy, G, true, in0);
         } else if (!prev_grid && !ph.grid) {
-          if (in0) __syncthreads();
+          if (in0) cluster0_sync(P.csize);
         } else {  // CTA 0 -> grid
           sync_point(C, sy, P.csize, in0, true);
         }
       }
       if (it == P.halt_it && p == P.halt_phase) return;  // attribution re-run
+      // a run of small fused levels (its first phase's sbegin = the run's end;
+      // fused plans are never halted -- their attribution replays unfused)
+      if (FUSED && ph.type == 2 && !ph.grid && ph.sbegin > p + 1) {
+        if ((int)blockIdx.x < P.csize) run_small_fused(P, s_ph, p, ph.sbegin, it);
+        p = ph.sbegin - 1;
+        continue;
+      }
       // Look-ahead for levelled schedules: the next list phase's first item
       // of this thread is copied into shared memory now (cp.async: no
       // register waits on it) and, once this phase is done, its slot word and
@@ -1700,7 +1755,28 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
   const bool fused = p->host.n_fused > 0;
   p->kernel = fused ? g->kernel_fused : g->kernel;
   p->threads = fused ? hbp::kFusedThreads : g->threads;
-  const int coop = fused ? g->coop_blocks_fused : g->coop_blocks;
+  int coop = fused ? g->coop_blocks_fused : g->coop_blocks;
+  // small levels on a thread-block cluster of csize CTAs (HBP_CSIZE, A/B)
+  p->csize = 1;
+  if (const char *ce = getenv("HBP_CSIZE")) p->csize = std::max(1, std::min(8, atoi(ce)));
+  bool has_small = false;
+  for (const auto &ph : p->host.phases) has_small |= !ph.grid;
+  if (!has_small) p->csize = 1;
+  if (p->csize > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p->csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(coop / p->csize * p->csize);
+    cfg.blockDim = dim3(p->threads);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    HBP_CUDA(cudaOccupancyMaxActiveClusters(&nclusters, p->kernel, &cfg));
+    coop = std::max(1, nclusters) * p->csize;
+  }
   // grid: enough CTAs for the largest grid-wide phase, at most one wave
   int64_t big = 0;
   for (const auto &ph : p->host.phases)
@@ -1708,9 +1784,11 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
       big = std::max<int64_t>(big, (ph.end - ph.begin) + (ph.list == 2 ? ph.send - ph.sbegin : 0));
   int64_t want = (big + p->threads - 1) / p->threads;
   if (big < 2 * p->threads) want = 1;
+  want = std::max<int64_t>(want, p->csize);
   p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, coop));
   if (const char *ge = getenv("HBP_GRID"))  // A/B: force the CTA count
     p->grid = std::max(1, std::min(atoi(ge), coop));
+  p->grid = std::max(p->csize, p->grid / p->csize * p->csize);
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();
   return HBP_OK;
@@ -1860,7 +1938,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.tol = opt->tolerance;
   P.time_limit_ns = opt->time_limit > 0 ? (long long)(opt->time_limit * 1e9) : 0;
   if (opt->time_limit > 0 && P.time_limit_ns == 0) P.time_limit_ns = 1;
-  P.csize = 1;
+  P.csize = p->csize;
   P.halt_it = 0;
   P.halt_phase = 0;
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
@@ -1918,8 +1996,25 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
 
 static hbp_status launch_kernel(hbp_plan *p, hbp::KParams &P) {
   void *args[] = {&P};
-  HBP_CUDA(cudaLaunchCooperativeKernel(p->kernel, dim3(p->grid), dim3(p->threads), args, 0,
-                                       p->g->stream));
+  if (p->csize > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = p->csize;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p->grid);
+    cfg.blockDim = dim3(p->threads);
+    cfg.stream = p->g->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    HBP_CUDA(cudaLaunchKernelExC(&cfg, p->kernel, args));
+  } else {
+    HBP_CUDA(cudaLaunchCooperativeKernel(p->kernel, dim3(p->grid), dim3(p->threads), args, 0,
+                                         p->g->stream));
+  }
   return HBP_OK;
 }
 
