@@ -87,7 +87,6 @@ struct KParams {
   int V, F, E, f_or_light, f_heavy, f_or_heavy;
   double2 *vtof, *ftov, *marg;
   double *p0;                 // [V] P(X=0) of the last marginal pass (prev P1 = 1 - p0)
-  int marg_direct;            // 1: put_marginal also writes marg[orig] (single-pass API)
   // evidence codes per internal variable (null: none): bit0 observed false,
   // bit1 observed true -- the clamp factors of clamp_evidence, multiplied in
   // after the row product (their slot is last in the row) for every marginal
@@ -172,11 +171,11 @@ __device__ __forceinline__ void sync_point(Ctrl *c, Sync &s, unsigned arrivals, 
 // re-run (attribute_underflow).
 __device__ __forceinline__ void put_message_ref(const KParams &P, double2 *dst, double &a0,
                                                 double &a1, int phase, int kind, int slot,
-                                                unsigned long long &ufkey) {
+                                                unsigned &ufkey) {
   if (P.normalize) {
     const double t = add(a0, a1);
     // bit `kind` of the phase's underflow flags (flush_underflow)
-    ufkey |= (unsigned long long)(t < kMinMessageSum) << kind;
+    ufkey |= (unsigned)(t < kMinMessageSum) << kind;
     div2_rn(a0, a1, t, a0, a1);
   }
   *dst = make_double2(a0, a1);
@@ -184,12 +183,12 @@ __device__ __forceinline__ void put_message_ref(const KParams &P, double2 *dst, 
 
 __device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
                                             int phase, int kind, int slot,
-                                            unsigned long long &ufkey) {
+                                            unsigned &ufkey) {
   put_message_ref(P, dst, a0, a1, phase, kind, slot, ufkey);
 }
 
 __device__ __forceinline__ void flush_underflow(const KParams &P, int it, int phase,
-                                                unsigned long long ufkey) {
+                                                unsigned ufkey) {
   if (ufkey) {
     atomicOr(&P.uf_msg[it], (int)ufkey);
     atomicMin(&P.uf_where[it], (unsigned long long)phase << 33 | (unsigned long long)(~ufkey & 1) << 32);
@@ -198,6 +197,9 @@ __device__ __forceinline__ void flush_underflow(const KParams &P, int it, int ph
 
 // marginal of iteration it-1 + its |dP1| (engine.py:510-523, :572); prev_p0 and
 // orig are loaded by the caller together with the row
+// DIRECT: also write marg[orig] (the single-pass API's pass_kernel; the
+// persistent kernel writes the marginals once, after the stop)
+template <bool DIRECT = false>
 __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
                                              unsigned long long &dmax, double prev_p0, int orig) {
   double t = add(q0, q1);
@@ -219,7 +221,7 @@ __device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0,
   asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
   dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
   P.p0[v] = p0;
-  if (P.marg_direct) P.marg[orig] = make_double2(p0, p1);
+  if (DIRECT) P.marg[orig] = make_double2(p0, p1);
   if (P.hist && it - 2 < P.hist_iters) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
 }
 
@@ -286,9 +288,10 @@ __device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg,
 
 // uniform: iteration 1, phase 0 -- every factor-to-variable message is still
 // the initial (1, 1), so the products are exactly 1 and nothing is loaded
+template <bool DIRECT = false>
 __device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned tw, int write,
                                        bool want_marg, int it, int phase, unsigned long long &dmax,
-                                       unsigned long long &ufkey, bool uniform = false) {
+                                       unsigned &ufkey, bool uniform = false) {
   const int d = w.y >> 16, j = w.y & 0xffff;
   const bool marg = want_marg && j == 0;
   const bool wr = write > 0 || (write < 0 && !(tw & kUnaryBit));
@@ -314,7 +317,7 @@ __device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned
   }
   if (marg) {
     if (code) apply_clamp(code, q0, q1);
-    put_marginal(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
+    put_marginal<DIRECT>(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
   }
 }
 
@@ -377,7 +380,7 @@ __device__ __forceinline__ void f_row(const KParams &P, int r, int j, double2 pp
 
 template <int KIND>
 __device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw, int phase,
-                                         unsigned long long &ufkey) {
+                                         unsigned &ufkey) {
   const int d = w.y >> 16, j = w.y & 0xffff;
   const int r = p - j;
   const double2 pp = P.fpar[w.x];
@@ -402,7 +405,7 @@ __device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw
 }
 
 __device__ __forceinline__ void f_item(const KParams &P, int p, int2 w, int tw, int phase,
-                                       unsigned long long &ufkey) {
+                                       unsigned &ufkey) {
   if (!factor_is_or(P, w.x))
     f_item_k<0>(P, p, w, tw, phase, ufkey);
   else
@@ -420,7 +423,7 @@ __device__ __forceinline__ void f_item(const KParams &P, int p, int2 w, int tw, 
 template <int D>
 __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool marg, bool vt,
                                             int it, int phase, unsigned long long &dmax,
-                                            unsigned long long &ufkey, bool uniform) {
+                                            unsigned &ufkey, bool uniform) {
   double x0[D], x1[D];
   unsigned tw[D];
   double prev_p0 = 0.0;
@@ -473,7 +476,7 @@ __device__ __forceinline__ void light_row(const int *cls_node, const int *cls_ro
 
 __device__ __forceinline__ void vnode(const KParams &P, int v, bool marg, bool vt, int it,
                                       int phase, unsigned long long &dmax,
-                                      unsigned long long &ufkey, bool uniform) {
+                                      unsigned &ufkey, bool uniform) {
   int r, d;
   light_row(P.vc_node, P.vc_row, v, r, d);
   switch (d) {
@@ -497,7 +500,7 @@ __device__ __forceinline__ void vnode(const KParams &P, int v, bool marg, bool v
 
 template <int D, int KIND>
 __device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int phase,
-                                            unsigned long long &ufkey) {
+                                            unsigned &ufkey) {
   const double2 pp = __ldg(P.fpar + f);
   double m0[D], m1[D];
   int tw[D];
@@ -546,7 +549,7 @@ __device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int 
 
 template <int KIND>
 __device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, int phase,
-                                        unsigned long long &ufkey) {
+                                        unsigned &ufkey) {
   switch (d) {
     case 1: fnode_fixed<1, KIND>(P, f, r, phase, ufkey); break;
     case 2: fnode_fixed<2, KIND>(P, f, r, phase, ufkey); break;
@@ -574,7 +577,7 @@ __device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, i
 
 __device__ __forceinline__ void vgroup(const KParams &P, int v, int q, int k, int d, int base,
                                        bool active, bool marg, bool vt, int it, int phase,
-                                       unsigned long long &dmax, unsigned long long &ufkey,
+                                       unsigned long long &dmax, unsigned &ufkey,
                                        bool uniform) {
   double2 m = make_double2(1.0, 1.0);
   unsigned tw = kUnaryBit, code = 0u;
@@ -616,7 +619,7 @@ __device__ __forceinline__ void vgroup(const KParams &P, int v, int q, int k, in
 
 template <int KIND>
 __device__ __forceinline__ void fgroup(const KParams &P, int f, int p, int k, int d, int base,
-                                       bool active, int phase, unsigned long long &ufkey) {
+                                       bool active, int phase, unsigned &ufkey) {
   double2 m = make_double2(1.0, 1.0), pp = make_double2(0.0, 0.0);
   int tw = 0;
   if (active) {
@@ -652,7 +655,7 @@ __device__ __forceinline__ void fgroup(const KParams &P, int f, int p, int k, in
 // one chunk of a whole-node phase: class cc, chunk j of the class
 __device__ __forceinline__ void var_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
                                           bool marg, bool vt, int it, int phase,
-                                          unsigned long long &dmax, unsigned long long &ufkey,
+                                          unsigned long long &dmax, unsigned &ufkey,
                                           bool uniform) {
   const int d = cc.info & 0xffff, style = cc.info >> 20;
   if (style == 0) {
@@ -680,7 +683,7 @@ __device__ __forceinline__ void var_chunk(const KParams &P, const ChunkClass &cc
 }
 
 __device__ __forceinline__ void fac_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
-                                          int phase, unsigned long long &ufkey) {
+                                          int phase, unsigned &ufkey) {
   const int d = cc.info & 0xffff, kind = (cc.info >> 16) & 0xf, style = cc.info >> 20;
   if (style == 0) {
     const int f = cc.node_begin + j * 32 + lane;
@@ -706,22 +709,9 @@ __device__ __forceinline__ void fac_chunk(const KParams &P, const ChunkClass &cc
   }
 }
 
-// class of chunk k: the last class whose chunk_begin <= k -- the classes'
-// chunk_begin values ascend, so the lanes that pass the test are a prefix of
-// the warp (one shared-memory compare per lane and a ballot per 32 classes)
-__device__ __forceinline__ int chunk_class(const ChunkClass *cc, int n, int k, int lane) {
-  int c = 0;
-  for (int b = 0; b < n; b += 32) {
-    const unsigned m = __ballot_sync(0xffffffffu, b + lane < n && cc[b + lane].chunk_begin <= k);
-    c += __popc(m);
-    if (m != 0xffffffffu) break;
-  }
-  return c - 1;
-}
-
 // first: iteration 1 -- afterwards the unary factors' messages are constants
 __device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool first,
-                                      unsigned long long &ufkey) {
+                                      unsigned &ufkey) {
   int r, d;
   if (f < P.f_or_light) {
     light_row(P.fa_node, P.fa_row, f, r, d);
@@ -754,7 +744,7 @@ constexpr int kFuseRow = 6;
 // (variable degree << 16) | own index, internal variable, ftov slot}.
 // Called by all 32 lanes of a warp.
 __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, int it, int phase,
-                                           unsigned long long &ufkey) {
+                                           unsigned &ufkey) {
   const int d = h.z & 0xff, k = (h.z >> 8) & 0xff, base = h.z >> 16;
   const int tmask = h.w & 0xfff, smask = (h.w >> 12) & 0xfff;
   const bool tgt = d && ((tmask >> k) & 1);
@@ -833,8 +823,11 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
 // sequence number: each phase resets the one the next phase uses (phases are
 // separated by __syncthreads; both are zeroed in the kernel prologue)
 __shared__ int s_claim[2];
-// the chunk classes of the two whole-node phases, staged from KParams at launch
+// the chunk classes of the two whole-node phases, staged from KParams at launch,
+// and per round of a grid-wide phase the class of the round's first chunk
 __shared__ ChunkClass s_vcc[kMaxVarClasses], s_fcc[kMaxFacClasses];
+constexpr int kRoundTab = 512;
+__shared__ unsigned char s_vround[kRoundTab], s_fround[kRoundTab];
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -858,7 +851,7 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     stride = P.csize * blockDim.x;
   }
   const int n = ph.end - ph.begin;
-  unsigned long long ufkey = 0;
+  unsigned ufkey = 0;
   if (FUSED && ph.type == 2) {  // n is a multiple of 32: whole warps
     for (int i = start; i < n; i += stride) {
       const int4 *lr = P.fitems + 2 * (size_t)(ph.begin + i);
@@ -882,34 +875,49 @@ __device__ __forceinline__ void exec_phase(const KParams &P, const Phase &ph, in
     // G-1-b on odd ones. Chunk cost falls along the class order, so a plain
     // deal would hand the low CTA ids the dearer chunk of every round.
     const int G = ph.grid ? (int)gridDim.x : P.csize;
+#ifdef HBP_TRACE_CHUNKS  // per-chunk ns of iteration 3 (tools/trace_probe.py)
     unsigned long long *ctr = (P.trace && it == 3 && P.nphases == 2 && nchunks <= kChunkTrace)
                                   ? P.trace + (size_t)kTraceIters * 2 * gridDim.x * 2 + pidx * kChunkTrace
                                   : nullptr;
+#else
+    constexpr unsigned long long *ctr = nullptr;
+#endif
     // Rounds are claimed dynamically by the CTA's warps from a shared-memory
     // counter: a warp whose chunks were cheap takes the next round, so the
     // CTA's phase ends near its mean warp load instead of its max (measured
     // at ftp: max-warp 4.8 us against a 3.5 us mean with a static deal).
     int *claim = &s_claim[seq & 1];
     const bool uniform = it == 1 && pidx == 0;
-    for (;;) {
-      int r = 0;
-      if (lane == 0) r = atomicAdd(claim, 1);
-      r = __shfl_sync(0xffffffffu, r, 0);
-      if (r * G >= nchunks) break;
+    const bool var = ph.type == 0;
+    const ChunkClass *ccs = var ? s_vcc : s_fcc;
+    const int ncc = var ? P.nvcc : P.nfcc;
+    const unsigned char *rtab = var ? s_vround : s_fround;
+    // (claiming the next round before running the current chunk measured
+    // slower: a busy warp then holds a round the others could take)
+    int r = 0;
+    if (lane == 0) r = atomicAdd(claim, 1);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    while (r * G < nchunks) {
+      int rn = 0;
       const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-      if (k >= nchunks) continue;
-      const unsigned long long t0 = ctr ? globaltimer() : 0;
-      if (ph.type == 0) {
-        const ChunkClass &cc = s_vcc[chunk_class(s_vcc, P.nvcc, k, lane)];
-        var_chunk(P, cc, k - cc.chunk_begin, lane, marg, do_vtof, it, pidx, dmax, ufkey, uniform);
-      } else {
-        const ChunkClass &cc = s_fcc[chunk_class(s_fcc, P.nfcc, k, lane)];
-        fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+      if (k < nchunks) {
+        // the chunk's class: from the round's first class (a table built at
+        // launch for grid-wide phases), walked forward
+        int c = (G == (int)gridDim.x && r < kRoundTab) ? rtab[r] : 0;
+        while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
+        const ChunkClass &cc = ccs[c];
+        const unsigned long long t0 = ctr ? globaltimer() : 0;
+        if (var)
+          var_chunk(P, cc, k - cc.chunk_begin, lane, marg, do_vtof, it, pidx, dmax, ufkey, uniform);
+        else
+          fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+        if (ctr) {
+          __syncwarp();
+          if (lane == 0) ctr[k] = globaltimer() - t0;
+        }
       }
-      if (ctr) {
-        __syncwarp();
-        if (lane == 0) ctr[k] = globaltimer() - t0;
-      }
+      if (lane == 0) rn = atomicAdd(claim, 1);
+      r = __shfl_sync(0xffffffffu, rn, 0);
     }
     flush_underflow(P, it, pidx, ufkey);
     return;
@@ -1028,7 +1036,7 @@ __device__ __forceinline__ void run_small_fused(const KParams &P, const Phase *c
     b = ph.begin;
     n = ph.end - ph.begin;
   };
-  unsigned long long ufkey = 0;
+  unsigned ufkey = 0;
   int b, n;
   span(p0, b, n);
   for (int p = p0; p < p1; ++p) {
@@ -1080,6 +1088,15 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
   if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
   for (int i = threadIdx.x; i < P.nvcc; i += blockDim.x) s_vcc[i] = P.vcc[i];
   for (int i = threadIdx.x; i < P.nfcc; i += blockDim.x) s_fcc[i] = P.fcc[i];
+  for (int r = threadIdx.x; r < kRoundTab; r += blockDim.x) {
+    const int k = r * (int)gridDim.x;
+    int c = 0;
+    while (c + 1 < P.nvcc && P.vcc[c + 1].chunk_begin <= k) ++c;
+    s_vround[r] = (unsigned char)c;
+    c = 0;
+    while (c + 1 < P.nfcc && P.fcc[c + 1].chunk_begin <= k) ++c;
+    s_fround[r] = (unsigned char)c;
+  }
   __syncthreads();
   auto phase_at = [&](int i) -> const Phase & { return i < kPhaseCache ? s_ph[i] : P.phases[i]; };
   const bool parall = P.nphases == 2 && s_ph[0].list == 2 && s_ph[1].list == 2;
@@ -1272,10 +1289,11 @@ __global__ void __launch_bounds__(256) pass_kernel(const __grid_constant__ KPara
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int item = items[i];
-  unsigned long long unused = 0, ufkey = 0;
+  unsigned long long unused = 0;
+  unsigned ufkey = 0;
   if (type == 0) {
     const int q = item & (kWriteBit - 1);
-    v_item(P, q, P.vslot[q], P.ftov_twin[q], (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1,
+    v_item<true>(P, q, P.vslot[q], P.ftov_twin[q], (item & kWriteBit) ? 1 : 0, marg != 0, marg ? 2 : 1,
            0, unused, ufkey);
   } else {
     f_item(P, item, P.fslot[item], P.vtof_twin[item], 0, ufkey);
@@ -2341,7 +2359,6 @@ hbp_status hbp_marginals(hbp_graph *g, const double *ftov0, const double *ftov1,
   P.uf_where = c.uf_where;
   P.uf_marg = c.uf_marg;
   P.uf_mwhere = c.uf_mwhere;
-  P.marg_direct = 1;
   std::vector<int32_t> rows((size_t)L.V);
   for (int32_t vi = 0; vi < L.V; ++vi) rows[vi] = L.vrow[vi];
   int *d_rows = nullptr;
