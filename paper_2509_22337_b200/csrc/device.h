@@ -43,6 +43,8 @@ struct hbp_graph {
   const void *kernel = nullptr;         // the single-graph executor
   const void *kernel_fused = nullptr;   // its instance for plans with fused levels
   int coop_blocks_fused = 0;
+  const void *kernel_parall = nullptr;  // its instance for PARALL plans (two whole-node phases)
+  int coop_blocks_parall = 0;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
   int2 *d_vslot = nullptr, *d_fslot = nullptr;

@@ -38,7 +38,18 @@ namespace hbp {
 
 using namespace dev;
 
-constexpr int kThreads = 768;  // default block size: 80 registers, fewest spills (measured best)
+// CTA sizes (one CTA per SM): levelled plans 768 threads (80 registers); the
+// two whole-node phases of a PARALL plan 640 threads (96 registers, no
+// spills) -- measured on B200 (C4-PARALL: 640 0.312 ms, 576 0.334, 704 0.320,
+// 768 0.326, 1024 0.324; levelled C3: 768 10.1 ms, 640 12.2 ms)
+#ifndef HBP_KTHREADS
+#define HBP_KTHREADS 768
+#endif
+#ifndef HBP_PARALL_THREADS
+#define HBP_PARALL_THREADS 640
+#endif
+constexpr int kThreads = HBP_KTHREADS;
+constexpr int kParallThreads = HBP_PARALL_THREADS;
 #ifndef HBP_FUSED_THREADS
 #define HBP_FUSED_THREADS 768
 #endif
@@ -1658,11 +1669,15 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   g->threads = hbp::kThreads;
   g->kernel = (const void *)hbp::lbp_persistent<hbp::kThreads, false>;
   g->kernel_fused = (const void *)hbp::lbp_persistent<hbp::kFusedThreads, true>;
+  g->kernel_parall = (const void *)hbp::lbp_persistent<hbp::kParallThreads, false>;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_fused,
                                                          hbp::kFusedThreads, 0));
   g->coop_blocks_fused = std::max(1, per_sm) * g->num_sms;
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_parall,
+                                                         hbp::kParallThreads, 0));
+  g->coop_blocks_parall = std::max(1, per_sm) * g->num_sms;
   // the layout is built on the device (layout_dev.cu); the host copy of it
   // only when a host-side consumer needs it (hbp::ensure_host_layout)
   hbp::set_last_launches(0);
@@ -1771,9 +1786,11 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
   }
   // kernel instance: plans with fused levels run the FUSED instance
   const bool fused = p->host.n_fused > 0;
-  p->kernel = fused ? g->kernel_fused : g->kernel;
-  p->threads = fused ? hbp::kFusedThreads : g->threads;
-  int coop = fused ? g->coop_blocks_fused : g->coop_blocks;
+  const auto &phs = p->host.phases;
+  const bool two_phase = phs.size() == 2 && phs[0].list == 2 && phs[1].list == 2;
+  p->kernel = fused ? g->kernel_fused : two_phase ? g->kernel_parall : g->kernel;
+  p->threads = fused ? hbp::kFusedThreads : two_phase ? hbp::kParallThreads : g->threads;
+  int coop = fused ? g->coop_blocks_fused : two_phase ? g->coop_blocks_parall : g->coop_blocks;
   // small levels on a thread-block cluster of csize CTAs (HBP_CSIZE, A/B)
   p->csize = 1;
   if (const char *ce = getenv("HBP_CSIZE")) p->csize = std::max(1, std::min(8, atoi(ce)));
