@@ -103,11 +103,6 @@ struct KParams {
   // after the row product (their slot is last in the row) for every marginal
   // and, from iteration 2 on, for every variable-to-factor message
   const unsigned char *ev;
-  // degree classes of the light nodes (rows computed, not loaded):
-  // [vc_node[d], vc_node[d+1]) are the light variables of degree d, first row vc_row[d]
-  int vc_node[kNodeMax + 2], vc_row[kNodeMax + 2];
-  int fa_node[kNodeMax + 2], fa_row[kNodeMax + 2];  // light AND factors
-  int fo_node[kNodeMax + 2], fo_row[kNodeMax + 2];  // light OR factors
   // whole-node phases: the chunk classes of each side (base_params), in
   // processing order (dearest first); a class's chunks are warp-uniform in
   // role, degree and style
@@ -476,39 +471,6 @@ __device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool
   }
 }
 
-// degree class of a light node: rows of class d are contiguous with stride d
-__device__ __forceinline__ void light_row(const int *cls_node, const int *cls_row, int n, int &r,
-                                          int &d) {
-  d = 1;
-#pragma unroll
-  for (int k = 2; k <= kNodeMax; ++k) d += n >= cls_node[k];
-  r = cls_row[d] + (n - cls_node[d]) * d;
-}
-
-__device__ __forceinline__ void vnode(const KParams &P, int v, bool marg, bool vt, int it,
-                                      int phase, unsigned long long &dmax,
-                                      unsigned &ufkey, bool uniform) {
-  int r, d;
-  light_row(P.vc_node, P.vc_row, v, r, d);
-  switch (d) {
-#define HBP_VCASE(D) \
-  case D: vnode_fixed<D>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-    HBP_VCASE(1)
-    HBP_VCASE(2)
-    HBP_VCASE(3)
-#if HBP_NODE_MAX > 4
-    HBP_VCASE(4)
-    HBP_VCASE(5)
-#endif
-#if HBP_NODE_MAX > 6
-    HBP_VCASE(6)
-    HBP_VCASE(7)
-#endif
-#undef HBP_VCASE
-    default: vnode_fixed<kNodeMax>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-  }
-}
-
 template <int D, int KIND>
 __device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int phase,
                                             unsigned &ufkey) {
@@ -674,9 +636,20 @@ __device__ __forceinline__ void var_chunk(const KParams &P, const ChunkClass &cc
     if (v >= cc.node_end) return;
     const int r = cc.row_begin + (v - cc.node_begin) * d;
     switch (d) {
-      case 1: vnode_fixed<1>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-      case 2: vnode_fixed<2>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-      case 3: vnode_fixed<3>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+#define HBP_VCASE(D) \
+  case D: vnode_fixed<D>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
+      HBP_VCASE(1)
+      HBP_VCASE(2)
+      HBP_VCASE(3)
+#if HBP_NODE_MAX > 4
+      HBP_VCASE(4)
+      HBP_VCASE(5)
+#endif
+#if HBP_NODE_MAX > 6
+      HBP_VCASE(6)
+      HBP_VCASE(7)
+#endif
+#undef HBP_VCASE
       default: vnode_fixed<kNodeMax>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
     }
   } else if (style == 1) {
@@ -720,18 +693,6 @@ __device__ __forceinline__ void fac_chunk(const KParams &P, const ChunkClass &cc
   }
 }
 
-// first: iteration 1 -- afterwards the unary factors' messages are constants
-__device__ __forceinline__ void fnode(const KParams &P, int f, int phase, bool first,
-                                      unsigned &ufkey) {
-  int r, d;
-  if (f < P.f_or_light) {
-    light_row(P.fa_node, P.fa_row, f, r, d);
-    if (d > 1 || first) fnode_k<0>(P, f, r, d, phase, ufkey);
-  } else {
-    light_row(P.fo_node, P.fo_row, f, r, d);
-    if (d > 1 || first) fnode_k<1>(P, f, r, d, phase, ufkey);
-  }
-}
 
 
 // --------------------------------------------------------------------------------------
@@ -1607,14 +1568,6 @@ hbp::KParams base_params(hbp_graph *g) {
     P.fchunks_nounary = P.fchunks;
     for (int k = 0; k < 2; ++k)
       push(P.fcc, P.nfcc, P.fchunks, 1, k, 0, L.fcls_node[k][1], L.fcls_cnt[k][1], L.fcls_row[k][1]);
-  }
-  for (int k = 0; k <= hbp::kNodeMax + 1; ++k) {
-    P.vc_node[k] = g->L.vc_node[k];
-    P.vc_row[k] = g->L.vc_row[k];
-    P.fa_node[k] = g->L.fa_node[k];
-    P.fa_row[k] = g->L.fa_row[k];
-    P.fo_node[k] = g->L.fo_node[k];
-    P.fo_row[k] = g->L.fo_row[k];
   }
   return P;
 }

@@ -59,6 +59,11 @@ m0 = d0.mean(0)
 order = np.argsort(-m0)
 print("slowest CTAs (cta, sm, mean us):", [(int(c), int(smid[c]), round(float(m0[c]), 2)) for c in order[:10]])
 print("fastest CTAs:", [(int(c), int(smid[c]), round(float(m0[c]), 2)) for c in order[-5:]])
+if d1 is not None:
+    m1 = d1.mean(0)
+    o1 = np.argsort(-m1)
+    print("phase-1 slowest CTAs (cta, sm, mean us):", [(int(c), int(smid[c]), round(float(m1[c]), 2)) for c in o1[:8]])
+    print("phase-1 median %.2f us" % np.median(m1))
 # by SM parity / half (die guess)
 for name_, mask in [("sm < 74", smid < 74), ("sm >= 74", smid >= 74), ("even sm", smid % 2 == 0), ("odd sm", smid % 2 == 1)]:
     print(f"  {name_}: mean ph0 {m0[mask].mean():.2f} us" + (f", ph1 {d1.mean(0)[mask].mean():.2f} us" if d1 is not None else ""))
