@@ -795,6 +795,10 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
 // sequence number: each phase resets the one the next phase uses (phases are
 // separated by __syncthreads; both are zeroed in the kernel prologue)
 __shared__ int s_claim[2];
+__shared__ unsigned long long s_dmax;  // lbp_parall: the CTA's |dP1| max of the iteration
+struct NoHookP {
+  __device__ void operator()() const {}
+};
 // the chunk classes of the two whole-node phases, staged from KParams at launch,
 // and per round of a grid-wide phase the class of the round's first chunk
 __shared__ ChunkClass s_vcc[kMaxVarClasses], s_fcc[kMaxFacClasses];
@@ -1247,6 +1251,183 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
   }
 }
 
+// ======================================================================================
+// PARALL plans (one batch: engine.py:566-570 as two whole-graph phases) run a
+// kernel of their own -- the same chunk work as lbp_persistent's whole-node
+// phases, without the level machinery -- so its tuning cannot disturb the
+// levelled instances' register allocation. The |dP1| reduction and the stop
+// decision ride on the two grid barriers of an iteration.
+
+// thread 0's hooks run inside the barrier: pre before its arrival (after the
+// CTA's __syncthreads), post after its wait (before the closing one)
+template <typename Pre, typename Post>
+__device__ __forceinline__ void sync_point_hooked(Ctrl *c, Sync &s, unsigned arrivals, bool arrive,
+                                                  bool wait, Pre pre, Post post) {
+  __syncthreads();
+  s.target += arrivals;
+  if (threadIdx.x == 0) {
+    pre();
+    if (arrive) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&c->bar) : "memory");
+    if (wait)
+      while (ld_acquire(&c->bar) < s.target) {
+      }
+    post();
+  }
+  __syncthreads();
+}
+
+// every node of one side in class-uniform warp chunks (the same loop as
+// exec_phase's list == 2 branch)
+__device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, int seq, int it,
+                                           int pidx, bool marg, bool vt,
+                                           unsigned long long &dmax, unsigned &ufkey) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_claim[(seq + 1) & 1] = 0;
+  if (var && !(marg || vt)) return;
+  if ((int)blockIdx.x >= G) return;
+  const int nchunks = var ? P.vchunks : (it == 1 ? P.fchunks : P.fchunks_nounary);
+  int *claim = &s_claim[seq & 1];
+  const ChunkClass *ccs = var ? s_vcc : s_fcc;
+  const int ncc = var ? P.nvcc : P.nfcc;
+  const unsigned char *rtab = var ? s_vround : s_fround;
+  int r = 0;
+  if (lane == 0) r = atomicAdd(claim, 1);
+  r = __shfl_sync(0xffffffffu, r, 0);
+  while (r * G < nchunks) {
+    int rn = 0;
+    const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    if (k < nchunks) {
+      int c = (G == (int)gridDim.x && r < kRoundTab) ? rtab[r] : 0;
+      while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
+      const ChunkClass &cc = ccs[c];
+      if (var)
+        var_chunk(P, cc, k - cc.chunk_begin, lane, marg, vt, it, pidx, dmax, ufkey, false);
+      else
+        fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+    }
+    if (lane == 0) rn = atomicAdd(claim, 1);
+    r = __shfl_sync(0xffffffffu, rn, 0);
+  }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__ KParams P) {
+  Ctrl *C = P.ctrl;
+  const bool multi = gridDim.x > 1;
+  const unsigned G = gridDim.x;
+  Sync sy;
+  if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_dmax = 0;
+  for (int i = threadIdx.x; i < P.nvcc; i += blockDim.x) s_vcc[i] = P.vcc[i];
+  for (int i = threadIdx.x; i < P.nfcc; i += blockDim.x) s_fcc[i] = P.fcc[i];
+  for (int r = threadIdx.x; r < kRoundTab; r += blockDim.x) {
+    const int k = r * (int)gridDim.x;
+    int c = 0;
+    while (c + 1 < P.nvcc && P.vcc[c + 1].chunk_begin <= k) ++c;
+    s_vround[r] = (unsigned char)c;
+    c = 0;
+    while (c + 1 < P.nfcc && P.fcc[c + 1].chunk_begin <= k) ++c;
+    s_fround[r] = (unsigned char)c;
+  }
+  // the factor side may be a small phase (CTAs [0, csize)) on small graphs
+  const int fG = P.phases[1].grid ? (int)gridDim.x : P.csize;
+  auto barrier = [&](unsigned arrivals, bool arrive, auto pre, auto post) {
+    if (multi) {
+      sync_point_hooked(C, sy, arrivals, arrive, true, pre, post);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pre();
+        post();
+      }
+      __syncthreads();
+    }
+  };
+  const NoHookP nohook;
+  // uniform start: iteration 1's variable side would only write the
+  // normalised (1, 1) into every vtof slot, so the start writes it directly
+  {
+    const int gs = gridDim.x * blockDim.x;
+    const double cst = P.normalize ? 0.5 : 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.E; i += gs) P.vtof[i] = make_double2(cst, cst);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.p0[i] = 0.5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
+    barrier(G, true, nohook, nohook);
+  }
+  __shared__ int s_stop;
+  for (int it = 1;; ++it) {
+    const bool final_pass = it == P.max_it + 1;
+    const int done = it - 1;
+    if (it == P.halt_it && P.halt_phase == 0) return;  // attribution re-run
+    if (it > 1) {
+      unsigned long long dmax = 0;
+      unsigned ufkey = 0;
+      trace_mark(P, it, 0, 0);
+      node_phase(P, true, (int)gridDim.x, it * 2, it, 0, true, !final_pass, dmax, ufkey);
+      flush_underflow(P, it, 0, ufkey);
+      trace_mark(P, it, 0, 1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, dmax, o);
+        dmax = w > dmax ? w : dmax;
+      }
+      if ((threadIdx.x & 31) == 0 && dmax) atomicMax(&s_dmax, dmax);
+      auto publish = [&]() {
+        if (s_dmax) atomicMax(&P.delta_bits[it - 1], s_dmax);
+        s_dmax = 0;
+        if (blockIdx.x == 0 && P.time_limit_ns > 0)
+          P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
+      };
+      barrier(G, true, publish, nohook);
+    }
+    // stop decision for iteration it-1, taken at the end of this iteration
+    // (its loads overlap the factor side; a stop only wastes that phase,
+    // whose output is never observed) -- or right away in the final pass
+    int ufm = 0, ufg = 0, tf = 0;
+    unsigned long long db = 0;
+    if (it > 1 && threadIdx.x == 0) {
+      ufm = ((const volatile int *)P.uf_msg)[done];
+      ufg = ((const volatile int *)P.uf_marg)[done];
+      tf = ((const volatile int *)P.tflag)[done];
+      db = ((const volatile unsigned long long *)P.delta_bits)[done];
+    }
+    auto decide = [&]() -> int {
+      if (ufm || ufg == 1) return 4;  // ufg bit1 (a NaN total) suppresses the raise
+      if (__longlong_as_double((long long)db) < P.tol) return 1;
+      if (done == P.max_it) return 2;
+      if (tf) return 3;
+      return 0;
+    };
+    auto decide_hook = [&]() { s_stop = it > 1 ? decide() : 0; };
+    if (final_pass) {
+      if (threadIdx.x == 0) decide_hook();
+      __syncthreads();
+    } else {
+      if (it == P.halt_it && P.halt_phase == 1) return;  // attribution re-run
+      unsigned long long unused = 0;
+      unsigned ufkey = 0;
+      trace_mark(P, it, 1, 0);
+      node_phase(P, false, fG, it * 2 + 1, it, 1, false, true, unused, ufkey);
+      flush_underflow(P, it, 1, ufkey);
+      trace_mark(P, it, 1, 1);
+      if (fG == (int)gridDim.x)
+        barrier(G, true, nohook, decide_hook);
+      else
+        barrier(P.csize, (int)blockIdx.x < P.csize, nohook, decide_hook);
+    }
+    if (it > 1 && s_stop) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        C->iterations = done;
+        C->last_delta = db;
+        C->converged = s_stop == 1;
+        C->stop = s_stop;
+      }
+      write_marginals(P);
+      return;
+    }
+  }
+}
+
 }  // namespace hbp
 
 // ======================================================================================
@@ -1622,7 +1803,7 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   g->threads = hbp::kThreads;
   g->kernel = (const void *)hbp::lbp_persistent<hbp::kThreads, false>;
   g->kernel_fused = (const void *)hbp::lbp_persistent<hbp::kFusedThreads, true>;
-  g->kernel_parall = (const void *)hbp::lbp_persistent<hbp::kParallThreads, false>;
+  g->kernel_parall = (const void *)hbp::lbp_parall<hbp::kParallThreads>;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_fused,
