@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhbp.so")
 
 SOURCES = ["engine.cu", "sweep.cu", "layout_dev.cu", "layout.cpp", "compiler.cpp", "capi.cpp"]
-HEADERS = ["internal.h", "device.h", "lbp_kernels.cuh", os.path.join("..", "..", "include", "hornbp_gpu.h")]
+HEADERS = ["internal.h", "device.h", "lbp_kernels.cuh", "lbp_node.inc", os.path.join("..", "..", "include", "hornbp_gpu.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -44,6 +44,7 @@ struct hbp_graph {
   const void *kernel_fused = nullptr;   // its instance for plans with fused levels
   int coop_blocks_fused = 0;
   const void *kernel_parall = nullptr;  // its instance for PARALL plans (two whole-node phases)
+  const void *kernel_parall_nonorm = nullptr;  // the same without message normalisation
   int coop_blocks_parall = 0;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
@@ -111,6 +112,7 @@ struct hbp_plan {
   hbp_plan *unfused = nullptr;  // the same schedule without fused levels (underflow attribution)
   int grid = 1;
   const void *kernel = nullptr;  // executor instance (fused levels or not)
+  const void *kernel_nonorm = nullptr;  // the instance for normalize_messages off
   int threads = 0;
   int csize = 1;  // CTAs (one cluster) that run the small levels
   // the schedule as given (reference batch order), for the exact underflow

@@ -167,531 +167,15 @@ __device__ __forceinline__ void sync_point(Ctrl *c, Sync &s, unsigned arrivals, 
   __syncthreads();
 }
 
-// --------------------------------------------------------------------------------------
-// message output with normalisation + underflow flag (engine.py:155-165)
-
-// Underflow is recorded in per-thread flag bits (bit 0 a vtof, bit 1 an ftov
-// message) and published once per phase by flush_underflow -- uf_msg gets the
-// bits, uf_where the earliest failing phase (<< 33) -- so the common path
-// issues no atomics; the failing message itself is named by the attribution
-// re-run (attribute_underflow).
-__device__ __forceinline__ void put_message_ref(const KParams &P, double2 *dst, double &a0,
-                                                double &a1, int phase, int kind, int slot,
-                                                unsigned &ufkey) {
-  if (P.normalize) {
-    const double t = add(a0, a1);
-    // bit `kind` of the phase's underflow flags (flush_underflow)
-    ufkey |= (unsigned)(t < kMinMessageSum) << kind;
-    div2_rn(a0, a1, t, a0, a1);
-  }
-  *dst = make_double2(a0, a1);
-}
-
-__device__ __forceinline__ void put_message(const KParams &P, double2 *dst, double a0, double a1,
-                                            int phase, int kind, int slot,
-                                            unsigned &ufkey) {
-  put_message_ref(P, dst, a0, a1, phase, kind, slot, ufkey);
-}
-
-__device__ __forceinline__ void flush_underflow(const KParams &P, int it, int phase,
-                                                unsigned ufkey) {
-  if (ufkey) {
-    atomicOr(&P.uf_msg[it], (int)ufkey);
-    atomicMin(&P.uf_where[it], (unsigned long long)phase << 33 | (unsigned long long)(~ufkey & 1) << 32);
-  }
-}
-
-// marginal of iteration it-1 + its |dP1| (engine.py:510-523, :572); prev_p0 and
-// orig are loaded by the caller together with the row
-// DIRECT: also write marg[orig] (the single-pass API's pass_kernel; the
-// persistent kernel writes the marginals once, after the stop)
-template <bool DIRECT = false>
-__device__ __forceinline__ void put_marginal(const KParams &P, int v, double q0, double q1, int it,
-                                             unsigned long long &dmax, double prev_p0, int orig) {
-  double t = add(q0, q1);
-  // the reference raises iff min(total) < 1e-300 (engine.py:512-518); numpy's
-  // min propagates NaN, so one NaN total anywhere in the pass suppresses the
-  // raise: bit0 = some total below the bound, bit1 = some total NaN
-  if (__builtin_expect(!(t >= kMinMessageSum), 0)) {
-    atomicOr(&P.uf_marg[it - 1], t != t ? 2 : 1);
-    if (t == t) atomicMin(&P.uf_mwhere[it - 1], orig);
-  }
-  const double p0 = div_rn(q0, t);
-  const double p1 = sub(1.0, p0);
-  // |P1 - prev| as np.abs does it: clear the sign bit, keep any NaN payload
-  // (integer AND in PTX: the compiler would otherwise turn it into an FP abs,
-  // which canonicalises NaN payloads differently from numpy)
-  const unsigned long long raw =
-      (unsigned long long)__double_as_longlong(sub(p1, sub(1.0, prev_p0)));
-  unsigned long long bits;
-  asm("and.b64 %0, %1, 0x7fffffffffffffff;" : "=l"(bits) : "l"(raw));
-  dmax = bits > dmax ? bits : dmax;  // NaN bits sort above every finite value
-  P.p0[v] = p0;
-  if (DIRECT) P.marg[orig] = make_double2(p0, p1);
-  if (P.hist && it - 2 < P.hist_iters) P.hist[(size_t)(it - 2) * P.V + orig] = make_double2(p0, p1);
-}
-
-// the clamp factors' messages (1,0) / (0,1), exact multiplications by 0 and 1
-__device__ __forceinline__ void apply_clamp(unsigned code, double &a0, double &a1) {
-  if (code & 1u) {
-    a0 = mul(a0, 1.0);
-    a1 = mul(a1, 0.0);
-  }
-  if (code & 2u) {
-    a0 = mul(a0, 0.0);
-    a1 = mul(a1, 1.0);
-  }
-}
-
-// --------------------------------------------------------------------------------------
-// variable side, one ftov slot q: the vtof message of the same edge (product of
-// the row without q, engine.py:186-195) and, at a row start, the marginal
-// (full row product). write: 1 = yes, 0 = no, -1 = unless the edge's factor
-// is unary (PARALL range mode).
-
-// rows longer than 8 (rare): same left-to-right products, loads in groups of 4
-__device__ __forceinline__ void v_row_long(const KParams &P, int r, int d, int j, bool marg,
-                                        double &a0, double &a1, double &q0, double &q1) {
-  for (int base = 0; base < d; base += 4) {
-    double2 m[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) m[k] = base + k < d ? P.ftov[r + base + k] : make_double2(1.0, 1.0);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (base + k < d) {
-        if (base + k != j) {
-          a0 = mul(a0, m[k].x);
-          a1 = mul(a1, m[k].y);
-        }
-        if (marg) {
-          q0 = mul(q0, m[k].x);
-          q1 = mul(q1, m[k].y);
-        }
-      }
-    }
-  }
-}
-
-// fixed-length row: loads issued together, left-to-right products
-template <int D>
-__device__ __forceinline__ void v_row(const KParams &P, int r, int j, bool marg, double &a0,
-                                      double &a1, double &q0, double &q1) {
-  double2 m[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) m[k] = P.ftov[r + k];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    if (k != j) {  // excluded slot: the reference multiplies by 1.0
-      a0 = mul(a0, m[k].x);
-      a1 = mul(a1, m[k].y);
-    }
-    if (marg) {
-      q0 = mul(q0, m[k].x);
-      q1 = mul(q1, m[k].y);
-    }
-  }
-}
-
-// uniform: iteration 1, phase 0 -- every factor-to-variable message is still
-// the initial (1, 1), so the products are exactly 1 and nothing is loaded
-template <bool DIRECT = false>
-__device__ __forceinline__ void v_item(const KParams &P, int q, int2 w, unsigned tw, int write,
-                                       bool want_marg, int it, int phase, unsigned long long &dmax,
-                                       unsigned &ufkey, bool uniform = false) {
-  const int d = w.y >> 16, j = w.y & 0xffff;
-  const bool marg = want_marg && j == 0;
-  const bool wr = write > 0 || (write < 0 && !(tw & kUnaryBit));
-  if (!wr && !marg) return;
-  const int r = q - j;
-  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
-  if (!uniform) switch (d) {
-    case 1: v_row<1>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 2: v_row<2>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 3: v_row<3>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 4: v_row<4>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 5: v_row<5>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 6: v_row<6>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 7: v_row<7>(P, r, j, marg, a0, a1, q0, q1); break;
-    case 8: v_row<8>(P, r, j, marg, a0, a1, q0, q1); break;
-    default: v_row_long(P, r, d, j, marg, a0, a1, q0, q1); break;
-  }
-  const unsigned code = P.ev ? P.ev[w.x] : 0u;
-  if (wr) {
-    const int out = (int)(tw & ~kUnaryBit);
-    if (code && it > 1) apply_clamp(code, a0, a1);
-    put_message(P, P.vtof + out, a0, a1, phase, 0, out, ufkey);
-  }
-  if (marg) {
-    if (code) apply_clamp(code, q0, q1);
-    put_marginal<DIRECT>(P, w.x, q0, q1, it, dmax, P.p0[w.x], __ldg(P.vorig + w.x));
-  }
-}
-
-// --------------------------------------------------------------------------------------
-// factor side, one vtof slot p: the ftov message of the same edge.
-// Head target (index 0): products over body slots of (m0 + m1) and of
-// m1 (AND) / m0 (OR) -- engine.py:229-248. Body target: the head slot
-// contributes blend = (1-c) m0 + c m1 and (m0 - m1) -- engine.py:198-226.
-
-__device__ __forceinline__ bool factor_is_or(const KParams &P, int f) {
-  return (f >= P.f_or_light && f < P.f_heavy) || f >= P.f_or_heavy;
-}
-
-template <int KIND>
-__device__ __forceinline__ void f_row_long(const KParams &P, int r, int d, int j, double2 pp,
-                                        double &b1, double &b2) {
-  for (int base = 0; base < d; base += 4) {
-    double2 m[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) m[k] = base + k < d ? P.vtof[r + base + k] : make_double2(1.0, 1.0);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = base + k;
-      if (i < d && i != j) {
-        double f1, f2;
-        if (i == 0) {
-          head_slot_terms<KIND>(pp.x, pp.y, m[k].x, m[k].y, f1, f2);
-        } else {
-          f1 = add(m[k].x, m[k].y);
-          f2 = KIND == 0 ? m[k].y : m[k].x;
-        }
-        b1 = mul(b1, f1);
-        b2 = mul(b2, f2);
-      }
-    }
-  }
-}
-
-template <int D, int KIND>
-__device__ __forceinline__ void f_row(const KParams &P, int r, int j, double2 pp, double &b1,
-                                      double &b2) {
-  double2 m[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) m[k] = P.vtof[r + k];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    if (k != j) {
-      double f1, f2;
-      if (k == 0) {
-        head_slot_terms<KIND>(pp.x, pp.y, m[k].x, m[k].y, f1, f2);
-      } else {
-        f1 = add(m[k].x, m[k].y);
-        f2 = KIND == 0 ? m[k].y : m[k].x;
-      }
-      b1 = mul(b1, f1);
-      b2 = mul(b2, f2);
-    }
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void f_item_k(const KParams &P, int p, int2 w, int tw, int phase,
-                                         unsigned &ufkey) {
-  const int d = w.y >> 16, j = w.y & 0xffff;
-  const int r = p - j;
-  const double2 pp = P.fpar[w.x];
-  double b1 = 1.0, b2 = 1.0;
-  switch (d) {
-    case 1: break;  // prior / evidence: empty products
-    case 2: f_row<2, KIND>(P, r, j, pp, b1, b2); break;
-    case 3: f_row<3, KIND>(P, r, j, pp, b1, b2); break;
-    case 4: f_row<4, KIND>(P, r, j, pp, b1, b2); break;
-    case 5: f_row<5, KIND>(P, r, j, pp, b1, b2); break;
-    case 6: f_row<6, KIND>(P, r, j, pp, b1, b2); break;
-    case 7: f_row<7, KIND>(P, r, j, pp, b1, b2); break;
-    case 8: f_row<8, KIND>(P, r, j, pp, b1, b2); break;
-    default: f_row_long<KIND>(P, r, d, j, pp, b1, b2); break;
-  }
-  double o0, o1;
-  if (j == 0)
-    head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-  else
-    body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-  put_message(P, P.ftov + tw, o0, o1, phase, 1, tw, ufkey);
-}
-
-__device__ __forceinline__ void f_item(const KParams &P, int p, int2 w, int tw, int phase,
-                                       unsigned &ufkey) {
-  if (!factor_is_or(P, w.x))
-    f_item_k<0>(P, p, w, tw, phase, ufkey);
-  else
-    f_item_k<1>(P, p, w, tw, phase, ufkey);
-}
-
-
-// --------------------------------------------------------------------------------------
-// node-centric items (PARALL range phases): one thread owns a whole variable or
-// factor, reads its row once into registers and emits every outgoing message.
-// The exclusion index is a compile-time constant of the unrolled loops, and
-// the left-to-right prefix products are shared across targets -- exact,
-// because they ARE the reference's partial products (engine.py:173-180).
-
-template <int D>
-__device__ __forceinline__ void vnode_fixed(const KParams &P, int v, int r, bool marg, bool vt,
-                                            int it, int phase, unsigned long long &dmax,
-                                            unsigned &ufkey, bool uniform) {
-  double x0[D], x1[D];
-  unsigned tw[D];
-  double prev_p0 = 0.0;
-  int orig = 0;
-  if (marg) {  // issued with the row loads: one memory round trip per node
-    prev_p0 = P.p0[v];
-    orig = __ldg(P.vorig + v);
-  }
-  const unsigned code = P.ev ? P.ev[v] : 0u;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double2 m = uniform ? make_double2(1.0, 1.0) : P.ftov[r + k];
-    x0[k] = m.x;
-    x1[k] = m.y;
-  }
-  if (vt) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) tw[k] = __ldg(P.ftov_twin + r + k);
-  }
-  double a0 = 1.0, a1 = 1.0;  // prefix x[0] * ... * x[j-1]
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    if (vt && !(tw[j] & kUnaryBit)) {
-      double b0 = a0, b1 = a1;
-#pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b0 = mul(b0, x0[k]);
-        b1 = mul(b1, x1[k]);
-      }
-      if (code && it > 1) apply_clamp(code, b0, b1);
-      put_message(P, P.vtof + tw[j], b0, b1, phase, 0, (int)tw[j], ufkey);
-    }
-    a0 = mul(a0, x0[j]);
-    a1 = mul(a1, x1[j]);
-  }
-  if (marg) {
-    if (code) apply_clamp(code, a0, a1);
-    put_marginal(P, v, a0, a1, it, dmax, prev_p0, orig);
-  }
-}
-
-template <int D, int KIND>
-__device__ __forceinline__ void fnode_fixed(const KParams &P, int f, int r, int phase,
-                                            unsigned &ufkey) {
-  const double2 pp = __ldg(P.fpar + f);
-  double m0[D], m1[D];
-  int tw[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double2 m = P.vtof[r + k];
-    m0[k] = m.x;
-    m1[k] = m.y;
-    tw[k] = __ldg(P.vtof_twin + r + k);
-  }
-  double s[D];
-#pragma unroll
-  for (int k = 1; k < D; ++k) s[k] = add(m0[k], m1[k]);
-  {  // head target: products over the body slots
-    double h1 = 1.0, h2 = 1.0;
-#pragma unroll
-    for (int k = 1; k < D; ++k) {
-      h1 = mul(h1, s[k]);
-      h2 = mul(h2, KIND == 0 ? m1[k] : m0[k]);
-    }
-    double o0, o1;
-    head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    put_message(P, P.ftov + tw[0], o0, o1, phase, 1, tw[0], ufkey);
-  }
-  if (D > 1) {  // body targets: the head slot contributes blend / (m0 - m1)
-    double a1, a2;
-    head_slot_terms<KIND>(pp.x, pp.y, m0[0], m1[0], a1, a2);
-#pragma unroll
-    for (int j = 1; j < D; ++j) {
-      double b1 = a1, b2 = a2;
-#pragma unroll
-      for (int k = j + 1; k < D; ++k) {
-        b1 = mul(b1, s[k]);
-        b2 = mul(b2, KIND == 0 ? m1[k] : m0[k]);
-      }
-      double o0, o1;
-      body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-      put_message(P, P.ftov + tw[j], o0, o1, phase, 1, tw[j], ufkey);
-      a1 = mul(a1, s[j]);
-      a2 = mul(a2, KIND == 0 ? m1[j] : m0[j]);
-    }
-  }
-}
-
-
-
-template <int KIND>
-__device__ __forceinline__ void fnode_k(const KParams &P, int f, int r, int d, int phase,
-                                        unsigned &ufkey) {
-  switch (d) {
-    case 1: fnode_fixed<1, KIND>(P, f, r, phase, ufkey); break;
-    case 2: fnode_fixed<2, KIND>(P, f, r, phase, ufkey); break;
-    case 3: fnode_fixed<3, KIND>(P, f, r, phase, ufkey); break;
-#if HBP_NODE_MAX > 4
-    case 4: fnode_fixed<4, KIND>(P, f, r, phase, ufkey); break;
-    case 5: fnode_fixed<5, KIND>(P, f, r, phase, ufkey); break;
-#endif
-#if HBP_NODE_MAX > 6
-    case 6: fnode_fixed<6, KIND>(P, f, r, phase, ufkey); break;
-    case 7: fnode_fixed<7, KIND>(P, f, r, phase, ufkey); break;
-#endif
-    default: fnode_fixed<kNodeMax, KIND>(P, f, r, phase, ufkey); break;
-  }
-}
-
-// --------------------------------------------------------------------------------------
-// lane groups (whole-node phases, kNodeMax < degree <= kClassMax): lane k of a
-// group owns row slot k of its node and loads that one message (a warp's loads
-// are one contiguous run of rows); the node's row reaches every lane of the
-// group by warp shuffles, and each lane forms its own slot's outgoing message
-// left to right over the row without its slot (engine.py:173-180) -- the
-// reference's order, so the same bits as the per-node kernels. d is
-// warp-uniform (one class per chunk); every lane of the warp calls these.
-
-__device__ __forceinline__ void vgroup(const KParams &P, int v, int q, int k, int d, int base,
-                                       bool active, bool marg, bool vt, int it, int phase,
-                                       unsigned long long &dmax, unsigned &ufkey,
-                                       bool uniform) {
-  double2 m = make_double2(1.0, 1.0);
-  unsigned tw = kUnaryBit, code = 0u;
-  double prev_p0 = 0.0;
-  int orig = 0;
-  const bool mk = marg && k == 0;
-  if (active) {
-    if (!uniform) m = P.ftov[q];
-    tw = __ldg(P.ftov_twin + q);
-    code = P.ev ? P.ev[v] : 0u;
-    if (mk) {
-      prev_p0 = P.p0[v];
-      orig = __ldg(P.vorig + v);
-    }
-  }
-  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
-  for (int i = 0; i < d; ++i) {
-    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
-    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
-    if (i != k) {
-      a0 = mul(a0, x0);
-      a1 = mul(a1, x1);
-    }
-    if (mk) {
-      q0 = mul(q0, x0);
-      q1 = mul(q1, x1);
-    }
-  }
-  if (!active) return;
-  if (vt && !(tw & kUnaryBit)) {
-    if (code && it > 1) apply_clamp(code, a0, a1);
-    put_message(P, P.vtof + tw, a0, a1, phase, 0, (int)tw, ufkey);
-  }
-  if (mk) {
-    if (code) apply_clamp(code, q0, q1);
-    put_marginal(P, v, q0, q1, it, dmax, prev_p0, orig);
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void fgroup(const KParams &P, int f, int p, int k, int d, int base,
-                                       bool active, int phase, unsigned &ufkey) {
-  double2 m = make_double2(1.0, 1.0), pp = make_double2(0.0, 0.0);
-  int tw = 0;
-  if (active) {
-    m = P.vtof[p];
-    tw = __ldg(P.vtof_twin + p);
-    pp = __ldg(P.fpar + f);
-  }
-  double b1 = 1.0, b2 = 1.0;
-  for (int i = 0; i < d; ++i) {
-    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
-    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
-    if (i != k) {
-      double f1, f2;
-      if (i == 0) {
-        head_slot_terms<KIND>(pp.x, pp.y, x0, x1, f1, f2);
-      } else {
-        f1 = add(x0, x1);
-        f2 = KIND == 0 ? x1 : x0;
-      }
-      b1 = mul(b1, f1);
-      b2 = mul(b2, f2);
-    }
-  }
-  if (!active) return;
-  double o0, o1;
-  if (k == 0)
-    head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-  else
-    body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-  put_message(P, P.ftov + tw, o0, o1, phase, 1, tw, ufkey);
-}
-
-// one chunk of a whole-node phase: class cc, chunk j of the class
-__device__ __forceinline__ void var_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
-                                          bool marg, bool vt, int it, int phase,
-                                          unsigned long long &dmax, unsigned &ufkey,
-                                          bool uniform) {
-  const int d = cc.info & 0xffff, style = cc.info >> 20;
-  if (style == 0) {
-    const int v = cc.node_begin + j * 32 + lane;
-    if (v >= cc.node_end) return;
-    const int r = cc.row_begin + (v - cc.node_begin) * d;
-    switch (d) {
-#define HBP_VCASE(D) \
-  case D: vnode_fixed<D>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-      HBP_VCASE(1)
-      HBP_VCASE(2)
-      HBP_VCASE(3)
-#if HBP_NODE_MAX > 4
-      HBP_VCASE(4)
-      HBP_VCASE(5)
-#endif
-#if HBP_NODE_MAX > 6
-      HBP_VCASE(6)
-      HBP_VCASE(7)
-#endif
-#undef HBP_VCASE
-      default: vnode_fixed<kNodeMax>(P, v, r, marg, vt, it, phase, dmax, ufkey, uniform); break;
-    }
-  } else if (style == 1) {
-    const int g = cc.grp & 0xff, ln = (lane * (cc.grp >> 8)) >> 16, k = lane - ln * d;
-    const int node = j * g + ln;
-    const int v = cc.node_begin + node;
-    vgroup(P, v, cc.row_begin + node * d + k, k, d, ln * d, ln < g && v < cc.node_end, marg, vt,
-           it, phase, dmax, ufkey, uniform);
-  } else {
-    const int q = cc.row_begin + j * 32 + lane;
-    if (q >= cc.node_end) return;
-    v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), vt ? -1 : 0, marg, it, phase, dmax,
-           ufkey, uniform);
-  }
-}
-
-__device__ __forceinline__ void fac_chunk(const KParams &P, const ChunkClass &cc, int j, int lane,
-                                          int phase, unsigned &ufkey) {
-  const int d = cc.info & 0xffff, kind = (cc.info >> 16) & 0xf, style = cc.info >> 20;
-  if (style == 0) {
-    const int f = cc.node_begin + j * 32 + lane;
-    if (f >= cc.node_end) return;
-    const int r = cc.row_begin + (f - cc.node_begin) * d;
-    if (kind == 0)
-      fnode_k<0>(P, f, r, d, phase, ufkey);
-    else
-      fnode_k<1>(P, f, r, d, phase, ufkey);
-  } else if (style == 1) {
-    const int g = cc.grp & 0xff, ln = (lane * (cc.grp >> 8)) >> 16, k = lane - ln * d;
-    const int node = j * g + ln;
-    const int f = cc.node_begin + node;
-    const bool active = ln < g && f < cc.node_end;
-    if (kind == 0)
-      fgroup<0>(P, f, cc.row_begin + node * d + k, k, d, ln * d, active, phase, ufkey);
-    else
-      fgroup<1>(P, f, cc.row_begin + node * d + k, k, d, ln * d, active, phase, ufkey);
-  } else {
-    const int p = cc.row_begin + j * 32 + lane;
-    if (p >= cc.node_end) return;
-    f_item(P, p, __ldg(P.fslot + p), __ldg(P.vtof_twin + p), phase, ufkey);
-  }
-}
+// the per-node kernels with the run-time normalise flag (namespace n0; n1
+// below fixes it on). Neither is hbp itself, so argument-dependent lookup on
+// KParams cannot mix the two copies.
+namespace n0 {
+#define HBP_NORMALIZE(P) ((P).normalize)
+#include "lbp_node.inc"
+#undef HBP_NORMALIZE
+}  // namespace n0
+using namespace n0;
 
 
 
@@ -1276,8 +760,16 @@ __device__ __forceinline__ void sync_point_hooked(Ctrl *c, Sync &s, unsigned arr
   __syncthreads();
 }
 
+// the per-node kernels again with normalisation fixed on (lbp_parall<.., true>)
+namespace n1 {
+#define HBP_NORMALIZE(P) 1
+#include "lbp_node.inc"
+#undef HBP_NORMALIZE
+}  // namespace n1
+
 // every node of one side in class-uniform warp chunks (the same loop as
-// exec_phase's list == 2 branch)
+// exec_phase's list == 2 branch); NORM: the n1 kernels
+template <bool NORM>
 __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, int seq, int it,
                                            int pidx, bool marg, bool vt,
                                            unsigned long long &dmax, unsigned &ufkey) {
@@ -1300,17 +792,24 @@ __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, in
       int c = (G == (int)gridDim.x && r < kRoundTab) ? rtab[r] : 0;
       while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
       const ChunkClass &cc = ccs[c];
-      if (var)
-        var_chunk(P, cc, k - cc.chunk_begin, lane, marg, vt, it, pidx, dmax, ufkey, false);
-      else
-        fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+      if (NORM) {
+        if (var)
+          n1::var_chunk(P, cc, k - cc.chunk_begin, lane, marg, vt, it, pidx, dmax, ufkey, false);
+        else
+          n1::fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+      } else {
+        if (var)
+          var_chunk(P, cc, k - cc.chunk_begin, lane, marg, vt, it, pidx, dmax, ufkey, false);
+        else
+          fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
+      }
     }
     if (lane == 0) rn = atomicAdd(claim, 1);
     r = __shfl_sync(0xffffffffu, rn, 0);
   }
 }
 
-template <int THREADS>
+template <int THREADS, bool NORM>
 __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__ KParams P) {
   Ctrl *C = P.ctrl;
   const bool multi = gridDim.x > 1;
@@ -1363,7 +862,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__
       unsigned long long dmax = 0;
       unsigned ufkey = 0;
       trace_mark(P, it, 0, 0);
-      node_phase(P, true, (int)gridDim.x, it * 2, it, 0, true, !final_pass, dmax, ufkey);
+      node_phase<NORM>(P, true, (int)gridDim.x, it * 2, it, 0, true, !final_pass, dmax, ufkey);
       flush_underflow(P, it, 0, ufkey);
       trace_mark(P, it, 0, 1);
 #pragma unroll
@@ -1407,7 +906,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__
       unsigned long long unused = 0;
       unsigned ufkey = 0;
       trace_mark(P, it, 1, 0);
-      node_phase(P, false, fG, it * 2 + 1, it, 1, false, true, unused, ufkey);
+      node_phase<NORM>(P, false, fG, it * 2 + 1, it, 1, false, true, unused, ufkey);
       flush_underflow(P, it, 1, ufkey);
       trace_mark(P, it, 1, 1);
       if (fG == (int)gridDim.x)
@@ -1803,7 +1302,8 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   g->threads = hbp::kThreads;
   g->kernel = (const void *)hbp::lbp_persistent<hbp::kThreads, false>;
   g->kernel_fused = (const void *)hbp::lbp_persistent<hbp::kFusedThreads, true>;
-  g->kernel_parall = (const void *)hbp::lbp_parall<hbp::kParallThreads>;
+  g->kernel_parall = (const void *)hbp::lbp_parall<hbp::kParallThreads, true>;
+  g->kernel_parall_nonorm = (const void *)hbp::lbp_parall<hbp::kParallThreads, false>;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel, g->threads, 0));
   g->coop_blocks = std::max(1, per_sm) * g->num_sms;
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_fused,
@@ -1923,6 +1423,7 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
   const auto &phs = p->host.phases;
   const bool two_phase = phs.size() == 2 && phs[0].list == 2 && phs[1].list == 2;
   p->kernel = fused ? g->kernel_fused : two_phase ? g->kernel_parall : g->kernel;
+  p->kernel_nonorm = two_phase ? g->kernel_parall_nonorm : p->kernel;
   p->threads = fused ? hbp::kFusedThreads : two_phase ? hbp::kParallThreads : g->threads;
   int coop = fused ? g->coop_blocks_fused : two_phase ? g->coop_blocks_parall : g->coop_blocks;
   // small levels on a thread-block cluster of csize CTAs (HBP_CSIZE, A/B)
@@ -2179,10 +1680,10 @@ static hbp_status launch_kernel(hbp_plan *p, hbp::KParams &P) {
     cfg.stream = p->g->stream;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    HBP_CUDA(cudaLaunchKernelExC(&cfg, p->kernel, args));
+    HBP_CUDA(cudaLaunchKernelExC(&cfg, P.normalize ? p->kernel : p->kernel_nonorm, args));
   } else {
-    HBP_CUDA(cudaLaunchCooperativeKernel(p->kernel, dim3(p->grid), dim3(p->threads), args, 0,
-                                         p->g->stream));
+    HBP_CUDA(cudaLaunchCooperativeKernel(P.normalize ? p->kernel : p->kernel_nonorm, dim3(p->grid),
+                                         dim3(p->threads), args, 0, p->g->stream));
   }
   return HBP_OK;
 }
