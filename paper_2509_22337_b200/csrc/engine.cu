@@ -782,15 +782,19 @@ __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, in
   const ChunkClass *ccs = var ? s_vcc : s_fcc;
   const int ncc = var ? P.nvcc : P.nfcc;
   const unsigned char *rtab = var ? s_vround : s_fround;
-  int r = 0;
-  if (lane == 0) r = atomicAdd(claim, 1);
-  r = __shfl_sync(0xffffffffu, r, 0);
+  // the first round of every warp is its own index; later ones are claimed
+  const int nwarps = (int)(blockDim.x >> 5);
+  int r = (int)(threadIdx.x >> 5);
   while (r * G < nchunks) {
     int rn = 0;
     const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
     if (k < nchunks) {
-      int c = (G == (int)gridDim.x && r < kRoundTab) ? rtab[r] : 0;
-      while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
+      // lbp_parall's table holds this CTA's exact class per round
+      int c = 0;
+      if (G == (int)gridDim.x && r < kRoundTab)
+        c = rtab[r];
+      else
+        while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
       const ChunkClass &cc = ccs[c];
       if (NORM) {
         if (var)
@@ -804,7 +808,7 @@ __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, in
           fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
       }
     }
-    if (lane == 0) rn = atomicAdd(claim, 1);
+    if (lane == 0) rn = atomicAdd(claim, 1) + nwarps;
     r = __shfl_sync(0xffffffffu, rn, 0);
   }
 }
@@ -819,8 +823,10 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__
   if (threadIdx.x == 0) s_dmax = 0;
   for (int i = threadIdx.x; i < P.nvcc; i += blockDim.x) s_vcc[i] = P.vcc[i];
   for (int i = threadIdx.x; i < P.nfcc; i += blockDim.x) s_fcc[i] = P.fcc[i];
+  // the class of this CTA's chunk in round r of a grid-wide phase
   for (int r = threadIdx.x; r < kRoundTab; r += blockDim.x) {
-    const int k = r * (int)gridDim.x;
+    const int G = (int)gridDim.x;
+    const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
     int c = 0;
     while (c + 1 < P.nvcc && P.vcc[c + 1].chunk_begin <= k) ++c;
     s_vround[r] = (unsigned char)c;
