@@ -796,6 +796,9 @@ __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, in
       else
         while (c + 1 < ncc && ccs[c + 1].chunk_begin <= k) ++c;
       const ChunkClass &cc = ccs[c];
+#ifdef HBP_TRACE_CHUNKS  // per-chunk ns | class << 48 of iteration 3 (tools/chunk_probe.py)
+      const unsigned long long t0 = globaltimer();
+#endif
       if (NORM) {
         if (var)
           n1::var_chunk(P, cc, k - cc.chunk_begin, lane, marg, vt, it, pidx, dmax, ufkey, false);
@@ -807,6 +810,14 @@ __device__ __forceinline__ void node_phase(const KParams &P, bool var, int G, in
         else
           fac_chunk(P, cc, k - cc.chunk_begin, lane, pidx, ufkey);
       }
+#ifdef HBP_TRACE_CHUNKS
+      if (P.trace && it == 3 && nchunks <= kChunkTrace) {
+        __syncwarp();
+        if (lane == 0)
+          P.trace[(size_t)kTraceIters * 2 * gridDim.x * 2 + pidx * kChunkTrace + k] =
+              (globaltimer() - t0) | (unsigned long long)c << 48;
+      }
+#endif
     }
     if (lane == 0) rn = atomicAdd(claim, 1) + nwarps;
     r = __shfl_sync(0xffffffffu, rn, 0);
