@@ -482,41 +482,64 @@ __device__ __forceinline__ void cluster0_sync(int csize) {
   }
 }
 
-// A run of consecutive small fused levels [p0, p1) on the small-level CTAs:
-// a tight loop -- the level's lanes, the barrier, the next level -- instead
-// of the generic phase loop, whose per-phase prologue (descriptor copies,
-// transition logic, look-ahead) measured about 1 us per level on B200.
-// Each level prefetches the next level's lane records into L1 first.
-__device__ __forceinline__ void run_small_fused(const KParams &P, const Phase *cache, int p0,
-                                                int p1, int it) {
+// A run of consecutive small phases [p0, p1) on the small-level CTAs (fused
+// levels, and the vtof / ftov phases of unfused ones): a tight loop -- the
+// phase's items, the barrier, the next phase -- instead of the generic phase
+// loop, whose per-phase prologue (descriptor copies, transition logic,
+// look-ahead) measured about 1 us per level on B200. Each phase loads this
+// thread's first item of the next one (a fused lane record: L1 prefetch; a
+// slot item: its slot-word / twin lines prefetched after this phase's work).
+// Underflow flags are published per phase (the attribution re-run halts at
+// the earliest failing phase; runs are not used in the halted iteration).
+template <bool FUSED>
+__device__ __forceinline__ void run_small(const KParams &P, const Phase *cache, int p0, int p1,
+                                          int it) {
   const int stride = P.csize * (int)blockDim.x;
   const int start = (int)blockIdx.x * (int)blockDim.x + (int)threadIdx.x;
-  auto span = [&](int p, int &b, int &n) {
-    const Phase &ph = p < kPhaseCache ? cache[p] : P.phases[p];
-    b = ph.begin;
-    n = ph.end - ph.begin;
-  };
-  unsigned ufkey = 0;
-  int b, n;
-  span(p0, b, n);
+  auto at = [&](int p) -> const Phase & { return p < kPhaseCache ? cache[p] : P.phases[p]; };
+  unsigned long long unused = 0;
   for (int p = p0; p < p1; ++p) {
     if (p > p0) cluster0_sync(P.csize);
-    int nb = 0, nn = 0;
+    const Phase &ph = at(p);
+    const int type = ph.type, b = ph.begin, n = ph.end - ph.begin;
+    int nxt = -1, ntype = 0;
     if (p + 1 < p1) {
-      span(p + 1, nb, nn);
-      if (start < nn) {
-        const int4 *nx = P.fitems + 2 * (size_t)(nb + start);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
+      const Phase &np = at(p + 1);
+      ntype = np.type;
+      if (start < np.end - np.begin) {
+        if (np.type == 2)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.fitems + 2 * (size_t)(np.begin + start)));
+        else
+          nxt = __ldg(P.items + np.begin + start) & (kWriteBit - 1);
       }
     }
-    for (int i = start; i < n; i += stride) {
-      const int4 *lr = P.fitems + 2 * (size_t)(b + i);
-      fused_lane(P, __ldg(lr), __ldg(lr + 1), it, p, ufkey);
+    unsigned ufkey = 0;
+    if (FUSED && type == 2) {
+      for (int i = start; i < n; i += stride) {
+        const int4 *lr = P.fitems + 2 * (size_t)(b + i);
+        fused_lane(P, __ldg(lr), __ldg(lr + 1), it, p, ufkey);
+      }
+    } else if (type == 0) {
+      for (int i = start; i < n; i += stride) {
+        const int item = __ldg(P.items + b + i);
+        const int q = item & (kWriteBit - 1);
+        v_item(P, q, __ldg(P.vslot + q), __ldg(P.ftov_twin + q), (item & kWriteBit) ? 1 : 0, false, it,
+               p, unused, ufkey, false);
+      }
+    } else {
+      for (int i = start; i < n; i += stride) {
+        const int q = __ldg(P.items + b + i);
+        f_item(P, q, __ldg(P.fslot + q), __ldg(P.vtof_twin + q), p, ufkey);
+      }
     }
-    b = nb;
-    n = nn;
+    flush_underflow(P, it, p, ufkey);
+    if (nxt >= 0) {
+      const void *x = ntype == 1 ? (const void *)(P.fslot + nxt) : (const void *)(P.vslot + nxt);
+      const void *y = ntype == 1 ? (const void *)(P.vtof_twin + nxt) : (const void *)(P.ftov_twin + nxt);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(x));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(y));
+    }
   }
-  flush_underflow(P, it, p0, ufkey);
 }
 
 // marginals of the stopping iteration in the reference's variable order
@@ -659,10 +682,13 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_persistent(const __grid_consta
         }
       }
       if (it == P.halt_it && p == P.halt_phase) return;  // attribution re-run
-      // a run of small fused levels (its first phase's sbegin = the run's end;
-      // fused plans are never halted -- their attribution replays unfused)
-      if (FUSED && ph.type == 2 && !ph.grid && ph.sbegin > p + 1) {
-        if ((int)blockIdx.x < P.csize) run_small_fused(P, s_ph, p, ph.sbegin, it);
+      // a run of small phases (its first phase's sbegin = the run's end); not
+      // in an attribution re-run's halted iteration. The run's phases skip
+      // exec_phase, whose prologue resets the whole-node claim counter of the
+      // following phase: that reset is done here, by every CTA.
+      if (ph.list != 2 && !ph.grid && ph.sbegin > p + 1 && it != P.halt_it) {
+        if ((int)blockIdx.x < P.csize) run_small<FUSED>(P, s_ph, p, ph.sbegin, it);
+        if (threadIdx.x == 0) s_claim[(it * P.nphases + ph.sbegin) & 1] = 0;
         p = ph.sbegin - 1;
         continue;
       }

@@ -557,12 +557,17 @@ hbp_status build_plan(const HostLayout &L, int64_t k, const int64_t *s_off,
       }
     }
   }
-  // runs of consecutive small fused levels: the first phase of a run carries
-  // the run's end in sbegin (the kernel executes the run in a tight loop)
+  // runs of consecutive small item phases (fused levels, list-mode vtof /
+  // ftov phases; never phase 0): the first phase of a run carries the run's
+  // end in sbegin (the kernel executes the run in a tight loop)
+  auto small_item = [&](size_t i) {
+    const Phase &ph = P.phases[i];
+    return i > 0 && !ph.grid && (ph.list == 1 || ph.list == 3);
+  };
   for (size_t i = P.phases.size(); i-- > 0;) {
     Phase &ph = P.phases[i];
-    if (ph.type != 2 || ph.grid) continue;
-    const bool next_small = i + 1 < P.phases.size() && P.phases[i + 1].type == 2 && !P.phases[i + 1].grid;
+    if (!small_item(i)) continue;
+    const bool next_small = i + 1 < P.phases.size() && small_item(i + 1);
     ph.sbegin = next_small ? P.phases[i + 1].sbegin : (int32_t)(i + 1);
   }
   return HBP_OK;
