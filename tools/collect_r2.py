@@ -108,8 +108,11 @@ json.dump({"kernel": "sweep_ws", "sets": 1024, "dram_bytes_per_launch": sw["dram
                      f"gpurun_out/{tag}): dram__bytes_read.sum + dram__bytes_write.sum in {sw['duration_ms']:.1f} ms"},
           open(os.path.join(prof, "traffic.json"), "w"))
 
-# ---- single-graph kernels
-l2 = {}
+# ---- single-graph kernels (entries of configs without a capture here are kept)
+try:
+    l2 = json.load(open(os.path.join(prof, "l2_traffic.json")))
+except (OSError, ValueError):
+    l2 = {}
 lines += ["", "## Single-graph kernels, full captures", "",
           "`ncu --set full --launch-skip 3 --launch-count 1 -k regex:lbp_ python tools/time_probe.py <config> 2` "
           "(one launch = one whole run to convergence).", "",
