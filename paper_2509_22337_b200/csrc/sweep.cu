@@ -352,12 +352,19 @@ __device__ __forceinline__ void ws_var(const SweepParams &P, const SwLaneT<T> *L
   }
 }
 
-// any degree, one set, rows re-read per target (heavy nodes: global memory)
+// any degree, one set, rows re-read per target (heavy nodes: global memory).
+// Not inlined (rare, long); its state goes in and out by value so that the
+// callers' running |dP1| / underflow registers never need an address (an
+// escaping reference pins them to local memory on the hot path).
+struct WsVarAcc {
+  unsigned long long dmax;
+  unsigned uf;
+};
 template <bool NORM, typename T>
-__device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &L, int v,
-                                        const typename Ar<T>::T2 *x, int d, const int *tw, unsigned code,
-                                        double prev_p0, int it, bool write_vtof,
-                                        unsigned long long &dmax, unsigned &uf) {
+__device__ __noinline__ WsVarAcc ws_var_any(const SweepParams &P, typename Ar<T>::T2 *vtof,
+                                            double *p0, int s, int v, const typename Ar<T>::T2 *x,
+                                            int d, const int *tw, unsigned code, double prev_p0,
+                                            int it, bool write_vtof, WsVarAcc acc) {
   if (write_vtof) {
     for (int j = 0; j < d; ++j) {
       const unsigned t = (unsigned)tw[j];
@@ -372,10 +379,10 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &
       if (code) sw_clamp(code, b0, b1);
       if (NORM) {
         const double tt = add(b0, b1);
-        uf = tt < kMinMessageSum ? t + 1 : uf;
+        acc.uf = tt < kMinMessageSum ? t + 1 : acc.uf;
         div2_rn(b0, b1, tt, b0, b1);
       }
-      st2(L.vtof + t * 32, b0, b1);
+      st2(vtof + t * 32, b0, b1);
     }
   }
   double q0 = 1.0, q1 = 1.0;
@@ -385,18 +392,19 @@ __device__ __noinline__ void ws_var_any(const SweepParams &P, const SwLaneT<T> &
     q1 = mul(q1, m.y);
   }
   if (code) sw_clamp(code, q0, q1);
-  sw_marginal_d(P, L.p0 + v * 32, L.s, v, it, q0, q1, prev_p0, dmax);
+  sw_marginal_d(P, p0 + v * 32, s, v, it, q0, q1, prev_p0, acc.dmax);
+  return acc;
 }
 
 template <bool NORM, typename T>
-__device__ __forceinline__ void ws_put(const SwLaneT<T> &L, int t, double o0, double o1, unsigned &uf,
-                                      bool store) {
+__device__ __forceinline__ void ws_put(typename Ar<T>::T2 *ftov, int t, double o0, double o1,
+                                      unsigned &uf, bool store) {
   if (NORM) {
     const double tt = add(o0, o1);
     uf = tt < kMinMessageSum ? (unsigned)t + 1 : uf;
     div2_rn(o0, o1, tt, o0, o1);
   }
-  if (store) st2(L.ftov + t * 32, o0, o1);
+  if (store) st2(ftov + t * 32, o0, o1);
 }
 
 // Factor node of degree D for NS sets; FIRST: iteration 1 (every vtof message
@@ -435,7 +443,7 @@ __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>
     }
     double o0, o1;
     head_message<KIND>(pp.x, pp.y, h1, h2, o0, o1);
-    ws_put<NORM, T>(L[u], tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
+    ws_put<NORM, T>(L[u].ftov, tw[0], o0, o1, uf[u], NS == 1 || alive[u]);
   }
   if (D > 1) {
     double a1[NS], a2[NS];
@@ -453,7 +461,7 @@ __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>
         }
         double o0, o1;
         body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-        ws_put<NORM, T>(L[u], tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
+        ws_put<NORM, T>(L[u].ftov, tw[j], o0, o1, uf[u], NS == 1 || alive[u]);
         a1[u] = mul(a1[u], sm[u][j]);
         a2[u] = mul(a2[u], KIND == 0 ? m1[u][j] : m0[u][j]);
       }
@@ -462,9 +470,8 @@ __device__ __forceinline__ void ws_fac(const SwLaneT<T> *L, const typename Ar<T>
 }
 
 template <int KIND, bool NORM, bool FIRST, typename T>
-__device__ __noinline__ void ws_fac_any(const SwLaneT<T> &L, const typename Ar<T>::T2 *x, int d,
-                                        const int *tw,
-                                        double2 pp, unsigned &uf) {
+__device__ __noinline__ unsigned ws_fac_any(typename Ar<T>::T2 *ftov, const typename Ar<T>::T2 *x,
+                                            int d, const int *tw, double2 pp, unsigned uf) {
   const double c = NORM ? 0.5 : 1.0;
   for (int j = 0; j < d; ++j) {
     double b1 = 1.0, b2 = 1.0;
@@ -486,8 +493,9 @@ __device__ __noinline__ void ws_fac_any(const SwLaneT<T> &L, const typename Ar<T
       head_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
     else
       body_message<KIND>(pp.x, pp.y, b1, b2, o0, o1);
-    ws_put<NORM, T>(L, tw[j], o0, o1, uf, true);
+    ws_put<NORM, T>(ftov, tw[j], o0, o1, uf, true);
   }
+  return uf;
 }
 
 // degree dispatch; NS = 2 keeps the register path to degree 4 (two sets of rows)
@@ -510,7 +518,7 @@ __device__ __forceinline__ void ws_fac_k(const SwLaneT<T> *L, const typename Ar<
     default:
 #pragma unroll
       for (int u = 0; u < NS; ++u)
-        if (NS == 1 || alive[u]) ws_fac_any<KIND, NORM, FIRST, T>(L[u], x[u], d, tw, pp, uf[u]);
+        if (NS == 1 || alive[u]) uf[u] = ws_fac_any<KIND, NORM, FIRST, T>(L[u].ftov, x[u], d, tw, pp, uf[u]);
       break;
   }
 }
@@ -541,9 +549,12 @@ __device__ __forceinline__ void ws_var_k(const SweepParams &P, const SwLaneT<T> 
     default:
 #pragma unroll
       for (int u = 0; u < NS; ++u)
-        if (NS == 1 || alive[u])
-          ws_var_any<NORM, T>(P, L[u], v, x[u], d, tw, code[u], prev_p0[u], it, write_vtof, dmax[u],
-                           uf[u]);
+        if (NS == 1 || alive[u]) {
+          const WsVarAcc a = ws_var_any<NORM, T>(P, L[u].vtof, L[u].p0, L[u].s, v, x[u], d, tw,
+                                                 code[u], prev_p0[u], it, write_vtof, {dmax[u], uf[u]});
+          dmax[u] = a.dmax;
+          uf[u] = a.uf;
+        }
       break;
   }
 }
@@ -658,8 +669,8 @@ __device__ __forceinline__ void ws_consume_fac(const SweepParams &P, WsShared<NS
           for (int u = 0; u < NS; ++u) {
             if (!alive[u]) continue;
             const typename Ar<T>::T2 *x = L[u].vtof + (size_t)r * 32;
-            if (!is_or) ws_fac_any<0, NORM, FIRST, T>(L[u], x, d, tw, pp, uf[u]);
-            else ws_fac_any<1, NORM, FIRST, T>(L[u], x, d, tw, pp, uf[u]);
+            uf[u] = !is_or ? ws_fac_any<0, NORM, FIRST, T>(L[u].ftov, x, d, tw, pp, uf[u])
+                           : ws_fac_any<1, NORM, FIRST, T>(L[u].ftov, x, d, tw, pp, uf[u]);
           }
         } else {
           const int *tw = ch.tw + (r - tw_lo);
@@ -715,10 +726,13 @@ __device__ __forceinline__ void ws_consume_var(const SweepParams &P, WsShared<NS
         if (ch.heavy) {
 #pragma unroll
           for (int u = 0; u < NS; ++u)
-            if (alive[u])
-              ws_var_any<NORM, T>(P, L[u], v, L[u].ftov + (size_t)r * 32, d,
-                               (const int *)P.ftov_twin + r, code[u], prev_p0[u], it, write_vtof,
-                               dmax[u], uf[u]);
+            if (alive[u]) {
+              const WsVarAcc a = ws_var_any<NORM, T>(
+                  P, L[u].vtof, L[u].p0, L[u].s, v, L[u].ftov + (size_t)r * 32, d,
+                  (const int *)P.ftov_twin + r, code[u], prev_p0[u], it, write_vtof, {dmax[u], uf[u]});
+              dmax[u] = a.dmax;
+              uf[u] = a.uf;
+            }
           continue;
         }
         const int *tw = ch.tw + (r - tw_lo);
