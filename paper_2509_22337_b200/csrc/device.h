@@ -46,6 +46,16 @@ struct hbp_graph {
   const void *kernel_parall = nullptr;  // its instance for PARALL plans (two whole-node phases)
   const void *kernel_parall_nonorm = nullptr;  // the same without message normalisation
   int coop_blocks_parall = 0;
+  const void *kernel_pslot = nullptr;  // PARALL plans as one phase per iteration (lbp_pslot)
+  const void *kernel_pslot_nonorm = nullptr;
+  int coop_blocks_pslot = 0;
+  // lbp_pslot's slot chunks (32 int4 lane records + one info word each,
+  // layout_dev.cu build_pslot_device) and second ftov / P0 buffers (on first use)
+  int4 *d_srec = nullptr;
+  int *d_sinfo = nullptr;
+  int pslot_chunks = 0, pslot_chunks_nounary = 0;
+  double2 *d_ftov_alt = nullptr;
+  double *d_p0_alt = nullptr;
   int *d_vtof_twin = nullptr, *d_vorig = nullptr, *d_vrow = nullptr, *d_frow = nullptr;
   unsigned *d_ftov_twin = nullptr;
   int2 *d_vslot = nullptr, *d_fslot = nullptr;
@@ -86,7 +96,8 @@ struct hbp_graph {
     cudaSetDevice(device);
     // the layout, message buffers and layout scratch live in d_block (pool)
     if (d_block) cudaFreeAsync(d_block, own_stream ? own_stream : stream);
-    for (void *p : {(void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace})
+    for (void *p : {(void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace,
+                    (void *)d_srec, (void *)d_sinfo, (void *)d_ftov_alt, (void *)d_p0_alt})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -99,6 +110,7 @@ namespace hbp {
 // on first host-side use, and the PARALL shape test of a one-batch schedule
 hbp_status build_layout_device(const hbp_graph_desc &desc, hbp_graph *g);
 hbp_status ensure_host_layout(hbp_graph *g);
+hbp_status build_pslot_device(hbp_graph *g);
 hbp_status parall_check_device(hbp_graph *g, int64_t ns, const int32_t *s_edges, int64_t nt,
                                const int32_t *t_edges, bool *is_parall);
 }  // namespace hbp
@@ -115,6 +127,7 @@ struct hbp_plan {
   const void *kernel_nonorm = nullptr;  // the instance for normalize_messages off
   int threads = 0;
   int csize = 1;  // CTAs (one cluster) that run the small levels
+  bool pslot = false;  // PARALL plan on lbp_pslot (slot classes in KParams::fcc)
   // the schedule as given (reference batch order), for the exact underflow
   // attribution: device [s_edges | t_edges] (stream-ordered pool) + host offsets
   int *d_sched = nullptr;

@@ -54,6 +54,15 @@ constexpr int kParallThreads = HBP_PARALL_THREADS;
 #define HBP_FUSED_THREADS 768
 #endif
 constexpr int kFusedThreads = HBP_FUSED_THREADS;  // plans with fused levels
+#ifndef HBP_PSLOT_THREADS
+#define HBP_PSLOT_THREADS 896
+#endif
+constexpr int kPslotThreads = HBP_PSLOT_THREADS;
+#ifndef HBP_PSLOT_ROW
+#define HBP_PSLOT_ROW 4
+#endif
+constexpr int kPslotRow = HBP_PSLOT_ROW;  // lbp_pslot: variable row slots held in registers
+constexpr int kPslotPairs = (kPslotRow + 2) / 2;  // 32-byte pairs covering a row at any parity  // PARALL as one phase per iteration (lbp_pslot)
 #ifndef HBP_GROUP_MIN
 #define HBP_GROUP_MIN (HBP_NODE_MAX + 1)
 #endif
@@ -134,6 +143,15 @@ struct KParams {
   // iteration halt_it (0: run normally), leaving that phase's inputs intact
   int halt_it, halt_phase;
   const int *canon2v;         // canonical edge -> internal vtof slot (attribution)
+  // lbp_pslot: 32 lane records per slot chunk {variable row start, variable,
+  // factor, variable degree | index in the row << 8 | slot << 16 | valid << 24},
+  // per chunk degree | kind << 8 | longest row << 16 (layout_dev.cu
+  // build_pslot_device); the
+  // second ftov and P0 buffers (iteration it writes buffer it & 1)
+  const int4 *srec;
+  const int *sinfo;
+  double2 *ftov_alt;
+  double *p0_alt;
 };
 
 // --------------------------------------------------------------------------------------
@@ -543,10 +561,11 @@ __device__ __forceinline__ void run_small(const KParams &P, const Phase *cache, 
 }
 
 // marginals of the stopping iteration in the reference's variable order
-__device__ __forceinline__ void write_marginals(const KParams &P) {
+__device__ __forceinline__ void write_marginals(const KParams &P, const double *src = nullptr) {
   const int gs = gridDim.x * blockDim.x;
+  const double *p0s = src ? src : P.p0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < P.V; v += gs) {
-    const double p0 = P.p0[v];
+    const double p0 = p0s[v];
     P.marg[__ldg(P.vorig + v)] = make_double2(p0, sub(1.0, p0));
   }
 }
@@ -970,6 +989,281 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__
   }
 }
 
+
+// ======================================================================================
+// PARALL as ONE phase per iteration (lbp_pslot). The two-phase form reads
+// every message twice per iteration and pays two grid barriers; here a lane
+// per factor slot computes its variable's vtof message straight from the
+// variable's ftov row of the previous iteration (engine.py:186-195: the row
+// without the own slot, left to right), the factor's lanes exchange them by
+// warp shuffles (as a fused level does) and each lane writes the factor's
+// ftov message of its slot (engine.py:198-248). The vtof buffer is never
+// materialised. Reads and writes of one iteration go to different ftov
+// buffers (iteration it writes buffer it & 1), so no lane reads a row another
+// lane is writing -- exactly the two-phase values. The lane holding slot 0
+// of its variable's row has that whole row loaded and also computes the
+// variable's marginal of iteration it-1 (engine.py:510-523) into P0 buffer
+// (it-1) & 1. One grid barrier per iteration; the stop decision on
+// iteration it-2 rides on the barrier closing iteration it (its inputs are
+// loaded while iteration it runs), which the alternating P0 buffers make
+// safe: the marginals of it-2 are still intact when it is taken.
+// Underflow only stops the run: the host replays the schedule with the
+// two-phase kernel, which attributes it exactly (bitwise the same run).
+
+// factor output of one slot with the kind a run-time flag: the operands of
+// head_message / body_message (lbp_kernels.cuh) selected, not the code
+// duplicated -- the same operations on the same values, so the same bits.
+// head: diff = (a - b) prod2, o1 = b prod1 + diff, o0 = (1 - b) prod1 - diff
+// with (a, b) = (p1, p2) for AND, (p2, p1) for OR; body: diff = (a - b) prod2,
+// s = prod1 + diff, with (a, b) = (p2, p1) and (o0, o1) = (prod1, s) for
+// AND, (p1, p2) and (s, prod1) for OR.
+__device__ __forceinline__ void factor_out(bool is_or, bool head, double p1, double p2,
+                                           double prod1, double prod2, double &o0, double &o1) {
+  const bool first = is_or != head;  // a = p1
+  const double a = first ? p1 : p2, b = first ? p2 : p1;
+  const double diff = mul(sub(a, b), prod2);
+  if (head) {
+    o1 = add(mul(b, prod1), diff);
+    o0 = sub(mul(sub(1.0, b), prod1), diff);
+  } else {
+    const double s = add(prod1, diff);
+    o0 = is_or ? s : prod1;
+    o1 = is_or ? prod1 : s;
+  }
+}
+
+// one chunk: info = degree | kind << 8 | longest row << 16 (warp-uniform),
+// rc = the lane's record. One instance for every degree: the kernel's speed
+// tracks its code size (measured: degree- or row-templated instances run
+// 15-70 % slower, instruction-cache bound).
+template <bool NORM>
+__device__ __forceinline__ void pslot_chunk(const KParams &P, int info, int4 rc, int lane, int it,
+                                            bool final_pass, const double2 *fin, double2 *fout,
+                                            const double *p0in, double *p0out,
+                                            unsigned long long &dmax, unsigned &ufkey) {
+  const int d = info & 0xff;
+  const bool is_or = ((info >> 8) & 1) != 0;
+  const bool valid = ((rc.w >> 24) & 1) != 0;
+  const int j = (rc.w >> 8) & 0xff, k = (rc.w >> 16) & 0xff;
+  const bool owner = valid && it >= 2 && j == 0;  // computes the variable's marginal
+  const bool tgt = valid && it >= 2 && !final_pass && d > 1;  // unary factors read no vtof
+  const int dv = (owner || tgt) ? (rc.w & 0xff) : 0;
+  // every load of the lane in one round trip: the row as 32-byte aligned
+  // message pairs (256-bit loads, half the load instructions and L1
+  // wavefronts of one message per load); element e of the pairs is row
+  // slot e - off
+  const int off = rc.x & 1, ne = off + dv;
+  const double2 *base2 = fin + (rc.x - off);
+  double2 y[2 * kPslotPairs];
+#pragma unroll
+  for (int t = 0; t < kPslotPairs; ++t) {
+    double v0 = 1.0, v1 = 1.0, v2 = 1.0, v3 = 1.0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %4, %5;\n\t"
+        "@p ld.global.v4.f64 {%0, %1, %2, %3}, [%6];\n\t}"
+        : "+d"(v0), "+d"(v1), "+d"(v2), "+d"(v3)
+        : "r"(2 * t), "r"(ne), "l"(base2 + 2 * t));
+    y[2 * t] = make_double2(v0, v1);
+    y[2 * t + 1] = make_double2(v2, v3);
+  }
+  const unsigned code = (dv && P.ev) ? P.ev[rc.y] : 0u;
+  double prev_p0 = 0.0;
+  if (owner) prev_p0 = p0in[rc.y];
+  // unary factors' constant messages: iterations 1 and 2 (one per buffer)
+  const bool out = valid && !final_pass && (d > 1 || it <= 2);
+  const double2 pp = out ? __ldg(P.fpar + rc.z) : make_double2(0.0, 0.0);
+  // both row products in one pass, left to right: a = the vtof message's
+  // (slot j skipped, engine.py:186-195), q = the marginal's (engine.py:510-516)
+  double a0 = 1.0, a1 = 1.0, q0 = 1.0, q1 = 1.0;
+#pragma unroll
+  for (int e = 0; e < 2 * kPslotPairs; ++e)
+    if (e >= off && e < ne) {
+      q0 = mul(q0, y[e].x);
+      q1 = mul(q1, y[e].y);
+      if (e != off + j) {
+        a0 = mul(a0, y[e].x);
+        a1 = mul(a1, y[e].y);
+      }
+    }
+  for (int e = 2 * kPslotPairs; e < ne; ++e) {
+    const double2 z = base2[e];
+    q0 = mul(q0, z.x);
+    q1 = mul(q1, z.y);
+    if (e != off + j) {
+      a0 = mul(a0, z.x);
+      a1 = mul(a1, z.y);
+    }
+  }
+  if (owner) {
+    double c0 = q0, c1 = q1;
+    if (code) apply_clamp(code, c0, c1);
+    put_marginal_to(P, p0out + rc.y, c0, c1, it, dmax, prev_p0, -1 - rc.y);
+  }
+  if (final_pass || (d == 1 && it > 2)) return;  // warp-uniform
+  // the vtof message of the slot (iteration 1: the uniform start message)
+  double2 m = make_double2(NORM ? 0.5 : 1.0, NORM ? 0.5 : 1.0);
+  if (tgt) {
+    if (code) apply_clamp(code, a0, a1);
+    if (NORM) {
+      const double t = add(a0, a1);
+      ufkey |= (unsigned)(t < kMinMessageSum);
+      div2_rn(a0, a1, t, a0, a1);
+    }
+    m = make_double2(a0, a1);
+  }
+  // the factor's messages: its vtof row by shuffles within the lane group,
+  // left to right with the own slot skipped (engine.py:198-248)
+  const int base = lane - k;
+  double b1 = 1.0, b2 = 1.0;
+  {
+    const double x0 = __shfl_sync(0xffffffffu, m.x, base);
+    const double x1 = __shfl_sync(0xffffffffu, m.y, base);
+    if (k != 0) {
+      const double c = is_or ? pp.x : pp.y;  // head_slot_terms
+      b1 = mul(b1, add(mul(sub(1.0, c), x0), mul(c, x1)));
+      b2 = mul(b2, sub(x0, x1));
+    }
+  }
+  for (int i = 1; i < d; ++i) {
+    const double x0 = __shfl_sync(0xffffffffu, m.x, base + i);
+    const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
+    if (i != k) {
+      b1 = mul(b1, add(x0, x1));
+      b2 = mul(b2, is_or ? x0 : x1);
+    }
+  }
+  if (out) {
+    double o0, o1;
+    factor_out(is_or, k == 0, pp.x, pp.y, b1, b2, o0, o1);
+    if (NORM) {
+      const double t = add(o0, o1);
+      ufkey |= (unsigned)(t < kMinMessageSum) << 1;
+      div2_rn(o0, o1, t, o0, o1);
+    }
+    fout[rc.x + j] = make_double2(o0, o1);
+  }
+}
+
+template <int THREADS, bool NORM>
+__global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ KParams P) {
+  Ctrl *C = P.ctrl;
+  const bool multi = gridDim.x > 1;
+  const int G = (int)gridDim.x;
+  Sync sy;
+  if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_dmax = 0;
+  __shared__ int s_stop;
+  auto barrier = [&](auto pre) {
+    if (multi) {
+      sync_point_hooked(C, sy, (unsigned)G, true, true, pre, NoHookP{});
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) pre();
+      __syncthreads();
+    }
+  };
+  // "iteration 0": P0 = 0.5, the previous P1 of iteration 1's marginal
+  {
+    const int gs = G * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.p0[i] = 0.5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
+    barrier(NoHookP{});
+  }
+  double2 *const fb0 = P.ftov, *const fb1 = P.ftov_alt;
+  double *const pb0 = P.p0, *const pb1 = P.p0_alt;
+  auto decide = [&](int done, int ufm, int ufg, int tf, unsigned long long db) -> int {
+    if (ufm || ufg == 1) return 4;  // ufg bit1 (a NaN total) suppresses the raise
+    if (__longlong_as_double((long long)db) < P.tol) return 1;
+    if (done == P.max_it) return 2;
+    if (tf) return 3;
+    return 0;
+  };
+  auto finish = [&](int done, unsigned long long db) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      C->iterations = done;
+      C->last_delta = db;
+      C->converged = s_stop == 1;
+      C->stop = s_stop;
+    }
+    write_marginals(P, (done & 1) ? pb1 : pb0);
+  };
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (int)(blockDim.x >> 5);
+  const int nchunks = P.fchunks;
+  for (int it = 1;; ++it) {
+    const bool final_pass = it == P.max_it + 1;
+    // the decision on iteration it-2: its inputs are complete since the
+    // barrier that closed iteration it-1
+    int ufm = 0, ufg = 0, tf = 0;
+    unsigned long long db = 0;
+    if (it >= 3 && threadIdx.x == 0) {
+      ufm = ((const volatile int *)P.uf_msg)[it - 2];
+      ufg = ((const volatile int *)P.uf_marg)[it - 2];
+      tf = ((const volatile int *)P.tflag)[it - 2];
+      db = ((const volatile unsigned long long *)P.delta_bits)[it - 2];
+    }
+    const double2 *fin = (it & 1) ? fb0 : fb1;
+    double2 *fout = (it & 1) ? fb1 : fb0;
+    const double *p0in = (it & 1) ? pb1 : pb0;  // marginals of it-2
+    double *p0out = (it & 1) ? pb0 : pb1;       // marginals of it-1
+    unsigned long long dmax = 0;
+    unsigned ufkey = 0;
+    {
+      // rounds as in node_phase: round r is G consecutive chunks dealt
+      // boustrophedon; a warp's first round is its index, later ones claimed
+      const int seq = it;
+      if (threadIdx.x == 0) s_claim[(seq + 1) & 1] = 0;
+      int *claim = &s_claim[seq & 1];
+      int r = (int)(threadIdx.x >> 5);
+      while (r * G < nchunks) {
+        int rn = 0;
+        const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+        if (k < nchunks) {
+          const int info = __ldg(P.sinfo + k);
+          const int4 rc = __ldg(P.srec + (size_t)k * 32 + lane);
+          pslot_chunk<NORM>(P, info, rc, lane, it, final_pass, fin, fout, p0in, p0out, dmax,
+                            ufkey);
+        }
+        if (lane == 0) rn = atomicAdd(claim, 1) + nwarps;
+        r = __shfl_sync(0xffffffffu, rn, 0);
+      }
+    }
+    flush_underflow(P, it, 0, ufkey);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long w = __shfl_xor_sync(0xffffffffu, dmax, o);
+      dmax = w > dmax ? w : dmax;
+    }
+    if (lane == 0 && dmax) atomicMax(&s_dmax, dmax);
+    auto publish = [&]() {
+      if (it >= 2) {
+        if (s_dmax) atomicMax(&P.delta_bits[it - 1], s_dmax);
+        if (blockIdx.x == 0 && P.time_limit_ns > 0)
+          P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
+      }
+      s_dmax = 0;
+      s_stop = it >= 3 ? decide(it - 2, ufm, ufg, tf, db) : 0;
+    };
+    barrier(publish);
+    if (s_stop) {
+      finish(it - 2, db);
+      return;
+    }
+    if (final_pass) {  // the decision on iteration max_it, right away
+      if (threadIdx.x == 0) {
+        const int done = it - 1;
+        db = ((const volatile unsigned long long *)P.delta_bits)[done];
+        s_stop = decide(done, ((const volatile int *)P.uf_msg)[done],
+                        ((const volatile int *)P.uf_marg)[done], ((const volatile int *)P.tflag)[done],
+                        db);
+      }
+      __syncthreads();
+      finish(it - 1, db);
+      return;
+    }
+  }
+}
+
 }  // namespace hbp
 
 // ======================================================================================
@@ -1355,6 +1649,11 @@ hbp_status hbp_graph_create(const hbp_graph_desc *desc, int32_t device, hbp_grap
   HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_parall,
                                                          hbp::kParallThreads, 0));
   g->coop_blocks_parall = std::max(1, per_sm) * g->num_sms;
+  g->kernel_pslot = (const void *)hbp::lbp_pslot<hbp::kPslotThreads, true>;
+  g->kernel_pslot_nonorm = (const void *)hbp::lbp_pslot<hbp::kPslotThreads, false>;
+  HBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, g->kernel_pslot,
+                                                         hbp::kPslotThreads, 0));
+  g->coop_blocks_pslot = std::max(1, per_sm) * g->num_sms;
   // the layout is built on the device (layout_dev.cu); the host copy of it
   // only when a host-side consumer needs it (hbp::ensure_host_layout)
   hbp::set_last_launches(0);
@@ -1396,6 +1695,12 @@ hbp_status hbp_graph_layout(hbp_graph *g, int64_t *rowptr_ftov, int64_t *ftov_to
 static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const int32_t *s_edges,
                               const int64_t *t_off, const int32_t *t_edges, bool fuse,
                               hbp_plan **out);
+
+// lbp_pslot's slot chunks and second buffers, built once per graph
+static hbp_status ensure_pslot(hbp_graph *g) {
+  if (g->d_srec) return HBP_OK;
+  return hbp::build_pslot_device(g);
+}
 
 hbp_status hbp_plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, const int32_t *s_edges,
                            const int64_t *t_off, const int32_t *t_edges, hbp_plan **out) {
@@ -1469,6 +1774,23 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
   p->kernel_nonorm = two_phase ? g->kernel_parall_nonorm : p->kernel;
   p->threads = fused ? hbp::kFusedThreads : two_phase ? hbp::kParallThreads : g->threads;
   int coop = fused ? g->coop_blocks_fused : two_phase ? g->coop_blocks_parall : g->coop_blocks;
+  // PARALL as one phase per iteration (lbp_pslot) when every factor fits a
+  // warp and no variable has more than kClassMax factors (no huge nodes;
+  // the lane records hold degrees and row indices in 8 bits); HBP_PSLOT=0 (A/B) keeps the two-phase kernel,
+  // which also serves the underflow attribution replay (fuse == false)
+  {
+    const char *pe = getenv("HBP_PSLOT");
+    const hbp::HostLayout &L = g->L;
+    if (two_phase && fuse && !(pe && atoi(pe) == 0) && L.fcls_cnt[0][hbp::kClassMax + 1] == 0 &&
+        L.fcls_cnt[1][hbp::kClassMax + 1] == 0 && L.vcls_cnt[hbp::kClassMax + 1] == 0) {
+      if ((st = ensure_pslot(g)) != HBP_OK) return st;
+      p->pslot = true;
+      p->kernel = g->kernel_pslot;
+      p->kernel_nonorm = g->kernel_pslot_nonorm;
+      p->threads = hbp::kPslotThreads;
+      coop = g->coop_blocks_pslot;
+    }
+  }
   // small levels on a thread-block cluster of csize CTAs (HBP_CSIZE, A/B)
   p->csize = 1;
   if (const char *ce = getenv("HBP_CSIZE")) p->csize = std::max(1, std::min(8, atoi(ce)));
@@ -1654,6 +1976,14 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.csize = p->csize;
   P.halt_it = 0;
   P.halt_phase = 0;
+  if (p->pslot) {
+    P.fchunks = g->pslot_chunks;
+    P.fchunks_nounary = g->pslot_chunks_nounary;
+    P.srec = g->d_srec;
+    P.sinfo = g->d_sinfo;
+    P.ftov_alt = g->d_ftov_alt;
+    P.p0_alt = g->d_p0_alt;
+  }
   HBP_CUDA(cudaEventRecord(g->ev0, g->stream));
   if ((st = launch_kernel(p, P))) return st;
   HBP_CUDA(cudaEventRecord(g->ev1, g->stream));
@@ -1682,7 +2012,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   res->device_ms = ms;
   std::memcpy(&res->last_delta, &hc.last_delta, 8);
   if (hc.stop == 4) {
-    if (p->host.n_fused > 0) {
+    if (p->host.n_fused > 0 || p->pslot) {
       // the attribution replays the failing pass group by group (engine.py:
       // 566-570), which needs the two-phase form of every level: re-run the
       // same schedule unfused -- bitwise the same run -- and attribute there
@@ -2188,6 +2518,9 @@ void hbp_debug_plan_info(hbp_plan *p, int32_t *nphases, int32_t *grid, int32_t *
   *grid = p->grid;
   *threads = p->threads;
 }
+
+// 1 when the plan runs PARALL as one phase per iteration (lbp_pslot); debug only.
+int32_t hbp_debug_plan_pslot(hbp_plan *p) { return p->pslot ? 1 : 0; }
 
 // Debug timeline of the last run with HBP_TRACE=1 (not part of the public header).
 int64_t hbp_debug_trace(hbp_plan *p, unsigned long long *out, int64_t cap) {

@@ -565,6 +565,108 @@ hbp_status parall_check_device(hbp_graph *g, int64_t ns, const int32_t *s_edges,
   return HBP_OK;
 }
 
+
+// ---- lbp_pslot's slot chunks (engine.cu): every factor as a lane group of a
+// 32-lane chunk, one int4 record per lane. Chunks come per class (kind,
+// degree), dearest degree first, the unary factors last; inside a class the
+// factors are ordered by the largest degree of their variables, so a chunk's
+// lanes load rows of similar length (the row loop runs to the chunk's max).
+namespace {
+struct PslotClasses {
+  int n;                        // classes
+  int rank[2][kClassMax + 1];   // (kind, degree) -> class rank, -1: empty
+  int start[2 * kClassMax + 2]; // first sorted position of each class
+  int chunk[2 * kClassMax + 2]; // first chunk of each class
+  int deg[2 * kClassMax + 2], kind[2 * kClassMax + 2];
+};
+
+__global__ void k_pslot_keys(const int *frow, const int *vtof_twin, const int2 *vslot, int F,
+                             int f_or_light, int f_heavy, int f_or_heavy, PslotClasses C,
+                             unsigned *key, int *val) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const int r = frow[f], d = frow[f + 1] - r;
+  const int kind = ((f >= f_or_light && f < f_heavy) || f >= f_or_heavy) ? 1 : 0;
+  int mx = 0;
+  for (int k = 0; k < d; ++k) mx = max(mx, (int)((unsigned)vslot[vtof_twin[r + k]].y >> 16));
+  key[f] = (unsigned)C.rank[kind][d] << 8 | (unsigned)(255 - min(mx, 255));
+  val[f] = f;
+}
+
+__global__ void k_pslot_records(const unsigned *key, const int *perm, const int *frow,
+                                const int *vtof_twin, const int2 *vslot, int F, PslotClasses C,
+                                int4 *srec, int *sinfo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  const int c = (int)(key[i] >> 8), f = perm[i];
+  const int d = C.deg[c], per = 32 / d, pos = i - C.start[c];
+  const int chunk = C.chunk[c] + pos / per, g = pos % per;
+  const int r = frow[f];
+  int mx = 0;
+  for (int k = 0; k < d; ++k) {
+    const int q = vtof_twin[r + k];
+    const int2 w = vslot[q];
+    const int j = w.y & 0xffff, dv = (int)((unsigned)w.y >> 16);
+    mx = max(mx, dv);
+    srec[(size_t)chunk * 32 + g * d + k] = make_int4(q - j, w.x, f, dv | j << 8 | k << 16 | 1 << 24);
+  }
+  // the chunk's first factor has its longest variable row (descending order)
+  if (g == 0) sinfo[chunk] = d | C.kind[c] << 8 | mx << 16;
+}
+}  // namespace
+
+hbp_status build_pslot_device(hbp_graph *g) {
+  const HostLayout &L = g->L;
+  const int F = L.F;
+  cudaStream_t s = g->stream;
+  PslotClasses C{};
+  for (int k = 0; k < 2; ++k)
+    for (int d = 0; d <= kClassMax; ++d) C.rank[k][d] = -1;
+  int pos = 0, chunks = 0;
+  auto add = [&](int d, int k) {
+    const int cnt = L.fcls_cnt[k][d];
+    if (cnt <= 0) return;
+    const int c = C.n++;
+    C.rank[k][d] = c;
+    C.start[c] = pos;
+    C.chunk[c] = chunks;
+    C.deg[c] = d;
+    C.kind[c] = k;
+    pos += cnt;
+    chunks += (cnt + 32 / d - 1) / (32 / d);
+  };
+  for (int d = kClassMax; d >= 2; --d)
+    for (int k = 0; k < 2; ++k) add(d, k);
+  const int chunks_nounary = chunks;
+  for (int k = 0; k < 2; ++k) add(1, k);
+  g->pslot_chunks = chunks;
+  g->pslot_chunks_nounary = chunks_nounary;
+  HBP_CUDA(cudaMalloc(&g->d_srec, (size_t)std::max(1, chunks) * 32 * sizeof(int4)));
+  HBP_CUDA(cudaMalloc(&g->d_sinfo, (size_t)std::max(1, chunks) * sizeof(int)));
+  // + 2 messages: lbp_pslot reads rows as 32-byte aligned pairs (d_ftov is
+  // followed by further arena allocations, which the last pair may touch)
+  HBP_CUDA(cudaMalloc(&g->d_ftov_alt, ((size_t)L.E + 2) * sizeof(double2)));
+  HBP_CUDA(cudaMalloc(&g->d_p0_alt, (size_t)std::max(1, L.V) * sizeof(double)));
+  HBP_CUDA(cudaMemsetAsync(g->d_srec, 0, (size_t)std::max(1, chunks) * 32 * sizeof(int4), s));
+  size_t tmp = 0;
+  HBP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (unsigned *)nullptr, (unsigned *)nullptr,
+                                           (int *)nullptr, (int *)nullptr, F, 0, 16, s));
+  char *buf = nullptr;
+  const size_t fb = ((size_t)std::max(1, F) * 4 + 255) & ~(size_t)255;
+  HBP_CUDA(cudaMallocAsync((void **)&buf, 4 * fb + tmp, s));
+  unsigned *key = (unsigned *)buf, *key_s = (unsigned *)(buf + fb);
+  int *val = (int *)(buf + 2 * fb), *val_s = (int *)(buf + 3 * fb);
+  const unsigned nb = (unsigned)((F + 255) / 256);
+  k_pslot_keys<<<nb, 256, 0, s>>>(g->d_frow, g->d_vtof_twin, g->d_vslot, F, L.f_or_light, L.f_heavy,
+                                  L.f_or_heavy, C, key, val);
+  HBP_CUDA(cub::DeviceRadixSort::SortPairs(buf + 4 * fb, tmp, key, key_s, val, val_s, F, 0, 16, s));
+  k_pslot_records<<<nb, 256, 0, s>>>(key_s, val_s, g->d_frow, g->d_vtof_twin, g->d_vslot, F, C,
+                                     g->d_srec, g->d_sinfo);
+  HBP_CUDA(cudaGetLastError());
+  HBP_CUDA(cudaFreeAsync(buf, s));
+  add_last_launches(3);
+  return HBP_OK;
+}
 }  // namespace hbp
 
 // Diagnostic: every device layout array against the host builder's (tests).

@@ -567,6 +567,66 @@ def test_level_fusion_bitwise_identical_to_two_phase(monkeypatch):
     P.engine.clear_device_cache()
 
 
+def _pslot(g, sched):
+    import ctypes as C
+    f = P._native.lib().hbp_debug_plan_pslot
+    f.restype = C.c_int32
+    f.argtypes = [C.c_void_p]
+    return f(P.engine.device_graph(g).plan(sched, g).handle)
+
+
+def test_pslot_bitwise_identical_to_two_phase(monkeypatch):
+    """PARALL runs as one phase per iteration (lbp_pslot: vtof messages
+    recomputed per factor slot from the variable rows, double-buffered ftov);
+    HBP_PSLOT=0 keeps the two-phase kernel. Same bits, iterations, deltas and
+    history, with and without normalisation and device evidence codes."""
+    rng = np.random.default_rng(777)
+    used = 0
+    graphs = [W.graph("weblech")[0], W.graph("hedc")[0]] + [
+        random_graph(rng, max_vars=60, max_factors=60, max_body=7) for _ in range(16)]
+    for i, g in enumerate(graphs):
+        sched = Strategy.parall().compile(g)
+        for norm in (True, False):
+            opts = EngineOptions(int(rng.integers(1, 80)), 1e-9, normalize_messages=norm,
+                                 record_history=True)
+            ev = None
+            if i % 3 == 1:
+                vs = np.sort(rng.choice(g.num_variables, size=min(3, g.num_variables), replace=False))
+                ev = (vs, rng.integers(0, 2, size=len(vs)).astype(bool))
+            out = []
+            for env in (None, "0"):
+                if env is None:
+                    monkeypatch.delenv("HBP_PSLOT", raising=False)
+                else:
+                    monkeypatch.setenv("HBP_PSLOT", env)
+                P.engine.clear_device_cache()
+                dg = P.engine.device_graph(g)
+                # eligible: no node of degree > 32 (a factor = a lane group of a warp)
+                small = (np.bincount(np.asarray(g.vars)).max() <= 32
+                         and np.diff(np.asarray(g.rowptr)).max() <= 32)
+                assert _pslot(g, sched) == (1 if env is None and small else 0), i
+                used += env is None and small
+                if ev is not None:
+                    dg.set_evidence(*ev)
+                try:
+                    out.append(P.run(g, sched, opts))
+                except UnderflowError as e:
+                    out.append((e.kind, e.iteration, e.index))
+            a, b = out
+            if isinstance(a, tuple) or isinstance(b, tuple):
+                assert a == b, (i, norm)
+                continue
+            assert a.iterations == b.iterations and a.converged == b.converged, (i, norm)
+            assert a.marginals.tobytes() == b.marginals.tobytes(), (i, norm)
+            assert np.asarray(a.deltas).tobytes() == np.asarray(b.deltas).tobytes(), (i, norm)
+            assert len(a.history) == len(b.history)
+            for x, y in zip(a.history, b.history):
+                assert np.asarray(x).tobytes() == np.asarray(y).tobytes(), (i, norm)
+    assert used >= 20, used
+    monkeypatch.delenv("HBP_PSLOT", raising=False)
+    P.engine.clear_device_cache()
+
+
 def test_fp32_run_within_1e5_of_fp64():
     """run(..., EngineOptions(precision="fp32")): fp32
     message storage, fp64 arithmetic -- marginals within the north star's
