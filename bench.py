@@ -704,6 +704,11 @@ def measure_single(torch, key: str, steps: int, warmup: int, e2e: bool = True,
     plan = dg.plan(sched, g)
     copt = plan.options(opts)
     nphases, grid, threads, nfused = plan_info(lib, plan)
+    lib.hbp_debug_plan_pslot.restype = C.c_int32
+    lib.hbp_debug_plan_pslot.argtypes = [C.c_void_p]
+    pslot = lib.hbp_debug_plan_pslot(plan.handle) == 1
+    kernel = ("hbp::lbp_pslot (PARALL, one phase per iteration; whole run in one launch)" if pslot
+              else "hbp::lbp_persistent (whole run in one launch)")
 
     def step():
         res = _native.Result()
@@ -748,17 +753,19 @@ def measure_single(torch, key: str, steps: int, warmup: int, e2e: bool = True,
         "workload": WORKLOAD_TEXT[key] + ", to convergence, L2 flushed (256 MiB write) between runs",
         "value": value, "unit": UNIT, "time_to_convergence_ms": total_ms / steps,
         "iterations": iters[-1], "updates_per_iteration": upd, "k_batches": sched.num_batches,
-        "phases_per_iteration": nphases, "fused_levels": nfused, "grid": [grid, threads],
+        "phases_per_iteration": 1 if pslot else nphases, "fused_levels": nfused,
+        "grid": [grid, threads],
         "parity_vs_reference_golden": parity, "gpu_launches": launches,
     }
     if levelled or key == "C1":
         # dependent-chain latency, not bandwidth: each phase is a barrier-
         # separated dependent step (a level on CTA 0, or a whole-graph pass)
         out["roofline"] = {
-            "bound": "latency", "us_per_phase": 1e3 * mean_ms / (iters[-1] * nphases),
-            "phases": iters[-1] * nphases, "achieved_gbs": achieved,
+            "bound": "latency",
+            "us_per_phase": 1e3 * mean_ms / (iters[-1] * (1 if pslot else nphases)),
+            "phases": iters[-1] * (1 if pslot else nphases), "achieved_gbs": achieved,
             "hbm_frac": achieved / peak, "l2_frac": l2["frac"] if l2 else None,
-            "kernel": "hbp::lbp_persistent (whole run in one launch)",
+            "kernel": kernel,
             "bytes_per_launch": bytes_per_launch}
     else:
         tr = l2_traffic(key)
@@ -770,9 +777,11 @@ def measure_single(torch, key: str, steps: int, warmup: int, e2e: bool = True,
             "peak_source": l2["peak_source"] if l2 else None,
             "hbm": {"peak": peak, "frac": achieved / peak,
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
-            "kernel": "hbp::lbp_persistent (whole run in one launch)",
+            "kernel": kernel,
             "bytes_per_launch": bytes_per_launch,
-            "note": "working set (~28 MB) is L2-resident within a run"}
+            "note": "working set (~36 MB) is L2-resident within a run; algorithmic bytes are "
+                    "SURVEY.md 8(d)'s two-phase count (lbp_pslot moves about the same: it "
+                    "re-reads variable rows instead of writing and reading vtof messages)"}
     if e2e:
         # end to end through run(): fresh device layout + plan every step. The
         # graphs and sweeps of the earlier legs are released (and collected)

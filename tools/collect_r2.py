@@ -64,6 +64,7 @@ def summary(rep):
         "dram_pct": get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed") if "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed" in h else get("FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed"),
         "lts_pct": get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
         "stalls": stall_mix(h, v),
+        "kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "",
     }
 
 
@@ -114,7 +115,7 @@ try:
 except (OSError, ValueError):
     l2 = {}
 lines += ["", "## Single-graph kernels, full captures", "",
-          "`ncu --set full --launch-skip 3 --launch-count 1 -k regex:lbp_ python tools/time_probe.py <config> 2` "
+          "`ncu --set full --launch-skip 3 --launch-count 1 -k 'regex:pslot|parall|persistent' python tools/time_probe.py <config> 2` "
           "(one launch = one whole run to convergence).", "",
           "| config | kernel | ms (ncu) | L2 sectors x 32 B | L1 ld / st sectors | DRAM bytes | warp instr | issue active | regs | stall mix |",
           "|---|---|---|---|---|---|---|---|---|---|"]
@@ -123,7 +124,7 @@ for c in ("C4-PARALL", "C1", "C4-SEQFIX", "C2", "C3"):
     if not os.path.exists(rep):
         continue
     s = summary(rep)
-    kname = "lbp_parall<640>" if c in ("C4-PARALL", "C1") else "lbp_persistent<768, fused>"
+    kname = s["kernel"].replace("(KParams)", "").replace("void ", "").replace("hbp::", "") or "?"
     l2b = s["l2_sectors"] * 32
     l2[c] = {"l2_bytes_per_launch": l2b, "kernel": kname,
              "source": f"ncu --set full lts__t_sectors.sum x 32 B of one launch ({pre}, gpurun_out/{tag})"}

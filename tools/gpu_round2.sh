@@ -16,8 +16,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sweep_ws -c 1 \
     -o $OUT/sweep_ws python tools/sweep_probe.py 1024 1 > $OUT/ncu_sweep.log 2>&1
 for c in C4-PARALL C1 C4-SEQFIX C2 C3; do
-  timeout 900 ncu --kernel-name-base demangled -k regex:lbp_ --launch-skip 3 --launch-count 1 --set full \
-      --import-source on --clock-control none -o $OUT/ncu_$c python tools/time_probe.py $c 2 > $OUT/ncu_$c.log 2>&1
+  bash tools/ncu_c4.sh $TAG $c
 done
+timeout 300 bash -c 'for c in C4-PARALL C1 C4-SEQFIX C2 C3; do python tools/time_probe.py $c 20 2>&1 | tail -1; done' > $OUT/times.txt 2>&1
 ls -la $OUT
 tail -2 $OUT/pytest_gpu.log; cat $OUT/smoke.log | tail -2
