@@ -1071,7 +1071,7 @@ __device__ __forceinline__ void pslot_chunk(const KParams &P, int info, int4 rc,
   }
   const unsigned code = (dv && P.ev) ? P.ev[rc.y] : 0u;
   double prev_p0 = 0.0;
-  if (owner) prev_p0 = p0in[rc.y];
+  if (owner) prev_p0 = it > 2 ? p0in[rc.y] : 0.5;  // iteration 1's previous P1 is 0.5
   // unary factors' constant messages: iterations 1 and 2 (one per buffer)
   const bool out = valid && !final_pass && (d > 1 || it <= 2);
   const double2 pp = out ? __ldg(P.fpar + rc.z) : make_double2(0.0, 0.0);
@@ -1153,9 +1153,9 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
   const bool multi = gridDim.x > 1;
   const int G = (int)gridDim.x;
   Sync sy;
-  if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_dmax = 0;
   __shared__ int s_stop;
+  if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_dmax = 0, s_stop = 0;
   auto barrier = [&](auto pre) {
     if (multi) {
       sync_point_hooked(C, sy, (unsigned)G, true, true, pre, NoHookP{});
@@ -1165,13 +1165,10 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
       __syncthreads();
     }
   };
-  // "iteration 0": P0 = 0.5, the previous P1 of iteration 1's marginal
-  {
-    const int gs = G * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.V; i += gs) P.p0[i] = 0.5;
-    if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
-    barrier(NoHookP{});
-  }
+  // iteration 1 reads no message (and iteration 2's previous P0 is the
+  // constant 0.5): no start-up pass, no barrier before it
+  if (blockIdx.x == 0 && threadIdx.x == 0) C->t0 = globaltimer();
+  __syncthreads();
   double2 *const fb0 = P.ftov, *const fb1 = P.ftov_alt;
   double *const pb0 = P.p0, *const pb1 = P.p0_alt;
   auto decide = [&](int done, int ufm, int ufg, int tf, unsigned long long db) -> int {
@@ -1195,15 +1192,17 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
   const int nchunks = P.fchunks;
   for (int it = 1;; ++it) {
     const bool final_pass = it == P.max_it + 1;
-    // the decision on iteration it-2: its inputs are complete since the
-    // barrier that closed iteration it-1
-    int ufm = 0, ufg = 0, tf = 0;
+    // the decision on iteration it-2, whose inputs are complete since the
+    // barrier that closed iteration it-1: thread 0 takes it while the other
+    // warps already run this iteration's chunks, and they stop claiming
+    // chunks once it says stop (the iteration's output is then never read)
     unsigned long long db = 0;
     if (it >= 3 && threadIdx.x == 0) {
-      ufm = ((const volatile int *)P.uf_msg)[it - 2];
-      ufg = ((const volatile int *)P.uf_marg)[it - 2];
-      tf = ((const volatile int *)P.tflag)[it - 2];
       db = ((const volatile unsigned long long *)P.delta_bits)[it - 2];
+      *(volatile int *)&s_stop =
+          decide(it - 2, ((const volatile int *)P.uf_msg)[it - 2],
+                 ((const volatile int *)P.uf_marg)[it - 2], ((const volatile int *)P.tflag)[it - 2],
+                 db);
     }
     const double2 *fin = (it & 1) ? fb0 : fb1;
     double2 *fout = (it & 1) ? fb1 : fb0;
@@ -1218,7 +1217,7 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
       if (threadIdx.x == 0) s_claim[(seq + 1) & 1] = 0;
       int *claim = &s_claim[seq & 1];
       int r = (int)(threadIdx.x >> 5);
-      while (r * G < nchunks) {
+      while (r * G < nchunks && !*(volatile int *)&s_stop) {
         int rn = 0;
         const int k = r * G + ((r & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
         if (k < nchunks) {
@@ -1238,6 +1237,11 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
       dmax = w > dmax ? w : dmax;
     }
     if (lane == 0 && dmax) atomicMax(&s_dmax, dmax);
+    __syncthreads();
+    if (s_stop) {  // every CTA took the same decision: none waits at a barrier
+      finish(it - 2, db);
+      return;
+    }
     auto publish = [&]() {
       if (it >= 2) {
         if (s_dmax) atomicMax(&P.delta_bits[it - 1], s_dmax);
@@ -1245,13 +1249,8 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
           P.tflag[it - 1] = (long long)(globaltimer() - C->t0) > P.time_limit_ns;
       }
       s_dmax = 0;
-      s_stop = it >= 3 ? decide(it - 2, ufm, ufg, tf, db) : 0;
     };
     barrier(publish);
-    if (s_stop) {
-      finish(it - 2, db);
-      return;
-    }
     if (final_pass) {  // the decision on iteration max_it, right away
       if (threadIdx.x == 0) {
         const int done = it - 1;
