@@ -51,6 +51,7 @@ struct hbp_graph {
   int coop_blocks_pslot = 0;
   // lbp_pslot's slot chunks (32 int4 lane records + one info word each,
   // layout_dev.cu build_pslot_device) and second ftov / P0 buffers (on first use)
+  void *d_pslot_block = nullptr;  // the four below, one pool allocation
   int4 *d_srec = nullptr;
   int *d_sinfo = nullptr;
   int pslot_chunks = 0, pslot_chunks_nounary = 0;
@@ -96,8 +97,8 @@ struct hbp_graph {
     cudaSetDevice(device);
     // the layout, message buffers and layout scratch live in d_block (pool)
     if (d_block) cudaFreeAsync(d_block, own_stream ? own_stream : stream);
-    for (void *p : {(void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace,
-                    (void *)d_srec, (void *)d_sinfo, (void *)d_ftov_alt, (void *)d_p0_alt})
+    if (d_pslot_block) cudaFreeAsync(d_pslot_block, own_stream ? own_stream : stream);
+    for (void *p : {(void *)d_ev, d_rank, d_ev_list, d_ctrl, (void *)d_hist, (void *)d_trace})
       if (p) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);

@@ -577,8 +577,14 @@ struct PslotClasses {
   int rank[2][kClassMax + 1];   // (kind, degree) -> class rank, -1: empty
   int start[2 * kClassMax + 2]; // first sorted position of each class
   int chunk[2 * kClassMax + 2]; // first chunk of each class
+  int node[2 * kClassMax + 2];  // first internal factor of each class
+  int count[2 * kClassMax + 2];
   int deg[2 * kClassMax + 2], kind[2 * kClassMax + 2];
 };
+
+__device__ __forceinline__ int pslot_kind(int f, int f_or_light, int f_heavy, int f_or_heavy) {
+  return ((f >= f_or_light && f < f_heavy) || f >= f_or_heavy) ? 1 : 0;
+}
 
 __global__ void k_pslot_keys(const int *frow, const int *vtof_twin, const int2 *vslot, int F,
                              int f_or_light, int f_heavy, int f_or_heavy, PslotClasses C,
@@ -586,21 +592,36 @@ __global__ void k_pslot_keys(const int *frow, const int *vtof_twin, const int2 *
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const int r = frow[f], d = frow[f + 1] - r;
-  const int kind = ((f >= f_or_light && f < f_heavy) || f >= f_or_heavy) ? 1 : 0;
+  const int kind = pslot_kind(f, f_or_light, f_heavy, f_or_heavy);
   int mx = 0;
   for (int k = 0; k < d; ++k) mx = max(mx, (int)((unsigned)vslot[vtof_twin[r + k]].y >> 16));
   key[f] = (unsigned)C.rank[kind][d] << 8 | (unsigned)(255 - min(mx, 255));
   val[f] = f;
 }
 
+// one thread per factor: its lane records, and the chunk's unused lanes
+// (zero = invalid) by the chunk's first / the class's last factor. perm ==
+// nullptr: the factors of a class in internal order (thread i = factor i)
 __global__ void k_pslot_records(const unsigned *key, const int *perm, const int *frow,
-                                const int *vtof_twin, const int2 *vslot, int F, PslotClasses C,
-                                int4 *srec, int *sinfo) {
+                                const int *vtof_twin, const int2 *vslot, int F, int f_or_light,
+                                int f_heavy, int f_or_heavy, PslotClasses C, int4 *srec,
+                                int *sinfo) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= F) return;
-  const int c = (int)(key[i] >> 8), f = perm[i];
-  const int d = C.deg[c], per = 32 / d, pos = i - C.start[c];
+  int c, f, pos;
+  if (perm) {
+    c = (int)(key[i] >> 8);
+    f = perm[i];
+    pos = i - C.start[c];
+  } else {
+    f = i;
+    const int kind = pslot_kind(f, f_or_light, f_heavy, f_or_heavy);
+    c = C.rank[kind][frow[f + 1] - frow[f]];
+    pos = f - C.node[c];
+  }
+  const int d = C.deg[c], per = 32 / d;
   const int chunk = C.chunk[c] + pos / per, g = pos % per;
+  int4 *lanes = srec + (size_t)chunk * 32;
   const int r = frow[f];
   int mx = 0;
   for (int k = 0; k < d; ++k) {
@@ -608,9 +629,14 @@ __global__ void k_pslot_records(const unsigned *key, const int *perm, const int 
     const int2 w = vslot[q];
     const int j = w.y & 0xffff, dv = (int)((unsigned)w.y >> 16);
     mx = max(mx, dv);
-    srec[(size_t)chunk * 32 + g * d + k] = make_int4(q - j, w.x, f, dv | j << 8 | k << 16 | 1 << 24);
+    lanes[g * d + k] = make_int4(q - j, w.x, f, dv | j << 8 | k << 16 | 1 << 24);
   }
-  // the chunk's first factor has its longest variable row (descending order)
+  const int4 none = make_int4(0, 0, 0, 0);
+  if (g == 0)
+    for (int l = per * d; l < 32; ++l) lanes[l] = none;
+  if (pos == C.count[c] - 1)
+    for (int l = (g + 1) * d; l < per * d; ++l) lanes[l] = none;
+  // sorted: the chunk's first factor has its longest variable row
   if (g == 0) sinfo[chunk] = d | C.kind[c] << 8 | mx << 16;
 }
 }  // namespace
@@ -630,6 +656,8 @@ hbp_status build_pslot_device(hbp_graph *g) {
     C.rank[k][d] = c;
     C.start[c] = pos;
     C.chunk[c] = chunks;
+    C.node[c] = L.fcls_node[k][d];
+    C.count[c] = cnt;
     C.deg[c] = d;
     C.kind[c] = k;
     pos += cnt;
@@ -641,30 +669,54 @@ hbp_status build_pslot_device(hbp_graph *g) {
   for (int k = 0; k < 2; ++k) add(1, k);
   g->pslot_chunks = chunks;
   g->pslot_chunks_nounary = chunks_nounary;
-  HBP_CUDA(cudaMalloc(&g->d_srec, (size_t)std::max(1, chunks) * 32 * sizeof(int4)));
-  HBP_CUDA(cudaMalloc(&g->d_sinfo, (size_t)std::max(1, chunks) * sizeof(int)));
-  // + 2 messages: lbp_pslot reads rows as 32-byte aligned pairs (d_ftov is
-  // followed by further arena allocations, which the last pair may touch)
-  HBP_CUDA(cudaMalloc(&g->d_ftov_alt, ((size_t)L.E + 2) * sizeof(double2)));
-  HBP_CUDA(cudaMalloc(&g->d_p0_alt, (size_t)std::max(1, L.V) * sizeof(double)));
-  HBP_CUDA(cudaMemsetAsync(g->d_srec, 0, (size_t)std::max(1, chunks) * 32 * sizeof(int4), s));
-  size_t tmp = 0;
-  HBP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (unsigned *)nullptr, (unsigned *)nullptr,
-                                           (int *)nullptr, (int *)nullptr, F, 0, 16, s));
-  char *buf = nullptr;
-  const size_t fb = ((size_t)std::max(1, F) * 4 + 255) & ~(size_t)255;
-  HBP_CUDA(cudaMallocAsync((void **)&buf, 4 * fb + tmp, s));
-  unsigned *key = (unsigned *)buf, *key_s = (unsigned *)(buf + fb);
-  int *val = (int *)(buf + 2 * fb), *val_s = (int *)(buf + 3 * fb);
+  // one stream-ordered allocation from the graph's pool (a fresh graph's
+  // run() pays no cudaMalloc / cudaFree synchronisation for it). The second
+  // ftov buffer has 2 messages of slack: lbp_pslot reads rows as 32-byte
+  // aligned pairs (d_ftov is followed by further arena allocations, which
+  // its last pair may touch)
+  {
+    const size_t nch = (size_t)std::max(1, chunks);
+    const size_t b_rec = nch * 32 * sizeof(int4), b_inf = (nch * 4 + 255) & ~(size_t)255,
+                 b_ft = (((size_t)L.E + 2) * sizeof(double2) + 255) & ~(size_t)255,
+                 b_p0 = (size_t)std::max(1, L.V) * sizeof(double);
+    char *blk = nullptr;
+    HBP_CUDA(cudaMallocAsync((void **)&blk, b_rec + b_inf + b_ft + b_p0, s));
+    g->d_pslot_block = blk;
+    g->d_srec = (int4 *)blk;
+    g->d_sinfo = (int *)(blk + b_rec);
+    g->d_ftov_alt = (double2 *)(blk + b_rec + b_inf);
+    g->d_p0_alt = (double *)(blk + b_rec + b_inf + b_ft);
+  }
   const unsigned nb = (unsigned)((F + 255) / 256);
-  k_pslot_keys<<<nb, 256, 0, s>>>(g->d_frow, g->d_vtof_twin, g->d_vslot, F, L.f_or_light, L.f_heavy,
-                                  L.f_or_heavy, C, key, val);
-  HBP_CUDA(cub::DeviceRadixSort::SortPairs(buf + 4 * fb, tmp, key, key_s, val, val_s, F, 0, 16, s));
-  k_pslot_records<<<nb, 256, 0, s>>>(key_s, val_s, g->d_frow, g->d_vtof_twin, g->d_vslot, F, C,
-                                     g->d_srec, g->d_sinfo);
+  // each class's factors ordered by their longest variable row (a CUB sort:
+  // a chunk's lanes then load rows of similar length, so fewer of its pair
+  // loads are live -- C4-PARALL 0.271 against 0.295 ms in the internal
+  // order, which HBP_PSLOT_SORT=0 keeps for A/B)
+  const char *se = getenv("HBP_PSLOT_SORT");
+  char *buf = nullptr;
+  if (!(se && atoi(se) == 0)) {
+    size_t tmp = 0;
+    HBP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (unsigned *)nullptr, (unsigned *)nullptr,
+                                             (int *)nullptr, (int *)nullptr, F, 0, 16, s));
+    const size_t fb = ((size_t)std::max(1, F) * 4 + 255) & ~(size_t)255;
+    HBP_CUDA(cudaMallocAsync((void **)&buf, 4 * fb + tmp, s));
+    unsigned *key = (unsigned *)buf, *key_s = (unsigned *)(buf + fb);
+    int *val = (int *)(buf + 2 * fb), *val_s = (int *)(buf + 3 * fb);
+    k_pslot_keys<<<nb, 256, 0, s>>>(g->d_frow, g->d_vtof_twin, g->d_vslot, F, L.f_or_light,
+                                    L.f_heavy, L.f_or_heavy, C, key, val);
+    HBP_CUDA(cub::DeviceRadixSort::SortPairs(buf + 4 * fb, tmp, key, key_s, val, val_s, F, 0, 16, s));
+    k_pslot_records<<<nb, 256, 0, s>>>(key_s, val_s, g->d_frow, g->d_vtof_twin, g->d_vslot, F,
+                                       L.f_or_light, L.f_heavy, L.f_or_heavy, C, g->d_srec,
+                                       g->d_sinfo);
+    add_last_launches(3);
+  } else {
+    k_pslot_records<<<nb, 256, 0, s>>>(nullptr, nullptr, g->d_frow, g->d_vtof_twin, g->d_vslot, F,
+                                       L.f_or_light, L.f_heavy, L.f_or_heavy, C, g->d_srec,
+                                       g->d_sinfo);
+    add_last_launches(1);
+  }
   HBP_CUDA(cudaGetLastError());
-  HBP_CUDA(cudaFreeAsync(buf, s));
-  add_last_launches(3);
+  if (buf) HBP_CUDA(cudaFreeAsync(buf, s));
   return HBP_OK;
 }
 }  // namespace hbp
