@@ -179,9 +179,9 @@ hbp_status hbp_graph_set_evidence(hbp_graph *g, int32_t n, const int32_t *var, c
 
 /* Rank a selection (ascending variable ids, e.g. the alarms) by the last run's
  * P1, skipping variables with evidence: rank_alarms order (ranking.py:83-91),
- * computed on the device: any selection size (candidates stream through a
- * 16,384-entry shared-memory window), topk < 16,384. ranked [topk] (-1
- * padded), p1 [topk] or NULL. */
+ * computed on the device: any selection size (a radix select of the k-th key,
+ * then a sort of the k selected), topk < 16,384. ranked [topk] (-1 padded),
+ * p1 [topk] or NULL. */
 hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *select, int32_t topk,
                           int32_t *ranked, double *p1);
 

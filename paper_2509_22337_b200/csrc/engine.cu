@@ -1387,14 +1387,15 @@ __global__ void __launch_bounds__(256) uf_attr_kernel(const __grid_constant__ KP
 // Alarm ranking of the last run (ranking.py:83-91): the selection's unlabeled
 // variables (no evidence code) by descending P1, ties by ascending position
 // in the id-sorted selection. One CTA. topk == 1: an argmax reduction;
-// otherwise a bitonic sort of (~bits(P1), position) in shared memory.
+// otherwise topk_select (radix select of the k-th key, then a sort of k).
 __global__ void __launch_bounds__(1024) rank_kernel(const double2 *marg, const unsigned char *ev,
                                                     const int *vinv, const int *sel, int nsel,
-                                                    int npow2, int topk, int *ranked,
+                                                    int npow2, int kpow2, int topk, int *ranked,
                                                     double *p1_out) {
   extern __shared__ unsigned char smem[];
-  unsigned long long *key = (unsigned long long *)smem;
-  int *pos = (int *)(key + npow2);
+  unsigned long long *cache = (unsigned long long *)smem;
+  unsigned long long *key = cache + npow2;
+  int *pos = (int *)(key + kpow2);
   auto key_of = [&](int i) -> unsigned long long {
     if (i >= nsel) return ~0ull;
     const int v = sel[i];
@@ -1446,9 +1447,9 @@ __global__ void __launch_bounds__(1024) rank_kernel(const double2 *marg, const u
     }
     return;
   }
-  topk_stream(key_of, nsel, topk, npow2, key, pos);
+  topk_select(key_of, nsel, topk, npow2, kpow2, cache, key, pos);
   for (int i = threadIdx.x; i < topk; i += blockDim.x) {
-    const bool ok = i < nsel && i < npow2 && key[i] != ~0ull;
+    const bool ok = key[i] != ~0ull;
     ranked[i] = ok ? sel[pos[i]] : -1;
     if (p1_out) p1_out[i] = ok ? marg[sel[pos[i]]].y : 0.0;
   }
@@ -2480,7 +2481,7 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
       hbp::set_error("selection must be ascending variable ids");
       return HBP_EINVAL;
     }
-  // the shared-memory window of the streaming top-k (lbp_kernels.cuh)
+  // the shared-memory key cache of the top-k select (lbp_kernels.cuh)
   int npow2 = 2;
   while (npow2 < num_select && npow2 < hbp::dev::kRankCap) npow2 <<= 1;
   if (topk > 1 && topk >= hbp::dev::kRankCap) {
@@ -2502,12 +2503,17 @@ hbp_status hbp_graph_rank(hbp_graph *g, int32_t num_select, const int32_t *selec
   double *d_p1 = (double *)(((uintptr_t)(d_out + topk) + 15) & ~(uintptr_t)15);
   if (num_select)
     HBP_CUDA(cudaMemcpyAsync(d_sel, select, (size_t)num_select * 4, cudaMemcpyHostToDevice, s));
-  const size_t smem = topk == 1 ? 0 : (size_t)npow2 * 12;
+  int kpow2 = 2;
+  while (kpow2 < topk) kpow2 <<= 1;
+  // the key cache shrinks when a large k takes the shared memory (it is
+  // optional: without it the select recomputes the keys per pass)
+  while (npow2 > 2 && (size_t)npow2 * 8 + (size_t)kpow2 * 12 > (size_t)200 * 1024) npow2 >>= 1;
+  const size_t smem = topk == 1 ? 0 : (size_t)npow2 * 8 + (size_t)kpow2 * 12;
   if (smem > 48 * 1024)
     HBP_CUDA(cudaFuncSetAttribute(hbp::rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   hbp::rank_kernel<<<1, 1024, smem, s>>>(g->d_marg, g->has_ev ? g->d_ev : nullptr, g->d_vinv,
-                                         d_sel, num_select, npow2, topk, d_out, d_p1);
+                                         d_sel, num_select, npow2, kpow2, topk, d_out, d_p1);
   HBP_CUDA(cudaGetLastError());
   HBP_CUDA(cudaMemcpyAsync(ranked, d_out, (size_t)topk * 4, cudaMemcpyDeviceToHost, s));
   if (p1) HBP_CUDA(cudaMemcpyAsync(p1, d_p1, (size_t)topk * 8, cudaMemcpyDeviceToHost, s));

@@ -36,6 +36,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <string>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -1151,11 +1152,12 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *
                                                            const unsigned char *ev_alt,
                                                            const int *res_pos,
                                                            const int *vinv, const int *sel,
-                                                           int nsel, int npow2, int V,
+                                                           int nsel, int npow2, int kpow2, int V,
                                                            int set_base, int topk, int *ranked) {
   extern __shared__ unsigned char smem[];
-  unsigned long long *key = (unsigned long long *)smem;
-  int *pos = (int *)(key + npow2);
+  unsigned long long *cache = (unsigned long long *)smem;
+  unsigned long long *key = cache + npow2;
+  int *pos = (int *)(key + kpow2);
   const int s = blockIdx.x;
   auto key_of = [&](int i) -> unsigned long long {
     int par;
@@ -1163,10 +1165,9 @@ __global__ void __launch_bounds__(1024) sweep_rank_kernel(const T *p0, const T *
     if ((par ? ev_alt : ev)[at] != 0) return ~0ull;
     return rank_key(sub(1.0, (double)(par ? p0_alt : p0)[at]));
   };
-  topk_stream(key_of, nsel, topk, npow2, key, pos);
+  topk_select(key_of, nsel, topk, npow2, kpow2, cache, key, pos);
   for (int i = threadIdx.x; i < topk; i += blockDim.x)
-    ranked[(size_t)(set_base + s) * topk + i] =
-        (i < nsel && i < npow2 && key[i] != ~0ull) ? sel[pos[i]] : -1;
+    ranked[(size_t)(set_base + s) * topk + i] = key[i] != ~0ull ? sel[pos[i]] : -1;
 }
 
 }  // namespace hbp
@@ -1651,14 +1652,18 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     if (out->ranked && out->topk > 0) {
       int *dst = rk_dev ? out->ranked : stage_rk;
       const int bbase = rk_dev ? base : 0;
-      const size_t smem = (size_t)std::max(npow2, 2) * 12;
+      int kpow2 = 2;
+      while (kpow2 < out->topk) kpow2 <<= 1;
+      int cache = std::max(npow2, 2);  // optional key cache: shrinks for a large k
+      while (cache > 2 && (size_t)cache * 8 + (size_t)kpow2 * 12 > (size_t)200 * 1024) cache >>= 1;
+      const size_t smem = (size_t)cache * 8 + (size_t)kpow2 * 12;
       if (smem > 48 * 1024) {
         HBP_CUDA(cudaFuncSetAttribute(hbp::sweep_rank_kernel<double>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       }
       hbp::sweep_rank_kernel<double><<<ns, 1024, smem, st>>>(
             sw->d_p0, sw->d_p0_alt, sw->d_ev, sw->d_ev_alt, d_rpos, sw->d_vinv, d_sel, nsel,
-            std::max(npow2, 2), L.V, bbase, out->topk, dst);
+            cache, kpow2, L.V, bbase, out->topk, dst);
       ++launches;
       if (!rk_dev)
         HBP_CUDA(cudaMemcpyAsync(out->ranked + (size_t)base * out->topk, stage_rk,
@@ -1683,6 +1688,12 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
       HBP_CUDA(cudaEventElapsedTime(&b, sw->k0, sw->k1));
       dev_ms += a;
       ker_ms += b;
+      if (getenv("HBP_SWEEP_TIMING")) {  // probe: set-up / kernel / outputs
+        float c = 0, d = 0;
+        cudaEventElapsedTime(&c, sw->e0, sw->k0);
+        cudaEventElapsedTime(&d, sw->k1, sw->e1);
+        fprintf(stderr, "sweep pass: setup %.3f ms kernel %.3f ms outputs %.3f ms\n", c, b, d);
+      }
     }
     compactions += (int)h_misc[2];
     int maxit_seen = 0;
