@@ -1101,6 +1101,13 @@ __global__ void sweep_evidence_kernel(unsigned char *ev, const int *vinv, const 
 // 32 x 32 tiles: coalesced reads along sets, coalesced writes along variables
 // res_pos[s] = slot | parity << 30: where set s's final marginals are (the
 // staged kernel may have moved the set; parity 1 = the alternate buffers)
+__global__ void sweep_ident_kernel(int *slot2set, int *res_pos, int S, int ns) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S) return;
+  slot2set[i] = i < ns ? i : -1;
+  res_pos[i] = i;
+}
+
 __device__ __forceinline__ size_t final_pos(const int *res_pos, int s, int vi, int V, int &parity) {
   const int rp = res_pos[s];
   parity = (rp >> 30) & 1;
@@ -1603,14 +1610,9 @@ hbp_status hbp_sweep_run(hbp_sweep *sw, const hbp_options *opt, const hbp_eviden
     HBP_CUDA(cudaMemsetAsync(d_tf, 0, nit * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_ri, 0, (size_t)S * 4, st));
     HBP_CUDA(cudaMemsetAsync(d_claim, 0, (size_t)cap / 32 * 8 + 8, st));
-    {  // slot s holds set s (pass-relative); res_pos defaults to the same slot
-      std::vector<int> ident((size_t)S);
-      for (int i = 0; i < S; ++i) ident[i] = i < ns ? i : -1;
-      HBP_CUDA(cudaMemcpyAsync(d_s2s, ident.data(), (size_t)S * 4, cudaMemcpyHostToDevice, st));
-      for (int i = ns; i < S; ++i) ident[i] = i;
-      HBP_CUDA(cudaMemcpyAsync(d_rpos, ident.data(), (size_t)S * 4, cudaMemcpyHostToDevice, st));
-      HBP_CUDA(cudaStreamSynchronize(st));  // ident is a stack buffer
-    }
+    // slot s holds set s (pass-relative); res_pos defaults to the same slot
+    hbp::sweep_ident_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(d_s2s, d_rpos, S, ns);
+    ++launches;
     HBP_CUDA(cudaMemsetAsync(d_rs, 0, (size_t)S * 4, st));
     const unsigned misc[3] = {(unsigned)(S - ns), 0u, 0u};
     HBP_CUDA(cudaMemcpyAsync(d_nstop, misc, 12, cudaMemcpyHostToDevice, st));

@@ -230,23 +230,33 @@ def run_many(graph: FactorGraph, evidence_sets: Iterable, strategy: Optional[Str
         if st == _native.HBP_EINVAL:
             raise ValueError(f"hbp_sweep_run: {_native.last_error()}")
         raise RuntimeError(f"hbp_sweep_run: {_native.last_error()}")
-    its = np.array([res[j].iterations for j in range(n)], dtype=np.int32)
-    errors: list[Optional[UnderflowError]] = []
-    for j in range(n):
-        k = res[j].underflow_kind
-        errors.append(None if k == 0 else _underflow_error(k, int(res[j].underflow_index),
-                                                            res[j].underflow_iteration))
+    # the per-set records as one numpy view (no per-set ctypes access)
+    rec = np.frombuffer(res, dtype=_SET_RESULT, count=max(1, n))[:n]
+    its = rec["iterations"].astype(np.int32)
+    uk = rec["underflow_kind"]
+    errors: list[Optional[UnderflowError]] = [None] * n
+    for j in np.flatnonzero(uk):
+        errors[j] = _underflow_error(int(uk[j]), int(rec["underflow_index"][j]),
+                                     int(rec["underflow_iteration"][j]))
     base_upd = dg.parall_updates(graph)
     return SweepResult(
         iterations=its,
-        converged=np.array([bool(res[j].converged) for j in range(n)]),
-        last_delta=np.array([res[j].last_delta for j in range(n)], dtype=np.float64),
+        converged=rec["converged"] != 0,
+        last_delta=rec["last_delta"].astype(np.float64),
         deltas=None if dl is None else [dl[j, :its[j]].tolist() for j in range(n)],
         marginals=mg, p1_select=p1, ranked=rk, select=sel, errors=errors,
         updates_per_iteration=base_upd + np.diff(off),
         device_ms=float(outs.device_ms), kernel_ms=float(outs.kernel_ms),
         launches=int(outs.launches), passes=int(outs.passes),
         compactions=int(outs.compactions))
+
+
+# numpy layout of _native.SetResult (hbp_set_result)
+_SET_RESULT = np.dtype({"names": [f[0] for f in _native.SetResult._fields_],
+                        "formats": [np.int32, np.int32, np.float64, np.int32, np.int32, np.int64],
+                        "offsets": [getattr(_native.SetResult, f[0]).offset
+                                    for f in _native.SetResult._fields_],
+                        "itemsize": C.sizeof(_native.SetResult)})
 
 
 def _run_materialised(graph, off, var, val, strategy, options, want_marg, want_deltas, sel, topk):
