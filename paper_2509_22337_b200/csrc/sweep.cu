@@ -785,7 +785,11 @@ constexpr int kMaxCompact = 1024;  // passes up to this many slots may compact
 //    control data is indexed by set, not slot, and res_pos records where each
 //    set's final marginals are.
 template <bool NORM, int NS, typename T>
+#ifdef HBP_WS_MAXNREG
+__global__ void __maxnreg__(HBP_WS_MAXNREG)
+#else
 __global__ void __launch_bounds__(WsCfg<NS>::threads, WsCfg<NS>::min_blocks)
+#endif
     sweep_ws(const __grid_constant__ SweepParams P) {
   using T2 = typename Ar<T>::T2;
   constexpr int kWsConsumers = WsCfg<NS>::consumers;
