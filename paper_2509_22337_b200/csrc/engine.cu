@@ -1157,7 +1157,14 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
   if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_dmax = 0, s_stop = 0;
   auto barrier = [&](auto pre) {
-    if (multi) {
+    if (P.csize > 1) {
+      // the whole grid is one thread-block cluster (small graphs): the
+      // hardware cluster barrier, release / acquire at cluster scope, orders
+      // the global-memory messages like the counter barrier does
+      __syncthreads();
+      if (threadIdx.x == 0) pre();
+      asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    } else if (multi) {
       sync_point_hooked(C, sy, (unsigned)G, true, true, pre, NoHookP{});
     } else {
       __syncthreads();
@@ -1831,6 +1838,28 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
     p->grid = (int)std::max<int64_t>(1, std::min<int64_t>((g->pslot_chunks + 7) / 8, coop));
   if (const char *ge = getenv("HBP_GRID"))  // A/B: force the CTA count
     p->grid = std::max(1, std::min(atoi(ge), coop));
+  // lbp_pslot on at most 8 CTAs: the grid is launched as ONE thread-block
+  // cluster and the iteration barrier is the hardware cluster barrier instead
+  // of the global-memory counter (HBP_PSLOT_CLUSTER=0: the counter, A/B)
+  if (p->pslot && p->grid > 1 && p->grid <= 8) {
+    const char *pc = getenv("HBP_PSLOT_CLUSTER");
+    if (!(pc && atoi(pc) == 0)) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = p->grid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(p->grid);
+      cfg.blockDim = dim3(p->threads);
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, p->kernel, &cfg) == cudaSuccess && nclusters >= 1)
+        p->csize = p->grid;
+      cudaGetLastError();
+    }
+  }
   p->grid = std::max(p->csize, p->grid / p->csize * p->csize);
   HBP_CUDA(cudaStreamSynchronize(s));
   *out = p.release();

@@ -627,6 +627,48 @@ def test_pslot_bitwise_identical_to_two_phase(monkeypatch):
     P.engine.clear_device_cache()
 
 
+def test_pslot_cluster_barrier_bitwise(monkeypatch):
+    """lbp_pslot on at most 8 CTAs runs as one thread-block cluster whose
+    iteration barrier is the hardware cluster barrier; HBP_PSLOT_CLUSTER=0
+    keeps the global-memory counter barrier. Forced grids of 2..8 CTAs
+    (HBP_GRID) and C1 weblech's own grid: same bits and iterations either
+    way, and the same as the two-phase kernel."""
+    rng = np.random.default_rng(4242)
+    graphs = [W.graph("weblech")[0]] + [
+        random_graph(rng, max_vars=60, max_factors=60, max_body=7) for _ in range(8)]
+    for i, g in enumerate(graphs):
+        sched = Strategy.parall().compile(g)
+        for grid in ((None,) if i == 0 else (2, 5, 8)):
+            opts = EngineOptions(int(rng.integers(1, 120)), 1e-9, record_history=(i % 2 == 0))
+            out = []
+            for env in ({}, {"HBP_PSLOT_CLUSTER": "0"}, {"HBP_PSLOT": "0"}):
+                for k in ("HBP_PSLOT_CLUSTER", "HBP_PSLOT", "HBP_GRID"):
+                    monkeypatch.delenv(k, raising=False)
+                for k, v in env.items():
+                    monkeypatch.setenv(k, v)
+                if grid is not None:
+                    monkeypatch.setenv("HBP_GRID", str(grid))
+                P.engine.clear_device_cache()
+                try:
+                    out.append(P.run(g, sched, opts))
+                except UnderflowError as e:
+                    out.append((e.kind, e.iteration, e.index))
+            for b in out[1:]:
+                a = out[0]
+                if isinstance(a, tuple) or isinstance(b, tuple):
+                    assert a == b, (i, grid)
+                    continue
+                assert a.iterations == b.iterations and a.converged == b.converged, (i, grid)
+                assert a.marginals.tobytes() == b.marginals.tobytes(), (i, grid)
+                assert np.asarray(a.deltas).tobytes() == np.asarray(b.deltas).tobytes(), (i, grid)
+                assert (a.history is None) == (b.history is None), (i, grid)
+                for x, y in zip(a.history or [], b.history or []):
+                    assert np.asarray(x).tobytes() == np.asarray(y).tobytes(), (i, grid)
+    for k in ("HBP_PSLOT_CLUSTER", "HBP_PSLOT", "HBP_GRID"):
+        monkeypatch.delenv(k, raising=False)
+    P.engine.clear_device_cache()
+
+
 def test_fp32_run_within_1e5_of_fp64():
     """run(..., EngineOptions(precision="fp32")): fp32
     message storage, fp64 arithmetic -- marginals within the north star's
