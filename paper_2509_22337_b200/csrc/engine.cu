@@ -535,6 +535,9 @@ __device__ __forceinline__ void run_small(const KParams &P, const Phase *cache, 
       }
     }
     unsigned ufkey = 0;
+#ifdef HBP_TRACE_SMALL
+    trace_mark(P, it, p, 0);
+#endif
     if (FUSED && type == 2) {
       for (int i = start; i < n; i += stride) {
         const int4 *lr = P.fitems + 2 * (size_t)(b + i);
@@ -554,6 +557,9 @@ __device__ __forceinline__ void run_small(const KParams &P, const Phase *cache, 
       }
     }
     flush_underflow(P, it, p, ufkey);
+#ifdef HBP_TRACE_SMALL
+    trace_mark(P, it, p, 1);
+#endif
     if (nxt >= 0) {
       const void *x = ntype == 1 ? (const void *)(P.fslot + nxt) : (const void *)(P.vslot + nxt);
       const void *y = ntype == 1 ? (const void *)(P.vtof_twin + nxt) : (const void *)(P.ftov_twin + nxt);
