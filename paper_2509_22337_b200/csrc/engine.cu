@@ -1162,8 +1162,14 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_pslot(const __grid_constant__ 
   __shared__ int s_stop;
   if (threadIdx.x < 2) s_claim[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_dmax = 0, s_stop = 0;
+  // the cluster barrier only when the launch really is one cluster of the
+  // whole grid (a launch without the cluster attribute -- e.g. a profiler's
+  // kernel replay -- takes the counter barrier instead of racing)
+  unsigned ncl;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+  const bool one_cluster = P.csize > 1 && ncl == gridDim.x;
   auto barrier = [&](auto pre) {
-    if (P.csize > 1) {
+    if (one_cluster) {
       // the whole grid is one thread-block cluster (small graphs): the
       // hardware cluster barrier, release / acquire at cluster scope, orders
       // the global-memory messages like the counter barrier does
