@@ -61,6 +61,14 @@ constexpr int kFusedThreads = HBP_FUSED_THREADS;  // plans with fused levels
 #define HBP_PSLOT_THREADS 896
 #endif
 constexpr int kPslotThreads = HBP_PSLOT_THREADS;
+// slot items (levelled phases, the single-pass API): rows loaded branch-free
+// in their length and the factor kind selected by operands, so one warp's
+// lanes share one round trip -- measured on B200: C2 8.92 -> 5.44 ms, C3
+// 8.70 -> 7.33 ms (HBP_ITEM_PRED=0: the per-length / per-kind switch, A/B)
+#ifndef HBP_ITEM_PRED
+#define HBP_ITEM_PRED 1
+#endif
+constexpr int kItemRow = 6;
 #ifndef HBP_PSLOT_ROW
 #define HBP_PSLOT_ROW 4
 #endif
@@ -245,12 +253,20 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
         a0 = mul(a0, x[i].x);
         a1 = mul(a1, x[i].y);
       }
-    for (int i = kFuseRow; i < dv; ++i)
-      if (i != j) {
-        const double2 y = P.ftov[rc.x + i];
-        a0 = mul(a0, y.x);
-        a1 = mul(a1, y.y);
-      }
+    // the rest of a long row in groups of four loads issued together (one
+    // round trip per group instead of one per slot), same left-to-right order
+    for (int b = kFuseRow; b < dv; b += 4) {
+      double2 y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        y[u] = b + u < dv ? P.ftov[rc.x + b + u] : make_double2(1.0, 1.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b + u < dv && b + u != j) {
+          a0 = mul(a0, y[u].x);
+          a1 = mul(a1, y[u].y);
+        }
+    }
     if (code && it > 1) apply_clamp(code, a0, a1);
     put_message_ref(P, P.vtof + h.y + k, a0, a1, phase, 0, h.y + k, ufkey);
     m = make_double2(a0, a1);
