@@ -69,6 +69,12 @@ constexpr int kPslotThreads = HBP_PSLOT_THREADS;
 #define HBP_ITEM_PRED 1
 #endif
 constexpr int kItemRow = 6;
+// fused lanes: the factor kind selects operands instead of branching (no
+// divergence between a warp's AND and OR factors; the same operations):
+// C4-SEQFIX 18.14 -> 17.62 ms (HBP_FUSED_SEL=0: the branches, A/B)
+#ifndef HBP_FUSED_SEL
+#define HBP_FUSED_SEL 1
+#endif
 #ifndef HBP_PSLOT_ROW
 #define HBP_PSLOT_ROW 4
 #endif
@@ -228,6 +234,28 @@ constexpr int kFuseRow = 6;
 // tmask | smask << 12}, rc = the slot's record {variable row start,
 // (variable degree << 16) | own index, internal variable, ftov slot}.
 // Called by all 32 lanes of a warp.
+// factor output of one slot with the kind a run-time flag: the operands of
+// head_message / body_message (lbp_kernels.cuh) selected, not the code
+// duplicated -- the same operations on the same values, so the same bits.
+// head: diff = (a - b) prod2, o1 = b prod1 + diff, o0 = (1 - b) prod1 - diff
+// with (a, b) = (p1, p2) for AND, (p2, p1) for OR; body: diff = (a - b) prod2,
+// s = prod1 + diff, with (a, b) = (p2, p1) and (o0, o1) = (prod1, s) for
+// AND, (p1, p2) and (s, prod1) for OR.
+__device__ __forceinline__ void factor_out(bool is_or, bool head, double p1, double p2,
+                                           double prod1, double prod2, double &o0, double &o1) {
+  const bool first = is_or != head;  // a = p1
+  const double a = first ? p1 : p2, b = first ? p2 : p1;
+  const double diff = mul(sub(a, b), prod2);
+  if (head) {
+    o1 = add(mul(b, prod1), diff);
+    o0 = sub(mul(sub(1.0, b), prod1), diff);
+  } else {
+    const double s = add(prod1, diff);
+    o0 = is_or ? s : prod1;
+    o1 = is_or ? prod1 : s;
+  }
+}
+
 __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, int it, int phase,
                                            unsigned &ufkey) {
   const int d = h.z & 0xff, k = (h.z >> 8) & 0xff, base = h.z >> 16;
@@ -279,12 +307,21 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
     const double x1 = __shfl_sync(0xffffffffu, m.y, base + i);
     if (out && i < d && i != k) {  // left to right, the own slot skipped
       double f1, f2;
+#if HBP_FUSED_SEL
+      // the kind selects operands (head_slot_terms with c = p1 for OR, p2 for AND)
+      if (i == 0) {
+        const double c = is_or ? pp.x : pp.y;
+        f1 = add(mul(sub(1.0, c), x0), mul(c, x1));
+        f2 = sub(x0, x1);
+      } else {
+#else
       if (i == 0) {
         if (is_or)
           head_slot_terms<1>(pp.x, pp.y, x0, x1, f1, f2);
         else
           head_slot_terms<0>(pp.x, pp.y, x0, x1, f1, f2);
       } else {
+#endif
         f1 = add(x0, x1);
         f2 = is_or ? x0 : x1;
       }
@@ -294,6 +331,9 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
   }
   if (out) {
     double o0, o1;
+#if HBP_FUSED_SEL
+    factor_out(is_or, k == 0, pp.x, pp.y, b1, b2, o0, o1);
+#else
     if (k == 0) {
       if (is_or)
         head_message<1>(pp.x, pp.y, b1, b2, o0, o1);
@@ -305,6 +345,7 @@ __device__ __forceinline__ void fused_lane(const KParams &P, int4 h, int4 rc, in
       else
         body_message<0>(pp.x, pp.y, b1, b2, o0, o1);
     }
+#endif
     put_message(P, P.ftov + rc.w, o0, o1, phase, 1, rc.w, ufkey);
   }
 }
@@ -1034,28 +1075,6 @@ __global__ void __launch_bounds__(THREADS, 1) lbp_parall(const __grid_constant__
 // safe: the marginals of it-2 are still intact when it is taken.
 // Underflow only stops the run: the host replays the schedule with the
 // two-phase kernel, which attributes it exactly (bitwise the same run).
-
-// factor output of one slot with the kind a run-time flag: the operands of
-// head_message / body_message (lbp_kernels.cuh) selected, not the code
-// duplicated -- the same operations on the same values, so the same bits.
-// head: diff = (a - b) prod2, o1 = b prod1 + diff, o0 = (1 - b) prod1 - diff
-// with (a, b) = (p1, p2) for AND, (p2, p1) for OR; body: diff = (a - b) prod2,
-// s = prod1 + diff, with (a, b) = (p2, p1) and (o0, o1) = (prod1, s) for
-// AND, (p1, p2) and (s, prod1) for OR.
-__device__ __forceinline__ void factor_out(bool is_or, bool head, double p1, double p2,
-                                           double prod1, double prod2, double &o0, double &o1) {
-  const bool first = is_or != head;  // a = p1
-  const double a = first ? p1 : p2, b = first ? p2 : p1;
-  const double diff = mul(sub(a, b), prod2);
-  if (head) {
-    o1 = add(mul(b, prod1), diff);
-    o0 = sub(mul(sub(1.0, b), prod1), diff);
-  } else {
-    const double s = add(prod1, diff);
-    o0 = is_or ? s : prod1;
-    o1 = is_or ? prod1 : s;
-  }
-}
 
 // one chunk: info = degree | kind << 8 | longest row << 16 (warp-uniform),
 // rc = the lane's record. One instance for every degree: the kernel's speed
