@@ -131,6 +131,10 @@ for c in ("C4-PARALL", "C1", "C4-SEQFIX", "C2", "C3"):
     lines.append(f"| {c} | `{kname}` | {s['duration_ms']:.3f} | {l2b / 1e9:.3f} GB | {s['l1_ld_sectors'] / 1e6:.1f} M / "
                  f"{s['l1_st_sectors'] / 1e6:.1f} M | {s['dram_bytes'] / 1e6:.1f} MB | {s['inst'] / 1e6:.1f} M | "
                  f"{s['issue_active_pct']:.1f} % | {s['regs']:.0f} | {s['stalls']} |")
+lines += ["", "C1's row is the counter-barrier path: `lbp_pslot` runs C1 as one 8-CTA thread-block cluster "
+          "with the hardware cluster barrier (`tools/time_probe.py`: 0.352 ms), but ncu's kernel replay launches "
+          "it without the cluster attribute, and the kernel then takes the global-memory counter barrier (it "
+          "checks `%cluster_nctarank` against the grid)."]
 json.dump(l2, open(os.path.join(prof, "l2_traffic.json"), "w"), indent=1)
 open(os.path.join(prof, f"{pre}_bench_launches.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
