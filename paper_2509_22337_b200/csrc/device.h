@@ -122,6 +122,7 @@ struct hbp_plan {
   hbp::Phase *d_phases = nullptr;
   int *d_items = nullptr;
   int32_t *d_fitems = nullptr;  // fused levels (int4 lane records)
+  int32_t *d_iw = nullptr;  // per list item: its slot word and twin (int4, small phases)
   hbp_plan *unfused = nullptr;  // the same schedule without fused levels (underflow attribution)
   int grid = 1;
   const void *kernel = nullptr;  // executor instance (fused levels or not)
@@ -140,7 +141,7 @@ struct hbp_plan {
   int ev_ok = -1;
   ~hbp_plan() {
     cudaSetDevice(g->device);
-    for (void *p : {(void *)d_phases, (void *)d_items, (void *)d_fitems})
+    for (void *p : {(void *)d_phases, (void *)d_items, (void *)d_fitems, (void *)d_iw})
       if (p) cudaFree(p);
     delete unfused;
     if (d_sched) cudaFreeAsync(d_sched, g->stream);

@@ -69,6 +69,12 @@ constexpr int kPslotThreads = HBP_PSLOT_THREADS;
 #define HBP_ITEM_PRED 1
 #endif
 constexpr int kItemRow = 6;
+// small phases' list items carry their slot word and twin in a parallel
+// int4 array (plan time), loaded beside the item: C2 5.53 -> 5.34 ms, C3
+// 7.34 -> 7.19 ms (HBP_ITEM_WORDS=0: item -> slot word chain, A/B)
+#ifndef HBP_ITEM_WORDS
+#define HBP_ITEM_WORDS 1
+#endif
 // fused lanes: the factor kind selects operands instead of branching (no
 // divergence between a warp's AND and OR factors; the same operations):
 // C4-SEQFIX 18.14 -> 17.62 ms (HBP_FUSED_SEL=0: the branches, A/B)
@@ -140,6 +146,7 @@ struct KParams {
   int nphases;
   const int *items;
   const int4 *fitems;  // fused levels: two int4 per lane (layout.cpp emit_fused)
+  const int4 *iw;      // list items: {slot word x, slot word y, twin, 0} (small phases)
   // control
   Ctrl *ctrl;
   unsigned long long *delta_bits;  // [max_it + 2]
@@ -599,6 +606,19 @@ __device__ __forceinline__ void run_small(const KParams &P, const Phase *cache, 
       for (int i = start; i < n; i += stride) {
         const int4 *lr = P.fitems + 2 * (size_t)(b + i);
         fused_lane(P, __ldg(lr), __ldg(lr + 1), it, p, ufkey);
+      }
+    } else if (P.iw && type == 0) {
+      for (int i = start; i < n; i += stride) {
+        const int item = __ldg(P.items + b + i);
+        const int4 w = __ldg(P.iw + b + i);
+        v_item(P, item & (kWriteBit - 1), make_int2(w.x, w.y), (unsigned)w.z,
+               (item & kWriteBit) ? 1 : 0, false, it, p, unused, ufkey, false);
+      }
+    } else if (P.iw) {
+      for (int i = start; i < n; i += stride) {
+        const int q = __ldg(P.items + b + i);
+        const int4 w = __ldg(P.iw + b + i);
+        f_item(P, q, make_int2(w.x, w.y), w.z, p, ufkey);
       }
     } else if (type == 0) {
       for (int i = start; i < n; i += stride) {
@@ -1804,6 +1824,33 @@ static hbp_status plan_create(hbp_graph *g, int64_t k, const int64_t *s_off, con
   if ((st = upload(&p->d_phases, p->host.phases, s)) || (st = upload(&p->d_items, p->host.items, s)) ||
       (st = upload(&p->d_fitems, p->host.fitems, s)))
     return st;
+#if HBP_ITEM_WORDS
+  // the slot word and twin of every list item of a small phase, beside the
+  // item: the tight loop then loads both at once instead of item -> slot word
+  if (!parall) {
+    const hbp::HostLayout &L = g->L;
+    std::vector<int32_t> iw(4 * std::max<size_t>(1, p->host.items.size()), 0);
+    bool any = false;
+    for (const auto &ph : p->host.phases) {
+      if (ph.list != 1 || ph.grid || (ph.type != 0 && ph.type != 1)) continue;
+      for (int32_t i = ph.begin; i < ph.end; ++i) {
+        const int32_t q = p->host.items[i] & (hbp::kWriteBit - 1);
+        int32_t *w = &iw[4 * (size_t)i];
+        if (ph.type == 0) {
+          w[0] = L.vslot[2 * (size_t)q];
+          w[1] = L.vslot[2 * (size_t)q + 1];
+          w[2] = (int32_t)L.ftov_twin[q];
+        } else {
+          w[0] = L.fslot[2 * (size_t)q];
+          w[1] = L.fslot[2 * (size_t)q + 1];
+          w[2] = L.vtof_twin[q];
+        }
+        any = true;
+      }
+    }
+    if (any && (st = upload(&p->d_iw, iw, s))) return st;
+  }
+#endif
   // keep the schedule in its reference order for the underflow attribution
   // (a PARALL-shape batch is already on the device: the shape test's copy)
   {
@@ -2031,6 +2078,7 @@ static hbp_status launch_run(hbp_plan *p, const hbp_options *opt, hbp_result *re
   P.nphases = (int)p->host.phases.size();
   P.items = p->d_items;
   P.fitems = (const int4 *)p->d_fitems;
+  P.iw = (const int4 *)p->d_iw;
   P.ctrl = c.ctrl;
   P.delta_bits = c.delta_bits;
   P.uf_msg = c.uf_msg;
