@@ -567,6 +567,36 @@ def test_level_fusion_bitwise_identical_to_two_phase(monkeypatch):
     P.engine.clear_device_cache()
 
 
+def test_small_levels_on_a_cluster_bitwise(monkeypatch):
+    """HBP_CSIZE=2/4 runs the small levels on a thread-block cluster of that
+    many CTAs (cluster barrier between them) instead of CTA 0 alone: same bits,
+    iterations and deltas (fused and unfused plans)."""
+    rng = np.random.default_rng(99)
+    graphs = [W.graph("hedc")[0]] + [random_graph(rng, max_vars=40, max_factors=40, max_body=6)
+                                     for _ in range(6)]
+    for i, g in enumerate(graphs):
+        for mode in (1, 2, 3):
+            sched = _compile_any(rng, g, mode)
+            opts = EngineOptions(60, 1e-9)
+            for fuse in (None, "0"):
+                out = []
+                for cs in (None, "2", "4"):
+                    for k, v in (("HBP_CSIZE", cs), ("HBP_FUSE", fuse)):
+                        if v is None:
+                            monkeypatch.delenv(k, raising=False)
+                        else:
+                            monkeypatch.setenv(k, v)
+                    P.engine.clear_device_cache()
+                    out.append(P.run(g, sched, opts))
+                for got in out[1:]:
+                    assert got.iterations == out[0].iterations, (i, mode, fuse)
+                    assert got.marginals.tobytes() == out[0].marginals.tobytes(), (i, mode, fuse)
+                    assert np.asarray(got.deltas).tobytes() == np.asarray(out[0].deltas).tobytes()
+    monkeypatch.delenv("HBP_CSIZE", raising=False)
+    monkeypatch.delenv("HBP_FUSE", raising=False)
+    P.engine.clear_device_cache()
+
+
 def _pslot(g, sched):
     import ctypes as C
     f = P._native.lib().hbp_debug_plan_pslot
